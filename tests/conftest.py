@@ -1,0 +1,19 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libjtfs.so")
+    config.addinivalue_line("markers", "slow: long-running oracle computation")
+
+
+@pytest.fixture(scope="session")
+def lib():
+    from paper_2602_11896_b200 import _lib
+    return _lib.load()
