@@ -1,0 +1,154 @@
+/* jtfs.h — C ABI of libjtfs.so: B200-native joint time–frequency scattering (JTFS) forward
+ * transform, Euclidean feature loss, its gradient with respect to the audio samples, and the
+ * metamer descent step of arxiv 2602.11896 ("musical metamers").
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; Rk = reading k of DESIGN.md §2.
+ *
+ * Conventions for every entry point
+ *  - Return value: JTFS_OK (0) or an error code; on error `jtfs_last_error()` (thread-local)
+ *    names the violated constraint. No entry point aborts the process.
+ *  - A plan is immutable after `jtfs_plan` returns, except for its lazily uploaded device copy
+ *    (see jtfs_plan_prepare); concurrent calls with one plan on different streams and distinct
+ *    workspaces are safe once the plan is prepared on that device.
+ *  - "device pointer": memory of the current CUDA device, fp32, contiguous, 16-byte aligned,
+ *    owned by the caller. Work is enqueued on `stream` in order; no host synchronisation unless
+ *    stated (the *_host variants synchronise `stream` before returning).
+ *  - Results are deterministic (bitwise) for a fixed (plan, B, device, workspace size): no
+ *    floating-point atomics on any output path.
+ */
+#ifndef JTFS_H
+#define JTFS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct jtfs_plan_s* jtfs_plan_t;
+typedef struct CUstream_st* jtfs_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  JTFS_OK = 0,
+  JTFS_ERR_CONFIG = 1,  /* plan hyper-parameters violate a constraint */
+  JTFS_ERR_SIZE = 2,    /* B <= 0, workspace too small, misaligned or NULL pointer, bad cap */
+  JTFS_ERR_NUMERIC = 3, /* non-finite loss or gradient detected */
+  JTFS_ERR_CUDA = 4,    /* CUDA runtime error (message = cudaGetErrorString) */
+  JTFS_ERR_OOM = 5,     /* host or device allocation failed */
+  JTFS_ERR_STATE = 6    /* invalid handle / state */
+} jtfs_status;
+
+/* ---------------------------------------------------------------------------------------
+ * Plan (host, float64). Builds the three filterbanks of P:157-193 (generator P:167-191, readings
+ * R1-R3), the Morlet responses with the κ correction of Eq.1 (R4-R5), the Gaussian
+ * low-pass φ_T / φ_F (R6), padding (R10), the frequential grid P (= phi['N'],
+ * P:276, R11), the admissible width-first blocks, and the path table in the
+ * yield order of P:314-351 (R15). Q2 = 1 (R7).
+ *  N     signal length (samples), multiple of T
+ *  J,Q   first-layer scale and quality factor (J >= 1, Q >= 1)
+ *  J_fr,Q_fr frequential scale and quality factor (>= 1)
+ *  T,F   time / log-frequency averaging widths, powers of two, 1 <= log2 T <= J,
+ *        0 <= log2 F <= J_fr; N_pad (R10) must be <= 2^22; ceil(N1/F) <= 32 (GPU limit).
+ *  out   receives the handle; release with jtfs_plan_destroy.
+ * Errors: JTFS_ERR_CONFIG (constraint named), JTFS_ERR_OOM. Touches no GPU. */
+jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
+                      jtfs_plan_t* out);
+jtfs_status jtfs_plan_destroy(jtfs_plan_t plan); /* frees host and device copies */
+
+typedef struct {
+  int64_t N, N_pad, pad_left, P, frames, n_coef, n_paths;
+  int32_t N1, N2, N_fr, n_blocks, log2T, log2F;
+} jtfs_plan_info_t;
+/* N1 = #psi1, N2 = #psi2, N_fr = #frequential filters with xi > 0 (per spin), frames = N/T,
+ * n_coef = packed coefficients per signal (S0 first, then orders 1 and 2, R15). */
+jtfs_status jtfs_plan_info(jtfs_plan_t plan, jtfs_plan_info_t* info);
+
+typedef struct {
+  int32_t order, n2, n_fr, spin, j2, j_fr, rows, frames;
+  int64_t offset; /* first coefficient of this path in the packed vector */
+} jtfs_path_t;
+/* Path table in yield order: S0 (order 0), order 1 over [phi_F, psi+...],
+ * order 2 by admissible n2 ascending over [phi_F, psi+..., psi-...] (R12). Each path occupies
+ * rows*frames coefficients, row-major. `cap` = capacity of `out` in entries. */
+jtfs_status jtfs_plan_paths(jtfs_plan_t plan, jtfs_path_t* out, int64_t cap);
+
+/* Test hook: filter parameters of one bank. layer 0 = psi1, 1 = psi2, 2 = L_fr (R12 order:
+ * phi_F, psi+..., psi-...), 3 = phi_T, 4 = phi_F. Writes up to `cap` entries; returns the
+ * count through *count. */
+jtfs_status jtfs_plan_filters(jtfs_plan_t plan, int layer, double* xi, double* sigma, int32_t* j,
+                              int64_t cap, int64_t* count);
+
+/* Test hook: level-k Fourier response (float64, periodised, R4/R9) of filter `idx` of `layer`
+ * on a grid of L0 >> k bins (L0 = N_pad for layers 0,1,3 and P for 2,4), written to out[cap]. */
+jtfs_status jtfs_plan_response(jtfs_plan_t plan, int layer, int idx, int k, double* out,
+                               int64_t cap);
+
+/* Uploads the plan's device tables (filter spectra, row kernels, twiddles) to the current device
+ * on `stream` and synchronises. Called implicitly by the first compute call; call it explicitly
+ * to keep the upload out of timed regions. */
+jtfs_status jtfs_plan_prepare(jtfs_plan_t plan, jtfs_stream_t stream);
+
+/* Workspace bytes for `batch` signals processed at once (with_grad = 1 for jtfs_loss_grad and
+ * metamer_step). It is affine in batch: fixed + batch * per_signal. A compute call processes its
+ * B signals in micro-batches of floor((ws_bytes - fixed) / per_signal) signals. */
+size_t jtfs_workspace_size(jtfs_plan_t plan, int64_t batch, int with_grad);
+
+/* ---------------------------------------------------------------------------------------
+ * Forward (Eq.2-4 with R14 averaging). x [B][N] device fp32 signals; S [B][n_coef]
+ * device fp32 packed coefficients (R15, unpadded R16). ws: device workspace of ws_bytes. */
+jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* S, void* ws,
+                         size_t ws_bytes, jtfs_stream_t stream);
+
+/* Loss and gradient (R19-R22). For each signal b:
+ *   loss[b] = 1/2 sum_{orders 1,2} (S(y_b) - S_target_b)^2   (S0 excluded, R19)
+ *   grad[b] = dE_b/dy_b, the TRUE gradient (the paper's "grad E" is its negative, R23).
+ * y [B][N], S_target [B][n_coef], loss [B], grad [B][N]: device fp32.
+ * shard/n_shards: second-order path shard (0,1 = whole). With n_shards > 1 the call computes the
+ * contribution of order-2 units with (unit index mod n_shards) == shard, plus (shard 0 only)
+ * order 1; summing loss and grad over shards (e.g. NCCL allreduce) gives the full result. */
+jtfs_status jtfs_loss_grad(jtfs_plan_t plan, const float* y, const float* S_target, int64_t B,
+                           float* loss, float* grad, int shard, int n_shards, void* ws,
+                           size_t ws_bytes, jtfs_stream_t stream);
+
+/* Metamer state (R23-R24); all device pointers, caller-owned:
+ *  y, u, y_prev, g_prev [B][N]; mu, loss_prev [B] (loss_prev = +inf before the first step);
+ *  accepted [B] int32 output flag; loss [B] output (loss at the y evaluated this step). */
+typedef struct {
+  float *y, *u, *y_prev, *g_prev, *mu, *loss_prev, *loss;
+  int32_t* accepted;
+  int64_t iter; /* incremented by each call (host field) */
+} jtfs_metamer_state;
+
+/* One descent trial, entirely stream-ordered (no host sync): E, g = jtfs_loss_grad(y); per
+ * signal accept if E <= loss_prev (then y_prev=y, g_prev=g, loss_prev=E, mu*=grow) else reject
+ * (y=y_prev, g=g_prev, u=0, mu*=shrink); then u = momentum*u - mu*g; y = y + u.
+ * Paper defaults: momentum 0.9, mu0 0.1; grow 1.1, shrink 0.5 (R24). */
+jtfs_status metamer_step(jtfs_plan_t plan, jtfs_metamer_state* st, const float* S_target,
+                         int64_t B, float momentum, float grow, float shrink, void* ws,
+                         size_t ws_bytes, jtfs_stream_t stream);
+
+/* End-to-end variants with HOST buffers (pinned or pageable): copy inputs host->device, run, copy
+ * results device->host, synchronise `stream`. The library allocates device staging of the given
+ * sizes inside ws (ws_bytes must include jtfs_host_staging_size). */
+size_t jtfs_host_staging_size(jtfs_plan_t plan, int64_t B, int with_grad);
+jtfs_status jtfs_loss_grad_host(jtfs_plan_t plan, const float* y_host, const float* S_target_host,
+                                int64_t B, float* loss_host, float* grad_host, void* ws,
+                                size_t ws_bytes, jtfs_stream_t stream);
+
+/* Thread-local message of the last error ("" if none). */
+const char* jtfs_last_error(void);
+
+/* Test-only: run the forward of one micro-batch and copy an intermediate stage to out:
+ *  stage 1 = U1 (|Z1|, [B][sum_n1 N_pad>>k1] fp32), 2 = S1t ([B][N1][N_pad/T] fp32),
+ *  3 = Y2 ([B][sum_blocks n1_max*T2] complex64 interleaved), 4 = S ([B][n_coef]). */
+jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_t B, void* out,
+                             size_t out_bytes, void* ws, size_t ws_bytes, jtfs_stream_t stream);
+
+/* Number of kernels the library has launched in this process (for launch-count reporting). */
+int64_t jtfs_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JTFS_H */

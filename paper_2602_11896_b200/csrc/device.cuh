@@ -1,0 +1,94 @@
+// device.cuh — device copies of the plan tables and the kernel launchers (kernels_*.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "plan.h"
+
+namespace jtfs {
+
+struct DeviceTables {
+  float* spec_vals = nullptr;
+  GatherJob* l1_jobs = nullptr;     int64_t* l1_tiles = nullptr;   int n_l1 = 0;   int64_t l1_ntiles = 0;
+  GatherJob* s1_jobs = nullptr;     int64_t* s1_tiles = nullptr;   int n_s1 = 0;   int64_t s1_ntiles = 0;
+  GatherJob* l2_jobs = nullptr;     int64_t* l2_tiles = nullptr;   int n_l2 = 0;   int64_t l2_ntiles = 0;
+  GatherJob* s0_job = nullptr;      int64_t* s0_tiles = nullptr;   int64_t s0_ntiles = 0;
+  Support* psi1_sup = nullptr;
+  Support* psi2_sup = nullptr;      // [n_blocks][log2T+1]
+  Support* phiT_sup = nullptr;      // [log2T+1]
+  float2* hfr = nullptr;            // [n_fr][P]
+  float* phiF_k = nullptr;          int64_t* phiF_off = nullptr;
+  float* phiT_half = nullptr;       int64_t* phiT_off = nullptr;   int64_t* phiT_H = nullptr;
+  JointUnit* units = nullptr;       int n_units = 0;
+  BlockInfo* binfo = nullptr;       int n_blocks = 0;
+  // forward unit lists per rows_out class KAP in {1,2,4,8,16,32}: unit indices + tile prefix
+  int32_t* fwd_ulist[6] = {};       int64_t* fwd_tiles[6] = {};    int fwd_n[6] = {};  int64_t fwd_ntiles[6] = {};
+  int32_t* kf_of = nullptr;         // [n_fr] k_f per frequential filter
+  int32_t* blk_nmax = nullptr;      // [n_blocks]
+  int64_t* ucoef = nullptr;         // [n_units] coefficient offset of the unit's path - o2_start
+  int64_t* uo = nullptr;            // [n_units] o_off
+  int64_t o2_start = 0, n_o2 = 0;
+  int maxLf = 0, max_rows_out = 0;
+  int64_t* bwd_tiles = nullptr;     int64_t bwd_ntiles = 0;        // prefix over blocks of (col tiles x n ranges)
+  int32_t* coef_path = nullptr;     // [n_coef]
+  int32_t* path_owner_unit = nullptr;  // [n_paths]: -2 order 0, -1 order 1, else unit index
+  int64_t* l1_off = nullptr;        int32_t* n1_k1 = nullptr;      // per n1 offsets, k1
+  int64_t* u1adj_tiles = nullptr;   int64_t u1adj_ntiles = 0;      // prefix over n1 of L1 tiles
+  int32_t* gx_tile_start = nullptr; int32_t* gx_list = nullptr;
+  int64_t* o1_rlo = nullptr;        int64_t* o1_nrows = nullptr;
+  float2* tw = nullptr;
+  int Kmax = 0;
+};
+
+constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels
+constexpr int kJC = 64;            // joint stage: columns per CTA
+constexpr int kJR = 64;            // joint stage: rows per chunk
+constexpr int kJN = 64;            // joint backward: n1 rows per CTA
+
+// ---- kernels_time.cu
+void launch_reflect_pad(const float* x, int64_t sx, float2* xp, const Plan& p, int B, cudaStream_t st);
+void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
+                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
+void launch_modulus(const float2* z, int64_t zsb, float2* u, int64_t usb, int64_t n_per_b, int B,
+                    cudaStream_t st);
+void launch_real_rows(const float2* in, int64_t in_sb, int64_t in_off, float* out, int64_t out_sb,
+                      int64_t out_off, int64_t n, int B, cudaStream_t st);
+void launch_s0_out(const float2* s0c, int64_t s0_sb, float* S, int64_t S_sb, const Plan& p, int B,
+                   cudaStream_t st);
+void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS, int64_t GS_sb,
+                          const float2* GY, int64_t GY_sb, float2* out, int64_t out_sb, int B,
+                          cudaStream_t st);
+void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
+                      int B, cudaStream_t st);
+void launch_adj_gather_x(const Plan& p, const DeviceTables& d, const float2* GZ, int64_t GZ_sb, float2* out,
+                         int64_t out_sb, int B, cudaStream_t st);
+void launch_real_to_complex(const float* in, int64_t in_sb, float2* out, int64_t out_sb, int64_t n, int B,
+                            cudaStream_t st);
+void launch_reflect_adj(const float2* gxp, int64_t sxp, float* g, int64_t sg, const Plan& p, int B,
+                        cudaStream_t st);
+void launch_metamer(float* y, float* u, float* y_prev, float* g_prev, float* mu, float* loss_prev,
+                    const float* loss, int32_t* accepted, const float* g, int64_t sg, int64_t N, int B,
+                    float momentum, float grow, float shrink, cudaStream_t st);
+
+// ---- kernels_fr.cu
+void launch_o1_fwd(const Plan& p, const DeviceTables& d, const float* S1t, int64_t S1t_sb, float2* W1,
+                   int64_t W1_sb, float* V2, int64_t V2_sb, float* S, int64_t S_sb, int B, cudaStream_t st);
+void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float2* W1,
+                   int64_t W1_sb, float* V2, int64_t V2_sb, const float* S1t, int64_t S1t_sb, float* gS1t,
+                   int64_t gS1t_sb, int B, cudaStream_t st);
+void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
+                      int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
+void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,
+                     int64_t S_sb, int shard, int n_shards, int B, cudaStream_t st);
+void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S_sb, const float* St,
+                 int64_t St_sb, float* r, int64_t r_sb, float* loss, int shard, int n_shards, int B,
+                 cudaStream_t st);
+void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
+                     int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);
+void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
+                      int64_t go_sb, float2* gY2, int64_t gy_sb, int shard, int n_shards, int B,
+                      cudaStream_t st);
+
+}  // namespace jtfs

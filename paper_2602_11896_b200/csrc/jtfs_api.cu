@@ -1,0 +1,577 @@
+// jtfs_api.cu — C ABI of libjtfs.so (include/jtfs.h): plan handles, device-table upload, workspace
+// layout, and the stream-ordered orchestration of the forward, loss + gradient
+// and metamer step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "fft.cuh"
+
+namespace jtfs {
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+}  // namespace jtfs
+
+using namespace jtfs;
+
+struct jtfs_plan_s {
+  Plan p;
+  std::mutex mu;
+};
+
+static thread_local std::string t_err;
+static jtfs_status fail(jtfs_status s, const std::string& m) {
+  t_err = m;
+  return s;
+}
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) return fail(JTFS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------------------------ device tables
+template <class T>
+static cudaError_t up(const std::vector<T>& v, T** dst) {
+  *dst = nullptr;
+  if (v.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc(dst, v.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+static std::vector<int64_t> prefix(const std::vector<int64_t>& counts) {
+  std::vector<int64_t> t(counts.size() + 1, 0);
+  for (size_t i = 0; i < counts.size(); ++i) t[i + 1] = t[i] + counts[i];
+  return t;
+}
+
+static void free_tables(DeviceTables* d) {
+  if (!d) return;
+  void* ptrs[] = {d->spec_vals, d->l1_jobs, d->l1_tiles, d->s1_jobs, d->s1_tiles, d->l2_jobs, d->l2_tiles,
+                  d->s0_job, d->s0_tiles, d->psi1_sup, d->psi2_sup, d->phiT_sup, d->hfr, d->phiF_k,
+                  d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
+                  d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_owner_unit, d->l1_off,
+                  d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (int c = 0; c < 6; ++c) {
+    if (d->fwd_ulist[c]) cudaFree(d->fwd_ulist[c]);
+    if (d->fwd_tiles[c]) cudaFree(d->fwd_tiles[c]);
+  }
+  delete d;
+}
+
+jtfs::Plan::~Plan() { free_tables(dev); }
+
+static cudaError_t upload(Plan& p) {
+  DeviceTables* d = new DeviceTables();
+  cudaError_t e;
+#define UP(v, f) \
+  if ((e = up(v, &d->f)) != cudaSuccess) { free_tables(d); return e; }
+  UP(p.spec_vals, spec_vals);
+  auto job_tiles = [](const std::vector<GatherJob>& jobs) {
+    std::vector<int64_t> c;
+    for (auto& j : jobs) c.push_back((j.L_out + kGatherTile - 1) / kGatherTile);
+    return prefix(c);
+  };
+  std::vector<int64_t> t;
+  UP(p.l1_jobs, l1_jobs); t = job_tiles(p.l1_jobs); UP(t, l1_tiles);
+  d->n_l1 = (int)p.l1_jobs.size(); d->l1_ntiles = t.back();
+  UP(p.s1_jobs, s1_jobs); t = job_tiles(p.s1_jobs); UP(t, s1_tiles);
+  d->n_s1 = (int)p.s1_jobs.size(); d->s1_ntiles = t.back();
+  UP(p.l2_jobs, l2_jobs); t = job_tiles(p.l2_jobs); UP(t, l2_tiles);
+  d->n_l2 = (int)p.l2_jobs.size(); d->l2_ntiles = t.back();
+  std::vector<GatherJob> s0{p.s0_job};
+  UP(s0, s0_job); t = job_tiles(s0); UP(t, s0_tiles); d->s0_ntiles = t.back();
+  UP(p.psi1_sup, psi1_sup);
+  UP(p.psi2_sup, psi2_sup);
+  UP(p.phiT_sup, phiT_sup);
+  {
+    std::vector<float2> h(p.hfr.size() / 2);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = make_float2(p.hfr[2 * i], p.hfr[2 * i + 1]);
+    UP(h, hfr);
+  }
+  UP(p.phiF_k, phiF_k); UP(p.phiF_off, phiF_off);
+  UP(p.phiT_half, phiT_half); UP(p.phiT_off, phiT_off); UP(p.phiT_H, phiT_H);
+  UP(p.units, units); d->n_units = (int)p.units.size();
+  UP(p.binfo, binfo); d->n_blocks = (int)p.binfo.size();
+  // forward unit lists per KAP class
+  const int kaps[6] = {1, 2, 4, 8, 16, 32};
+  for (int c = 0; c < 6; ++c) {
+    std::vector<int32_t> ul;
+    std::vector<int64_t> cnt;
+    for (size_t u = 0; u < p.units.size(); ++u) {
+      int ro = p.units[u].rows_out;
+      int cls = 0;
+      while (kaps[cls] < ro) ++cls;
+      if (cls != c) continue;
+      ul.push_back((int32_t)u);
+      cnt.push_back((p.binfo[p.units[u].bi].n_cols + kJC - 1) / kJC);
+    }
+    d->fwd_n[c] = (int)ul.size();
+    if (!ul.empty()) {
+      t = prefix(cnt);
+      UP(ul, fwd_ulist[c]);
+      UP(t, fwd_tiles[c]);
+      d->fwd_ntiles[c] = t.back();
+    }
+  }
+  std::vector<int32_t> kf;
+  for (auto& f : p.L_fr) kf.push_back(std::min(f.j, p.log2F));
+  UP(kf, kf_of);
+  std::vector<int32_t> nm;
+  std::vector<int64_t> bt;
+  d->Kmax = 0;
+  for (size_t bi = 0; bi < p.blocks.size(); ++bi) {
+    nm.push_back(p.blocks[bi].n1_max);
+    d->Kmax = std::max(d->Kmax, p.blocks[bi].n1_max);
+    int64_t ntc = (p.binfo[bi].n_cols + kJC - 1) / kJC;
+    int64_t nr = (p.blocks[bi].n1_max + kJN - 1) / kJN;
+    bt.push_back(ntc * nr);
+  }
+  UP(nm, blk_nmax);
+  t = prefix(bt); UP(t, bwd_tiles); d->bwd_ntiles = t.back();
+  const int nfr1 = 1 + (int)p.psi_fr_plus.size();
+  d->o2_start = p.units.empty() ? p.n_coef : p.paths[1 + nfr1].offset;
+  d->n_o2 = p.n_coef - d->o2_start;
+  std::vector<int64_t> uc, uo;
+  for (auto& u : p.units) { uc.push_back(p.paths[u.path].offset - d->o2_start); uo.push_back(u.o_off); }
+  UP(uc, ucoef); UP(uo, uo);
+  std::vector<int32_t> cp(p.n_coef), pu(p.paths.size());
+  for (size_t q = 0; q < p.paths.size(); ++q) {
+    auto& pa = p.paths[q];
+    for (int64_t i = 0; i < (int64_t)pa.rows * pa.frames; ++i) cp[pa.offset + i] = (int32_t)q;
+    pu[q] = pa.order == 0 ? -2 : (pa.order == 1 ? -1 : (int32_t)(q - 1 - nfr1));
+  }
+  UP(cp, coef_path); UP(pu, path_owner_unit);
+  UP(p.L1_off, l1_off);
+  std::vector<int32_t> k1;
+  std::vector<int64_t> ut;
+  for (size_t n = 0; n < p.psi1.size(); ++n) {
+    k1.push_back(std::min(p.psi1[n].j, p.log2T));
+    ut.push_back((p.L1[n] + 255) / 256);
+  }
+  UP(k1, n1_k1);
+  t = prefix(ut); UP(t, u1adj_tiles); d->u1adj_ntiles = t.back();
+  UP(p.gx_tile_start, gx_tile_start); UP(p.gx_list, gx_list);
+  UP(p.o1_rlo, o1_rlo); UP(p.o1_nrows, o1_nrows);
+  std::vector<float2> tw = fft_twiddle_table();
+  UP(tw, tw);
+  d->maxLf = (int)p.P;
+#undef UP
+  p.dev = d;
+  return cudaSuccess;
+}
+
+static jtfs_status ensure_device(jtfs_plan_s* h) {
+  int dev = -1;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->p.dev) {
+    if (h->p.dev_id != dev) return fail(JTFS_ERR_STATE, "plan was prepared on another device");
+    return JTFS_OK;
+  }
+  CK(upload(h->p));
+  h->p.dev_id = dev;
+  return JTFS_OK;
+}
+
+// ------------------------------------------------------------------------------ workspace layout
+struct Layout {
+  // per-signal sizes in bytes (each 256-aligned) of every buffer, in this order
+  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss;
+  size_t per_signal() const { return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss; }
+};
+static size_t al(size_t b) { return (b + 255) / 256 * 256; }
+static Layout layout(const Plan& p, int with_grad) {
+  Layout L{};
+  const int64_t nfr1 = 1 + (int64_t)p.psi_fr_plus.size();
+  const int64_t N1 = (int64_t)p.psi1.size();
+  L.xp = al(p.N_pad * 8); L.Xh = al(p.N_pad * 8);
+  L.A = al(std::max(p.sumL1, p.sumY2) * 8);
+  L.Z1 = al(p.sumL1 * 8); L.U1h = al(p.sumL1 * 8); L.Y2 = al(std::max<int64_t>(p.sumY2, 1) * 8);
+  L.cs = al((1 + N1) * p.Ft * 8); L.ct = L.cs;
+  L.S1t = al(N1 * p.Ft * 4);
+  L.W1 = al(nfr1 * p.P * p.Ft * 8);
+  L.V2 = al(nfr1 * p.P * p.frames * 4);
+  L.o = al(std::max<int64_t>(p.o_size, 1) * 4);
+  L.S = al(p.n_coef * 4); L.r = al(p.n_coef * 4);
+  L.gS1t = al(N1 * p.Ft * 4);
+  L.g = with_grad ? al(p.N * 4) : 0;
+  L.loss = 256;
+  return L;
+}
+
+struct Bufs {
+  float2 *xp, *Xh, *A, *Z1, *U1h, *Y2, *cs, *ct, *W1;
+  float *S1t, *V2, *o, *S, *r, *gS1t, *g, *loss;
+  // per-signal strides in elements
+  int64_t s_xp, s_A, s_L1, s_Y2, s_c, s_S1t, s_W1, s_V2, s_o, s_S, s_g;
+};
+static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
+  Bufs b{};
+  char* q = base;
+  auto take = [&](size_t per) { char* r = q; q += per * mb; return r; };
+  b.xp = (float2*)take(L.xp); b.Xh = (float2*)take(L.Xh); b.A = (float2*)take(L.A); b.Z1 = (float2*)take(L.Z1);
+  b.U1h = (float2*)take(L.U1h); b.Y2 = (float2*)take(L.Y2); b.cs = (float2*)take(L.cs); b.ct = (float2*)take(L.ct);
+  b.S1t = (float*)take(L.S1t); b.W1 = (float2*)take(L.W1); b.V2 = (float*)take(L.V2); b.o = (float*)take(L.o);
+  b.S = (float*)take(L.S); b.r = (float*)take(L.r); b.gS1t = (float*)take(L.gS1t); b.g = (float*)take(L.g);
+  b.loss = (float*)take(L.loss);
+  b.s_xp = L.xp / 8; b.s_A = L.A / 8; b.s_L1 = L.Z1 / 8; b.s_Y2 = L.Y2 / 8; b.s_c = L.cs / 8;
+  b.s_S1t = L.S1t / 4; b.s_W1 = L.W1 / 8; b.s_V2 = L.V2 / 4; b.s_o = L.o / 4; b.s_S = L.S / 4; b.s_g = L.g / 4;
+  (void)p;
+  return b;
+}
+
+static cudaError_t fft_rows(const Plan& p, const float2* in, int64_t in_sb, float2* out, int64_t out_sb,
+                            int64_t off, int64_t count, int64_t L, int B, bool inv, cudaStream_t st) {
+  Rows ri{in_sb, off, count, L}, ro{out_sb, off, count, L};
+  return fft_launch(in, out, ri, ro, B, inv, p.dev->tw, st);
+}
+
+// Forward of one micro-batch. stop: 0 = full; 1 = after U1 (in A); 2 = after S1t; 3 = after Y2.
+static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb, float* S, int64_t S_sb,
+                               const Bufs& w, int shard, int n_shards, cudaStream_t st, int stop = 0) {
+  const DeviceTables& d = *p.dev;
+  cudaError_t e;
+#define RET() if ((e = cudaGetLastError()) != cudaSuccess) return e
+  // A1: reflect pad + FFT
+  launch_reflect_pad(x, sx, w.xp, p, mb, st);
+  if ((e = fft_rows(p, w.xp, w.s_xp, w.Xh, w.s_xp, 0, 1, p.N_pad, mb, false, st))) return e;
+  // A2: layer 1: cdgmm + subsample_fourier, ifft, modulus, fft
+  launch_gather(w.Xh, w.s_xp, w.A, w.s_A, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals, mb, st);
+  for (auto& g : p.l1_groups)
+    if ((e = fft_rows(p, w.A, w.s_A, w.Z1, w.s_L1, g.off, g.count, g.L, mb, true, st))) return e;
+  launch_modulus(w.Z1, w.s_L1, w.A, w.s_A, p.sumL1, mb, st);  // A rows use the L1 layout
+  RET();
+  if (stop == 1) return cudaSuccess;
+  for (auto& g : p.l1_groups) {
+    Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_L1, g.off, g.count, g.L};
+    if ((e = fft_launch(w.A, w.U1h, ri, ro, mb, false, d.tw, st))) return e;
+  }
+  // S0 and S1 time averages (Eq.3 time part)
+  launch_gather(w.Xh, w.s_xp, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
+  launch_gather(w.U1h, w.s_L1, w.cs + p.Ft, w.s_c, d.s1_jobs, d.s1_tiles, d.n_s1, d.s1_ntiles, d.spec_vals, mb, st);
+  if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, 1 + (int64_t)p.psi1.size(), p.Ft, mb, true, st))) return e;
+  launch_s0_out(w.ct, w.s_c, S, S_sb, p, mb, st);
+  launch_real_rows(w.ct, w.s_c, p.Ft, w.S1t, w.s_S1t, 0, (int64_t)p.psi1.size() * p.Ft, mb, st);
+  RET();
+  if (stop == 2) return cudaSuccess;
+  // A3: order-1 frequential scattering (shard 0 only)
+  if (shard == 0) launch_o1_fwd(p, d, w.S1t, w.s_S1t, w.W1, w.s_W1, w.V2, w.s_V2, S, S_sb, mb, st);
+  // A4: layer 2, width-first
+  if (!p.blocks.empty()) {
+    launch_gather(w.U1h, w.s_L1, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st);
+    for (auto& g : p.y2_groups) {
+      Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
+      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, true, d.tw, st))) return e;
+    }
+    RET();
+    if (stop == 3) return cudaSuccess;
+    // A5: joint lambda_1 stage + phi_F; A6: phi_T
+    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
+    launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, shard, n_shards, mb, st);
+  }
+  RET();
+  return cudaSuccess;
+}
+
+// Backward of one micro-batch (after run_forward + loss): r in w.r -> grad [mb][N] (stride sg)
+static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64_t sg, int mb, int shard,
+                                int n_shards, cudaStream_t st) {
+  const DeviceTables& d = *p.dev;
+  cudaError_t e;
+  const int64_t N1 = (int64_t)p.psi1.size();
+  if (!p.blocks.empty()) {
+    // A7: phi_T adjoint (r -> g_o, reusing o), joint adjoint (-> g_Y2 in A)
+    launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, shard, n_shards, mb, st);
+    if ((e = cudaMemsetAsync(w.A, 0, (size_t)w.s_A * 8 * mb, st))) return e;
+    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, shard, n_shards, mb, st);
+    // FFT of g_Y2 rows -> G_Y (into Y2)
+    for (auto& g : p.y2_groups) {
+      Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
+      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, false, d.tw, st))) return e;
+    }
+  }
+  // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)
+  launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, mb, st);
+  launch_real_to_complex(w.gS1t, w.s_S1t, w.cs, w.s_c, N1 * p.Ft, mb, st);
+  if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, N1, p.Ft, mb, false, st))) return e;
+  // A8: g_hat_U1 -> U1h ; g_U1 = Re IFFT -> A
+  launch_adj_gather_u1(p, d, w.ct, w.s_c, w.Y2, w.s_Y2, w.U1h, w.s_L1, mb, st);
+  for (auto& g : p.l1_groups) {
+    Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
+    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, true, d.tw, st))) return e;
+  }
+  // A9: modulus adjoint, FFT, layer-1 adjoint gather, IFFT, reflect adjoint
+  launch_phase_mul(w.Z1, w.A, w.s_A, w.U1h, p.sumL1, w.s_L1, mb, st);  // Z1, U1h share the L1 stride
+  for (auto& g : p.l1_groups) {
+    Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
+    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, false, d.tw, st))) return e;
+  }
+  launch_adj_gather_x(p, d, w.A, w.s_A, w.Xh, w.s_xp, mb, st);
+  if ((e = fft_rows(p, w.Xh, w.s_xp, w.xp, w.s_xp, 0, 1, p.N_pad, mb, true, st))) return e;
+  launch_reflect_adj(w.xp, w.s_xp, grad, sg, p, mb, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ ABI
+extern "C" {
+
+const char* jtfs_last_error(void) { return t_err.c_str(); }
+int64_t jtfs_launch_count(void) { return jtfs::g_launches.load(); }
+
+jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, jtfs_plan_t* out) {
+  if (!out) return fail(JTFS_ERR_SIZE, "out is NULL");
+  *out = nullptr;
+  jtfs_plan_s* h = new (std::nothrow) jtfs_plan_s();
+  if (!h) return fail(JTFS_ERR_OOM, "host allocation failed");
+  std::string err;
+  int rc;
+  try {
+    rc = make_plan(N, J, Q, J_fr, Q_fr, T, F, &h->p, &err);
+  } catch (const std::bad_alloc&) {
+    delete h;
+    return fail(JTFS_ERR_OOM, "host allocation failed");
+  }
+  if (rc) {
+    delete h;
+    return fail(JTFS_ERR_CONFIG, err);
+  }
+  *out = h;
+  t_err.clear();
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_destroy(jtfs_plan_t plan) {
+  if (!plan) return fail(JTFS_ERR_STATE, "NULL plan");
+  delete plan;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_info(jtfs_plan_t plan, jtfs_plan_info_t* info) {
+  if (!plan || !info) return fail(JTFS_ERR_STATE, "NULL argument");
+  const Plan& p = plan->p;
+  info->N = p.N; info->N_pad = p.N_pad; info->pad_left = p.pad_left; info->P = p.P; info->frames = p.frames;
+  info->n_coef = p.n_coef; info->n_paths = (int64_t)p.paths.size();
+  info->N1 = (int32_t)p.psi1.size(); info->N2 = (int32_t)p.psi2.size();
+  info->N_fr = (int32_t)p.psi_fr_plus.size(); info->n_blocks = (int32_t)p.blocks.size();
+  info->log2T = p.log2T; info->log2F = p.log2F;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_paths(jtfs_plan_t plan, jtfs_path_t* out, int64_t cap) {
+  if (!plan || !out) return fail(JTFS_ERR_STATE, "NULL argument");
+  if (cap < (int64_t)plan->p.paths.size()) return fail(JTFS_ERR_SIZE, "cap < n_paths");
+  std::memcpy(out, plan->p.paths.data(), plan->p.paths.size() * sizeof(jtfs_path_t));
+  return JTFS_OK;
+}
+
+static const std::vector<Filter>* bank(const Plan& p, int layer, std::vector<Filter>* tmp) {
+  switch (layer) {
+    case 0: return &p.psi1;
+    case 1: return &p.psi2;
+    case 2: return &p.L_fr;
+    case 3: tmp->assign(1, p.phiT); return tmp;
+    case 4: tmp->assign(1, p.phiF); return tmp;
+  }
+  return nullptr;
+}
+
+jtfs_status jtfs_plan_filters(jtfs_plan_t plan, int layer, double* xi, double* sigma, int32_t* j, int64_t cap,
+                              int64_t* count) {
+  if (!plan || !count) return fail(JTFS_ERR_STATE, "NULL argument");
+  std::vector<Filter> tmp;
+  auto* b = bank(plan->p, layer, &tmp);
+  if (!b) return fail(JTFS_ERR_SIZE, "layer must be 0..4");
+  *count = (int64_t)b->size();
+  for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)b->size()); ++i) {
+    if (xi) xi[i] = (*b)[i].xi;
+    if (sigma) sigma[i] = (*b)[i].sigma;
+    if (j) j[i] = (*b)[i].j;
+  }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_response(jtfs_plan_t plan, int layer, int idx, int k, double* out, int64_t cap) {
+  if (!plan || !out) return fail(JTFS_ERR_STATE, "NULL argument");
+  std::vector<Filter> tmp;
+  auto* b = bank(plan->p, layer, &tmp);
+  if (!b || idx < 0 || idx >= (int)b->size()) return fail(JTFS_ERR_SIZE, "bad layer/idx");
+  int64_t L0 = (layer == 2 || layer == 4) ? plan->p.P : plan->p.N_pad;
+  if (k < 0 || (L0 >> k) < 1 || cap < (L0 >> k)) return fail(JTFS_ERR_SIZE, "bad level or cap");
+  std::vector<double> v;
+  level_response((*b)[idx], L0, k, &v);
+  std::memcpy(out, v.data(), v.size() * sizeof(double));
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_prepare(jtfs_plan_t plan, jtfs_stream_t stream) {
+  if (!plan) return fail(JTFS_ERR_STATE, "NULL plan");
+  jtfs_status s = ensure_device(plan);
+  if (s) return s;
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return JTFS_OK;
+}
+
+size_t jtfs_workspace_size(jtfs_plan_t plan, int64_t batch, int with_grad) {
+  if (!plan || batch < 0) return 0;
+  return layout(plan->p, with_grad).per_signal() * (size_t)batch;
+}
+
+static jtfs_status check_common(jtfs_plan_t plan, int64_t B, size_t ws_bytes, int with_grad, void* ws, int* mb) {
+  if (!plan) return fail(JTFS_ERR_STATE, "NULL plan");
+  if (B <= 0) return fail(JTFS_ERR_SIZE, "B must be > 0");
+  if (!ws) return fail(JTFS_ERR_SIZE, "workspace is NULL");
+  if (((uintptr_t)ws) % 256) return fail(JTFS_ERR_SIZE, "workspace must be 256-byte aligned");
+  size_t per = layout(plan->p, with_grad).per_signal();
+  int64_t m = (int64_t)(ws_bytes / per);
+  if (m < 1) return fail(JTFS_ERR_SIZE, "workspace too small for one signal (need jtfs_workspace_size(plan,1,...))");
+  *mb = (int)std::min<int64_t>(m, B);
+  return ensure_device(plan);
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p % 16) == 0; }
+
+jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* S, void* ws, size_t ws_bytes,
+                         jtfs_stream_t stream) {
+  int mb;
+  jtfs_status s = check_common(plan, B, ws_bytes, 0, ws, &mb);
+  if (s) return s;
+  if (!x || !S || !aligned16(x) || !aligned16(S)) return fail(JTFS_ERR_SIZE, "x/S NULL or not 16-byte aligned");
+  const Plan& p = plan->p;
+  Layout L = layout(p, 0);
+  Bufs w = carve(p, L, (char*)ws, mb);
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    int n = (int)std::min<int64_t>(mb, B - b0);
+    CK(run_forward(p, x + b0 * p.N, p.N, n, S + b0 * p.n_coef, p.n_coef, w, 0, 1, (cudaStream_t)stream));
+  }
+  t_err.clear();
+  return JTFS_OK;
+}
+
+static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float* St, int64_t B, float* loss,
+                                  float* grad, int shard, int n_shards, void* ws, size_t ws_bytes, cudaStream_t st,
+                                  jtfs_metamer_state* mstate, float momentum, float grow, float shrink) {
+  int mb;
+  jtfs_status s = check_common(plan, B, ws_bytes, 1, ws, &mb);
+  if (s) return s;
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(JTFS_ERR_SIZE, "need 0 <= shard < n_shards");
+  const Plan& p = plan->p;
+  Layout L = layout(p, 1);
+  Bufs w = carve(p, L, (char*)ws, mb);
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    int n = (int)std::min<int64_t>(mb, B - b0);
+    CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, shard, n_shards, st));
+    float* lossp = mstate ? mstate->loss + b0 : loss + b0;
+    launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, shard, n_shards, n, st);
+    float* gp = mstate ? w.g : grad + b0 * p.N;
+    int64_t sg = mstate ? w.s_g : p.N;
+    CK(run_backward(p, w, gp, sg, n, shard, n_shards, st));
+    if (mstate) {
+      launch_metamer(mstate->y + b0 * p.N, mstate->u + b0 * p.N, mstate->y_prev + b0 * p.N,
+                     mstate->g_prev + b0 * p.N, mstate->mu + b0, mstate->loss_prev + b0, lossp,
+                     mstate->accepted + b0, gp, sg, p.N, n, momentum, grow, shrink, st);
+      CK(cudaGetLastError());
+    }
+  }
+  t_err.clear();
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_loss_grad(jtfs_plan_t plan, const float* y, const float* S_target, int64_t B, float* loss,
+                           float* grad, int shard, int n_shards, void* ws, size_t ws_bytes, jtfs_stream_t stream) {
+  if (!y || !S_target || !loss || !grad) return fail(JTFS_ERR_SIZE, "NULL data pointer");
+  if (!aligned16(y) || !aligned16(S_target) || !aligned16(grad))
+    return fail(JTFS_ERR_SIZE, "y/S_target/grad must be 16-byte aligned");
+  return loss_grad_impl(plan, y, S_target, B, loss, grad, shard, n_shards, ws, ws_bytes, (cudaStream_t)stream,
+                        nullptr, 0, 0, 0);
+}
+
+jtfs_status metamer_step(jtfs_plan_t plan, jtfs_metamer_state* st, const float* S_target, int64_t B,
+                         float momentum, float grow, float shrink, void* ws, size_t ws_bytes, jtfs_stream_t stream) {
+  if (!st || !st->y || !st->u || !st->y_prev || !st->g_prev || !st->mu || !st->loss_prev || !st->loss ||
+      !st->accepted || !S_target)
+    return fail(JTFS_ERR_SIZE, "NULL state or target pointer");
+  jtfs_status s = loss_grad_impl(plan, st->y, S_target, B, nullptr, nullptr, 0, 1, ws, ws_bytes,
+                                 (cudaStream_t)stream, st, momentum, grow, shrink);
+  if (s == JTFS_OK) st->iter += 1;
+  return s;
+}
+
+size_t jtfs_host_staging_size(jtfs_plan_t plan, int64_t B, int with_grad) {
+  if (!plan || B < 0) return 0;
+  const Plan& p = plan->p;
+  size_t s = al(B * p.N * 4) + al(B * p.n_coef * 4) + al(B * 4);
+  if (with_grad) s += al(B * p.N * 4);
+  return s;
+}
+
+jtfs_status jtfs_loss_grad_host(jtfs_plan_t plan, const float* y_host, const float* S_target_host, int64_t B,
+                                float* loss_host, float* grad_host, void* ws, size_t ws_bytes, jtfs_stream_t stream) {
+  if (!plan) return fail(JTFS_ERR_STATE, "NULL plan");
+  if (!y_host || !S_target_host || !loss_host || !grad_host) return fail(JTFS_ERR_SIZE, "NULL host pointer");
+  const Plan& p = plan->p;
+  size_t stg = jtfs_host_staging_size(plan, B, 1);
+  if (ws_bytes < stg) return fail(JTFS_ERR_SIZE, "workspace smaller than the host staging");
+  char* q = (char*)ws;
+  float* y = (float*)q; q += al(B * p.N * 4);
+  float* St = (float*)q; q += al(B * p.n_coef * 4);
+  float* loss = (float*)q; q += al(B * 4);
+  float* grad = (float*)q; q += al(B * p.N * 4);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(y, y_host, B * p.N * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(St, S_target_host, B * p.n_coef * 4, cudaMemcpyHostToDevice, st));
+  jtfs_status s = loss_grad_impl(plan, y, St, B, loss, grad, 0, 1, q, ws_bytes - stg, st, nullptr, 0, 0, 0);
+  if (s) return s;
+  CK(cudaMemcpyAsync(loss_host, loss, B * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(grad_host, grad, B * p.N * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_t B, void* out, size_t out_bytes,
+                             void* ws, size_t ws_bytes, jtfs_stream_t stream) {
+  int mb;
+  jtfs_status s = check_common(plan, B, ws_bytes, 0, ws, &mb);
+  if (s) return s;
+  if (mb < B) return fail(JTFS_ERR_SIZE, "debug stage needs the whole batch in one micro-batch");
+  const Plan& p = plan->p;
+  Layout L = layout(p, 0);
+  Bufs w = carve(p, L, (char*)ws, mb);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = (int)B;
+  if (stage == 1) {
+    if (out_bytes < (size_t)B * p.sumL1 * 4) return fail(JTFS_ERR_SIZE, "out too small");
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 1));
+    launch_real_rows(w.A, w.s_A, 0, (float*)out, p.sumL1, 0, p.sumL1, n, st);
+  } else if (stage == 2) {
+    int64_t per = (int64_t)p.psi1.size() * p.Ft;
+    if (out_bytes < (size_t)B * per * 4) return fail(JTFS_ERR_SIZE, "out too small");
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 2));
+    CK(cudaMemcpy2DAsync(out, per * 4, w.S1t, w.s_S1t * 4, per * 4, B, cudaMemcpyDeviceToDevice, st));
+  } else if (stage == 3) {
+    if (out_bytes < (size_t)B * p.sumY2 * 8) return fail(JTFS_ERR_SIZE, "out too small");
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 3));
+    if (p.sumY2 > 0)
+      CK(cudaMemcpy2DAsync(out, p.sumY2 * 8, w.Y2, w.s_Y2 * 8, p.sumY2 * 8, B, cudaMemcpyDeviceToDevice, st));
+  } else if (stage == 4) {
+    if (out_bytes < (size_t)B * p.n_coef * 4) return fail(JTFS_ERR_SIZE, "out too small");
+    CK(run_forward(p, x, p.N, n, (float*)out, p.n_coef, w, 0, 1, st, 0));
+  } else {
+    return fail(JTFS_ERR_SIZE, "stage must be 1..4");
+  }
+  CK(cudaGetLastError());
+  return JTFS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,325 @@
+// kernels_time.cu — time-axis stages of the JTFS path on sm_100a: padding, Fourier-domain
+// filtering + subsampling (cdgmm + subsample_fourier), modulus, and
+// the adjoints of those stages for the gradient; plus the metamer update.
+// All HBM-bound; coalesced along the contiguous time / frequency axis.
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace jtfs {
+
+__device__ __forceinline__ int64_t floor_div(int64_t a, int64_t b) {  // b > 0
+  return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+
+__device__ __forceinline__ int find_job(const int64_t* __restrict__ tiles, int n, int64_t t) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(tiles + mid) <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// R10 half-sample symmetric extension: xp[i] = x[e(i - pad_left)], e = 2N-periodic even extension.
+__global__ void k_reflect_pad(const float* __restrict__ x, int64_t sx, float2* __restrict__ xp, int64_t N,
+                              int64_t N_pad, int64_t pad_left) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N_pad) return;
+  int b = blockIdx.y;
+  int64_t t = (i - pad_left) % (2 * N);
+  if (t < 0) t += 2 * N;
+  int64_t src = t < N ? t : 2 * N - 1 - t;
+  xp[(int64_t)b * N_pad + i] = make_float2(__ldg(x + b * sx + src), 0.f);
+}
+
+void launch_reflect_pad(const float* x, int64_t sx, float2* xp, const Plan& p, int B, cudaStream_t st) {
+  dim3 g((unsigned)((p.N_pad + 255) / 256), (unsigned)B);
+  k_reflect_pad<<<g, 256, 0, st>>>(x, sx, xp, p.N, p.N_pad, p.pad_left);
+  count_launch();
+}
+
+// out[m] = scale * sum_{s in [lo, lo+len), s = m (mod L_out)} h[s-lo] * in[s mod L_in]
+// i.e. cdgmm with a support-limited real response, then subsample_fourier (fold-mean).
+__global__ void __launch_bounds__(kGatherTile) k_gather(const float2* __restrict__ in, int64_t in_sb,
+                                                         float2* __restrict__ out, int64_t out_sb,
+                                                         const GatherJob* __restrict__ jobs,
+                                                         const int64_t* __restrict__ tiles, int njobs,
+                                                         const float* __restrict__ vals) {
+  const int64_t tile = blockIdx.x;
+  const int b = blockIdx.y;
+  const int j = find_job(tiles, njobs, tile);
+  const GatherJob J = jobs[j];
+  const int64_t m = (tile - tiles[j]) * kGatherTile + threadIdx.x;
+  if (m >= J.L_out) return;
+  const float2* src = in + b * in_sb + J.in_off;
+  int64_t s = m - floor_div(m - J.lo, J.L_out) * J.L_out;  // smallest s >= lo with s = m mod L_out
+  float2 acc = make_float2(0.f, 0.f);
+  for (; s < J.lo + J.len; s += J.L_out) {
+    float h = __ldg(vals + J.val_off + (s - J.lo));
+    int64_t si = s % J.L_in;
+    if (si < 0) si += J.L_in;
+    float2 v = src[si];
+    acc.x = fmaf(h, v.x, acc.x);
+    acc.y = fmaf(h, v.y, acc.y);
+  }
+  out[b * out_sb + J.out_off + m] = cscale(acc, J.scale);
+}
+
+void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
+                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+  if (njobs <= 0 || ntiles <= 0) return;
+  dim3 g((unsigned)ntiles, (unsigned)B);
+  k_gather<<<g, kGatherTile, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
+  count_launch();
+}
+
+// U1 = |Z1|, stored as a complex row with zero imaginary part for the next FFT.
+__global__ void k_modulus(const float2* __restrict__ z, int64_t zsb, float2* __restrict__ u, int64_t usb,
+                          int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float2 v = z[blockIdx.y * zsb + i];
+  u[blockIdx.y * usb + i] = make_float2(sqrtf(v.x * v.x + v.y * v.y), 0.f);
+}
+
+void launch_modulus(const float2* z, int64_t zsb, float2* u, int64_t usb, int64_t n_per_b, int B,
+                    cudaStream_t st) {
+  dim3 g((unsigned)((n_per_b + 255) / 256), (unsigned)B);
+  k_modulus<<<g, 256, 0, st>>>(z, zsb, u, usb, n_per_b);
+  count_launch();
+}
+
+__global__ void k_real_rows(const float2* __restrict__ in, int64_t in_sb, int64_t in_off, float* __restrict__ out,
+                            int64_t out_sb, int64_t out_off, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[blockIdx.y * out_sb + out_off + i] = in[blockIdx.y * in_sb + in_off + i].x;
+}
+
+void launch_real_rows(const float2* in, int64_t in_sb, int64_t in_off, float* out, int64_t out_sb,
+                      int64_t out_off, int64_t n, int B, cudaStream_t st) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
+  k_real_rows<<<g, 256, 0, st>>>(in, in_sb, in_off, out, out_sb, out_off, n);
+  count_launch();
+}
+
+// S0 = phi_T * x_p at stride T, unpadded (R14, R16): path 0 of the packed vector.
+__global__ void k_s0_out(const float2* __restrict__ s0c, int64_t s0_sb, float* __restrict__ S, int64_t S_sb,
+                         int64_t m0, int64_t frames) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= frames) return;
+  S[blockIdx.y * S_sb + t] = s0c[blockIdx.y * s0_sb + m0 + t].x;
+}
+
+void launch_s0_out(const float2* s0c, int64_t s0_sb, float* S, int64_t S_sb, const Plan& p, int B,
+                   cudaStream_t st) {
+  dim3 g((unsigned)((p.frames + 255) / 256), (unsigned)B);
+  k_s0_out<<<g, 256, 0, st>>>(s0c, s0_sb, S, S_sb, p.pad_left / p.T, p.frames);
+  count_launch();
+}
+
+// Adjoint of layer 2 and of the S1 time average, in Fourier (R21: responses are real, so the
+// adjoint of "multiply + fold-mean + IFFT" is "FFT + periodic extension + multiply"):
+//   g_hat_U1[n1][m] = phiT_k1[m] GS[n1][m mod Ft] + sum_{blocks with n1 < n1_max} psi2_k1[m] GY[n1][m mod T2]
+__global__ void __launch_bounds__(256) k_adj_gather_u1(
+    const float2* __restrict__ GS, int64_t GS_sb, const float2* __restrict__ GY, int64_t GY_sb,
+    float2* __restrict__ out, int64_t out_sb, const int64_t* __restrict__ tiles, int N1,
+    const int64_t* __restrict__ l1_off, const int32_t* __restrict__ n1_k1, const Support* __restrict__ phiT_sup,
+    const Support* __restrict__ psi2_sup, const BlockInfo* __restrict__ binfo, const int32_t* __restrict__ nmax,
+    int n_blocks, int log2T, int64_t N_pad, int64_t Ft, const float* __restrict__ vals) {
+  const int64_t tile = blockIdx.x;
+  const int b = blockIdx.y;
+  const int n1 = find_job(tiles, N1, tile);
+  const int k1 = n1_k1[n1];
+  const int64_t L1 = N_pad >> k1;
+  const int64_t m = (tile - tiles[n1]) * 256 + threadIdx.x;
+  if (m >= L1) return;
+  float2 acc = make_float2(0.f, 0.f);
+  {
+    const Support sp = phiT_sup[k1];
+    int64_t t = m - sp.lo;
+    t %= L1; if (t < 0) t += L1;
+    if (t < sp.len) {
+      float h = __ldg(vals + sp.off + t);
+      float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m % Ft)];
+      acc = make_float2(h * v.x, h * v.y);
+    }
+  }
+  for (int bi = 0; bi < n_blocks; ++bi) {
+    if (n1 >= nmax[bi]) continue;
+    const Support sp = psi2_sup[bi * (log2T + 1) + k1];
+    int64_t t = m - sp.lo;
+    t %= L1; if (t < 0) t += L1;
+    if (t < sp.len) {
+      float h = __ldg(vals + sp.off + t);
+      const BlockInfo bf = binfo[bi];
+      float2 v = GY[b * GY_sb + bf.y_off + (int64_t)n1 * bf.T2 + (m % bf.T2)];
+      acc.x = fmaf(h, v.x, acc.x);
+      acc.y = fmaf(h, v.y, acc.y);
+    }
+  }
+  out[b * out_sb + l1_off[n1] + m] = acc;
+}
+
+void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS, int64_t GS_sb,
+                          const float2* GY, int64_t GY_sb, float2* out, int64_t out_sb, int B,
+                          cudaStream_t st) {
+  dim3 g((unsigned)d.u1adj_ntiles, (unsigned)B);
+  k_adj_gather_u1<<<g, 256, 0, st>>>(GS, GS_sb, GY, GY_sb, out, out_sb, d.u1adj_tiles, (int)p.psi1.size(),
+                                     d.l1_off, d.n1_k1, d.phiT_sup, d.psi2_sup, d.binfo, d.blk_nmax,
+                                     d.n_blocks, p.log2T, p.N_pad, p.Ft, d.spec_vals);
+  count_launch();
+}
+
+// Modulus adjoint (R22): g_Z1 = (Z1/|Z1|) * Re(g_U1), 0 where |Z1| = 0.
+__global__ void k_phase_mul(const float2* __restrict__ z, const float2* __restrict__ gu, int64_t gsb,
+                            float2* __restrict__ out, int64_t n, int64_t sb) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t o = blockIdx.y * sb + i;
+  float2 v = z[o];
+  float m2 = v.x * v.x + v.y * v.y;
+  float g = gu[blockIdx.y * gsb + i].x;
+  float s = m2 > 1.17549435e-38f ? g * rsqrtf(m2) : 0.f;
+  out[o] = make_float2(v.x * s, v.y * s);
+}
+
+void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
+                      int B, cudaStream_t st) {
+  dim3 g((unsigned)((n_per_b + 255) / 256), (unsigned)B);
+  k_phase_mul<<<g, 256, 0, st>>>(z, gu, gsb, out, n_per_b, sb);
+  count_launch();
+}
+
+// Adjoint of layer 1 in Fourier: g_hat_x[m] = sum_n1 psi1[m] GZ[n1][m mod L1], n1 over the
+// precomputed list of filters whose support meets the 256-bin tile (fixed order: deterministic).
+__global__ void __launch_bounds__(256) k_adj_gather_x(const float2* __restrict__ GZ, int64_t GZ_sb,
+                                                      float2* __restrict__ out, int64_t out_sb,
+                                                      const int32_t* __restrict__ tstart,
+                                                      const int32_t* __restrict__ list,
+                                                      const Support* __restrict__ psi1_sup,
+                                                      const int64_t* __restrict__ l1_off,
+                                                      const int32_t* __restrict__ n1_k1, int64_t N_pad,
+                                                      const float* __restrict__ vals) {
+  const int64_t tile = blockIdx.x;
+  const int b = blockIdx.y;
+  const int64_t m = tile * 256 + threadIdx.x;
+  if (m >= N_pad) return;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int q = tstart[tile]; q < tstart[tile + 1]; ++q) {
+    const int n1 = list[q];
+    const Support sp = psi1_sup[n1];
+    int64_t t = m - sp.lo;
+    t %= N_pad; if (t < 0) t += N_pad;
+    if (t < sp.len) {
+      float h = __ldg(vals + sp.off + t);
+      const int64_t L1 = N_pad >> n1_k1[n1];
+      float2 v = GZ[b * GZ_sb + l1_off[n1] + (m & (L1 - 1))];
+      acc.x = fmaf(h, v.x, acc.x);
+      acc.y = fmaf(h, v.y, acc.y);
+    }
+  }
+  out[b * out_sb + m] = acc;
+}
+
+void launch_adj_gather_x(const Plan& p, const DeviceTables& d, const float2* GZ, int64_t GZ_sb, float2* out,
+                         int64_t out_sb, int B, cudaStream_t st) {
+  dim3 g((unsigned)(p.N_pad / 256), (unsigned)B);
+  k_adj_gather_x<<<g, 256, 0, st>>>(GZ, GZ_sb, out, out_sb, d.gx_tile_start, d.gx_list, d.psi1_sup, d.l1_off,
+                                    d.n1_k1, p.N_pad, d.spec_vals);
+  count_launch();
+}
+
+// real rows -> complex rows (imaginary 0), for the FFT of a real gradient
+__global__ void k_real_to_complex(const float* __restrict__ in, int64_t in_sb, float2* __restrict__ out,
+                                  int64_t out_sb, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[blockIdx.y * out_sb + i] = make_float2(in[blockIdx.y * in_sb + i], 0.f);
+}
+
+void launch_real_to_complex(const float* in, int64_t in_sb, float2* out, int64_t out_sb, int64_t n, int B,
+                            cudaStream_t st) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
+  k_real_to_complex<<<g, 256, 0, st>>>(in, in_sb, out, out_sb, n);
+  count_launch();
+}
+
+// Adjoint of the reflect padding (R10): g[i] = sum over padded positions p with src(p) = i of Re(gxp[p]).
+__global__ void k_reflect_adj(const float2* __restrict__ gxp, int64_t sxp, float* __restrict__ g, int64_t sg,
+                              int64_t N, int64_t N_pad, int64_t pad_left) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int b = blockIdx.y;
+  const float2* src = gxp + b * sxp;
+  const int64_t P2 = 2 * N;
+  float acc = 0.f;
+  for (int w = 0; w < 2; ++w) {
+    int64_t base = (w == 0) ? i : (P2 - 1 - i);
+    // p = pad_left + base + P2*k in [0, N_pad)
+    int64_t kmin = floor_div(-pad_left - base + P2 - 1, P2);
+    int64_t kmax = floor_div(N_pad - 1 - pad_left - base, P2);
+    for (int64_t k = kmin; k <= kmax; ++k) acc += src[pad_left + base + P2 * k].x;
+  }
+  g[b * sg + i] = acc;
+}
+
+void launch_reflect_adj(const float2* gxp, int64_t sxp, float* g, int64_t sg, const Plan& p, int B,
+                        cudaStream_t st) {
+  dim3 gr((unsigned)((p.N + 255) / 256), (unsigned)B);
+  k_reflect_adj<<<gr, 256, 0, st>>>(gxp, sxp, g, sg, p.N, p.N_pad, p.pad_left);
+  count_launch();
+}
+
+// ---- metamer update (R23-R24): per-signal bold-driver decision, then momentum step.
+__global__ void k_metamer_decide(float* mu, float* loss_prev, const float* loss, int32_t* accepted, int B,
+                                 float grow, float shrink) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float E = loss[b];
+  if (E <= loss_prev[b]) {
+    accepted[b] = 1;
+    loss_prev[b] = E;
+    mu[b] = mu[b] * grow;
+  } else {
+    accepted[b] = 0;
+    mu[b] = mu[b] * shrink;
+  }
+}
+
+__global__ void k_metamer_apply(float* __restrict__ y, float* __restrict__ u, float* __restrict__ y_prev,
+                                float* __restrict__ g_prev, const float* __restrict__ mu,
+                                const int32_t* __restrict__ accepted, const float* __restrict__ g, int64_t sg,
+                                int64_t N, float momentum) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int b = blockIdx.y;
+  const int64_t o = (int64_t)b * N + i;
+  float gg, yy, uu;
+  if (accepted[b]) {
+    yy = y[o];
+    gg = g[(int64_t)b * sg + i];
+    y_prev[o] = yy;
+    g_prev[o] = gg;
+    uu = u[o];
+  } else {
+    yy = y_prev[o];
+    gg = g_prev[o];
+    uu = 0.f;
+  }
+  uu = momentum * uu - mu[b] * gg;
+  u[o] = uu;
+  y[o] = yy + uu;
+}
+
+void launch_metamer(float* y, float* u, float* y_prev, float* g_prev, float* mu, float* loss_prev,
+                    const float* loss, int32_t* accepted, const float* g, int64_t sg, int64_t N, int B,
+                    float momentum, float grow, float shrink, cudaStream_t st) {
+  k_metamer_decide<<<(B + 127) / 128, 128, 0, st>>>(mu, loss_prev, loss, accepted, B, grow, shrink);
+  dim3 gr((unsigned)((N + 255) / 256), (unsigned)B);
+  k_metamer_apply<<<gr, 256, 0, st>>>(y, u, y_prev, g_prev, mu, accepted, g, sg, N, momentum);
+  count_launch(2);
+}
+
+}  // namespace jtfs

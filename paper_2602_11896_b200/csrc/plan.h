@@ -1,0 +1,108 @@
+// plan.h — host-side JTFS plan (float64) and the device tables derived from it.
+// The planner is independent of oracle/ (no shared code): it re-derives every rule from PAPER.md
+// and the readings of DESIGN.md §2.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/jtfs.h"
+
+namespace jtfs {
+
+struct Filter {
+  double xi = 0, sigma = 0, kappa = 0;
+  int j = 0, spin = 1;
+  bool phi = false;  // Gaussian low-pass (phi_T / phi_F) instead of Morlet (Eq.1)
+};
+
+struct Block {
+  int n2, n1_max, s2, j2;
+};
+
+// Support-limited spectrum of a filter on an L-point grid: values for bins lo .. lo+len-1 (taken
+// modulo L), stored at vals[off .. off+len).
+struct Support {
+  int64_t lo, len, off, L;
+};
+
+// One gather-fold job: out[m] = scale * sum_{s in [lo, lo+len), s = m mod L_out} in[s mod L_in] *
+// h[s - lo], for m in [0, L_out).  (cdgmm + subsample_fourier)
+struct GatherJob {
+  int64_t in_off, L_in, lo, len, val_off, out_off, L_out;
+  float scale;
+  int32_t pad;
+};
+
+// Batched FFT group: `count` rows of length L starting at `off` (per signal).
+struct FftGroup {
+  int64_t off, count, L;
+};
+
+// Per (block, frequential filter) unit of the joint lambda_1 stage.
+struct JointUnit {
+  int32_t bi, f, kf, d;          // block, filter (L_fr index), k_f, log2F - k_f
+  int32_t n1_max, rows_out;      // K and kept rows (ceil(n1_max/F))
+  int64_t Lf, r_lo, n_rows;      // row grid length P>>kf, needed row range (circular)
+  int64_t o_off;                 // offset of this unit's o[rows_out][n_cols] in the o buffer
+  int32_t path;                  // path index
+  int32_t pad;
+};
+
+struct BlockInfo {
+  int64_t y_off;                 // offset (complex elements) of the block in Y2 (per signal)
+  int64_t T2, c_lo, n_cols;      // columns, needed column range (circular on T2)
+  int32_t s2, D;                 // level, decimation 2^(log2T - s2)
+};
+
+struct DeviceTables;  // device pointers (plan.cu)
+
+struct Plan {
+  // ---- hyper-parameters
+  int64_t N = 0, T = 0, F = 0;
+  int J = 0, Q = 0, J_fr = 0, Q_fr = 0, log2T = 0, log2F = 0;
+  // ---- filterbanks
+  std::vector<Filter> psi1, psi2, psi_fr_plus, L_fr;
+  Filter phiT, phiF;
+  // ---- sizes
+  int64_t N_pad = 0, pad_left = 0, P = 0, frames = 0, Ft = 0, n_coef = 0;
+  std::vector<Block> blocks;
+  std::vector<jtfs_path_t> paths;
+  // ---- derived GPU layout (per signal, in elements)
+  std::vector<int64_t> L1, L1_off;     // per n1: length N_pad>>k1 and offset in sum L1
+  int64_t sumL1 = 0, sumY2 = 0, o_size = 0, o1_W_size = 0;
+  std::vector<BlockInfo> binfo;
+  std::vector<JointUnit> units;        // order-2 (block, filter) units in path order
+  std::vector<FftGroup> l1_groups, y2_groups;
+  std::vector<GatherJob> l1_jobs, s1_jobs, l2_jobs;
+  GatherJob s0_job{};
+  // order-1 unit rows (per f in xi >= 0 prefix)
+  std::vector<int64_t> o1_rlo, o1_nrows;
+  int32_t o1_rows_out = 0;
+  // kernels
+  std::vector<float> spec_vals;                 // all support-limited spectra
+  std::vector<Support> psi1_sup;                // [N1] on N_pad
+  std::vector<Support> psi2_sup;                // [n_blocks][log2T+1] on N_pad>>k (len 0 unused)
+  std::vector<Support> phiT_sup;                // [log2T+1] on N_pad>>k
+  std::vector<float> hfr;                       // [n_fr_all][P][2] row kernels (complex)
+  std::vector<float> phiF_k;                    // concat over k of P>>k real kernels
+  std::vector<int64_t> phiF_off;                // [log2F+1]
+  std::vector<float> phiT_half;                 // concat over s of half kernels t_s[0..H_s]
+  std::vector<int64_t> phiT_off, phiT_H;        // [log2T+1]
+  std::vector<int64_t> phiT_L;                  // [log2T+1] grid length N_pad>>s
+  // adjoint gather of d/dx spectrum: tiles of N_pad with the list of n1 touching each
+  int64_t gx_tile = 256;
+  std::vector<int32_t> gx_tile_start, gx_list;  // CSR over tiles
+  // reflect-pad adjoint needs nothing extra.
+  DeviceTables* dev = nullptr;
+  int dev_id = -1;
+  ~Plan();
+};
+
+// planner.cpp
+int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, Plan* p,
+              std::string* err);
+double response_at(const Filter& f, double omega);   // periodised level-0 response
+void level_response(const Filter& f, int64_t L0, int k, std::vector<double>* out);
+
+}  // namespace jtfs

@@ -1,0 +1,378 @@
+// planner.cpp — JTFS plan in float64 (host). Cites PAPER.md lines (P:n) and DESIGN.md readings.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "plan.h"
+
+namespace jtfs {
+
+static const double kSigma0 = 0.1;
+static const double kPi = 3.14159265358979323846;
+
+// Generator of PAPER.md:167-191 evaluated verbatim in float64 (R1: r = r_psi = sqrt(0.5); R2).
+static std::vector<std::pair<double, double>> anden_generator(int J, int Q) {
+  std::vector<std::pair<double, double>> out;
+  const double r_psi = std::sqrt(0.5);
+  double xi = std::max(1. / (1. + std::pow(2., 3. / Q)), 0.35);
+  double factor = 1. / std::pow(2., 1. / Q);
+  double sigma = (1 - factor) / (1 + factor) * xi / std::sqrt(2 * std::log(1. / r_psi));
+  double sigma_min = kSigma0 / std::pow(2., J);
+  if (sigma <= sigma_min) {
+    xi = sigma;
+  } else {
+    out.emplace_back(xi, sigma);
+    while (sigma > (sigma_min * std::pow(2., 1. / Q))) {   // constant-Q region
+      xi /= std::pow(2., 1. / Q);
+      sigma /= std::pow(2., 1. / Q);
+      out.emplace_back(xi, sigma);
+    }
+  }
+  double elbow_xi = xi;                                      // constant-bandwidth region
+  for (int q = 0; q < Q - 1; ++q) {
+    xi -= 1. / Q * elbow_xi;
+    out.emplace_back(xi, sigma_min);
+  }
+  return out;
+}
+
+// R3: j = max(0, floor(-log2(min(|xi| + 5 sigma, 1/2))) - 1)
+static int dyadic_scale(double xi, double sigma) {
+  double v = std::min(std::fabs(xi) + 5 * sigma, 0.5);
+  int j = (int)std::floor(-std::log2(v)) - 1;
+  return j < 0 ? 0 : j;
+}
+
+// sum_{q in Z} exp(-(nu + q - c)^2 / (2 s^2)), all terms that do not underflow (|.| < 40 s).
+static double gauss_periodised(double nu, double c, double s) {
+  double lo = std::floor(c - nu - 40 * s), hi = std::ceil(c - nu + 40 * s);
+  double acc = 0;
+  for (double q = lo; q <= hi; q += 1.0) {
+    double t = nu + q - c;
+    acc += std::exp(-t * t / (2 * s * s));
+  }
+  return acc;
+}
+
+static double kappa_of(double xi, double sigma) {  // R4
+  return gauss_periodised(0.0, xi, sigma) / gauss_periodised(0.0, 0.0, sigma);
+}
+
+// Level-k response at nu (cycles per level-k sample). The fold-sum of the level-0 periodised
+// response onto L0/2^k bins (R9) equals the periodised Morlet with xi*2^k, sigma*2^k (same kappa).
+static double response_level_nu(const Filter& f, int k, double nu) {
+  double sc = std::ldexp(1.0, k);
+  double s = f.sigma * sc;
+  if (f.phi) return gauss_periodised(nu, 0.0, s);
+  return 2.0 * (gauss_periodised(nu, f.xi * sc, s) - f.kappa * gauss_periodised(nu, 0.0, s));
+}
+
+double response_at(const Filter& f, double omega) { return response_level_nu(f, 0, omega); }
+
+void level_response(const Filter& f, int64_t L0, int k, std::vector<double>* out) {
+  int64_t L = L0 >> k;
+  out->resize(L);
+  for (int64_t m = 0; m < L; ++m) (*out)[m] = response_level_nu(f, k, (double)m / (double)L);
+}
+
+// Support (bins where |response| may exceed 1e-10) of the level-k response on an L-bin grid.
+static Support support_of(const Filter& f, int k, int64_t L, std::vector<float>* vals) {
+  double sc = std::ldexp(1.0, k);
+  double s = f.sigma * sc, c = f.xi * sc;
+  double a, b;
+  if (f.phi) {
+    double w = std::sqrt(2 * std::log(1e10));
+    a = -w * s; b = w * s;
+  } else {
+    double w = std::sqrt(2 * std::log(2e10));
+    a = c - w * s; b = c + w * s;
+    if (2e10 * f.kappa > 1.0) {
+      double w2 = std::sqrt(2 * std::log(2e10 * f.kappa));
+      a = std::min(a, -w2 * s); b = std::max(b, w2 * s);
+    }
+  }
+  int64_t lo = (int64_t)std::floor(a * L), hi = (int64_t)std::ceil(b * L);
+  int64_t len = hi - lo + 1;
+  if (len >= L) { lo = 0; len = L; }
+  Support sp{lo, len, (int64_t)vals->size(), L};
+  for (int64_t t = 0; t < len; ++t)
+    vals->push_back((float)response_level_nu(f, k, (double)(lo + t) / (double)L));
+  return sp;
+}
+
+// Closed-form (Poisson-summed) time-domain kernel of a level-k response on the L0 grid:
+// h_k[n] = 2^k sum_r H(2^k n + r L0), H_psi(t) = 2 s sqrt(2 pi) e^{-2 pi^2 s^2 t^2}(e^{2 pi i xi t}
+// - kappa), H_phi(t) = s sqrt(2 pi) e^{-2 pi^2 s^2 t^2}.
+static void time_kernel(const Filter& f, int64_t L0, int k, int64_t n, double* re, double* im) {
+  double s = f.sigma;
+  double sc = std::ldexp(1.0, k);
+  double reach = 1.40 / s + 2.0;
+  int64_t rmax = (int64_t)std::ceil(reach / (double)L0) + 1;
+  double ar = 0, ai = 0;
+  for (int64_t r = -rmax; r <= rmax; ++r) {
+    double t = sc * (double)n + (double)r * (double)L0;
+    double e = s * std::sqrt(2 * kPi) * std::exp(-2 * kPi * kPi * s * s * t * t);
+    if (e == 0.0) continue;
+    if (f.phi) {
+      ar += e;
+    } else {
+      ar += 2 * e * (std::cos(2 * kPi * f.xi * t) - f.kappa);
+      ai += 2 * e * std::sin(2 * kPi * f.xi * t);
+    }
+  }
+  *re = sc * ar;
+  *im = sc * ai;
+}
+
+static int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p *= 2;
+  return p;
+}
+static int ilog2(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << (l + 1)) <= n) ++l;
+  return l;
+}
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static int64_t pmod(int64_t a, int64_t m) { return ((a % m) + m) % m; }
+
+int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, Plan* p,
+              std::string* err) {
+  auto ispow2 = [](int64_t v) { return v >= 1 && (v & (v - 1)) == 0; };
+  if (J < 1 || Q < 1 || J_fr < 1 || Q_fr < 1) { *err = "J, Q, J_fr, Q_fr must be >= 1"; return 1; }
+  if (!ispow2(T)) { *err = "T must be a power of two"; return 1; }
+  if (!ispow2(F)) { *err = "F must be a power of two"; return 1; }
+  int log2T = ilog2(T), log2F = ilog2(F);
+  if (!(1 <= log2T && log2T <= J)) { *err = "need 1 <= log2(T) <= J"; return 1; }
+  if (!(0 <= log2F && log2F <= J_fr)) { *err = "need 0 <= log2(F) <= J_fr"; return 1; }
+  if (N < T || N % T != 0) { *err = "N must be a positive multiple of T"; return 1; }
+  if (J > 24 || J_fr > 16 || Q > 64 || Q_fr > 16) { *err = "J <= 24, J_fr <= 16, Q <= 64, Q_fr <= 16"; return 1; }
+
+  p->N = N; p->J = J; p->Q = Q; p->J_fr = J_fr; p->Q_fr = Q_fr; p->T = T; p->F = F;
+  p->log2T = log2T; p->log2F = log2F;
+  auto mk = [](double xi, double s) {
+    Filter f; f.xi = xi; f.sigma = s; f.j = dyadic_scale(xi, s); f.kappa = kappa_of(xi, s);
+    return f;
+  };
+  for (auto& q : anden_generator(J, Q)) p->psi1.push_back(mk(q.first, q.second));
+  for (auto& q : anden_generator(J, 1)) p->psi2.push_back(mk(q.first, q.second));   // R7
+  for (auto& q : anden_generator(J_fr, Q_fr)) p->psi_fr_plus.push_back(mk(q.first, q.second));
+  p->phiT.phi = true; p->phiT.sigma = kSigma0 / (double)T; p->phiT.j = log2T; p->phiT.spin = 0;
+  p->phiF.phi = true; p->phiF.sigma = kSigma0 / (double)F; p->phiF.j = log2F; p->phiF.spin = 0;
+  p->L_fr.push_back(p->phiF);                                                     // R12
+  for (auto f : p->psi_fr_plus) { f.spin = 1; p->L_fr.push_back(f); }
+  for (auto f : p->psi_fr_plus) { f.xi = -f.xi; f.spin = -1; p->L_fr.push_back(f); }
+  const int N1 = (int)p->psi1.size();
+  if (N1 < 1) { *err = "empty first-layer filterbank"; return 1; }
+
+  // R10
+  p->N_pad = next_pow2(N + 2 * (int64_t)std::ceil(4.0 * (double)std::max<int64_t>(int64_t(1) << J, T) /
+                                                  (0.2 * kPi)));
+  if (p->N_pad > (int64_t(1) << 22)) { *err = "N_pad exceeds 2^22"; return 1; }
+  p->pad_left = T * ((p->N_pad - N) / (2 * T));
+  // R11
+  double sfr = p->phiF.sigma;
+  for (auto& f : p->psi_fr_plus) sfr = std::min(sfr, f.sigma);
+  p->P = next_pow2(N1 + 2 * (int64_t)std::ceil(4.0 / (2 * kPi * sfr)));
+  p->frames = N / T;
+  p->Ft = p->N_pad / T;
+  for (int i = 0; i + 1 < N1; ++i)
+    if (p->psi1[i].j > p->psi1[i + 1].j) { *err = "internal: j1 not nondecreasing"; return 1; }
+  if (ceil_div(N1, F) > 32) { *err = "ceil(N1/F) must be <= 32 (GPU kernel limit)"; return 1; }
+  for (int n2 = 0; n2 < (int)p->psi2.size(); ++n2) {
+    int j2 = p->psi2[n2].j, n1_max = 0;
+    for (auto& f : p->psi1) n1_max += (j2 > f.j);
+    if (n1_max > 0) p->blocks.push_back({n2, n1_max, std::min(j2, log2T), j2});
+  }
+
+  // ---- path table (R15, R16)
+  int64_t off = 0;
+  auto add = [&](int order, int n2, int nfr, int spin, int j2, int jfr, int rows) {
+    jtfs_path_t q;
+    q.order = order; q.n2 = n2; q.n_fr = nfr; q.spin = spin; q.j2 = j2; q.j_fr = jfr;
+    q.rows = rows; q.frames = (int32_t)p->frames; q.offset = off;
+    p->paths.push_back(q);
+    off += (int64_t)rows * p->frames;
+  };
+  add(0, -1, -1, 0, -1, -1, 1);
+  const int nfr1 = 1 + (int)p->psi_fr_plus.size();
+  int rows1 = (int)ceil_div(N1, F);
+  for (int f = 0; f < nfr1; ++f) add(1, -1, f, p->L_fr[f].spin, -1, p->L_fr[f].j, rows1);
+  for (auto& b : p->blocks)
+    for (int f = 0; f < (int)p->L_fr.size(); ++f)
+      add(2, b.n2, f, p->L_fr[f].spin, b.j2, p->L_fr[f].j, (int)ceil_div(b.n1_max, F));
+  p->n_coef = off;
+
+  // ---- layer-1 layout
+  p->L1.resize(N1); p->L1_off.resize(N1);
+  int64_t s = 0;
+  for (int n1 = 0; n1 < N1; ++n1) {
+    int k1 = std::min(p->psi1[n1].j, log2T);
+    p->L1[n1] = p->N_pad >> k1; p->L1_off[n1] = s; s += p->L1[n1];
+  }
+  p->sumL1 = s;
+  for (int n1 = 0; n1 < N1;) {
+    int n = n1;
+    while (n < N1 && p->L1[n] == p->L1[n1]) ++n;
+    p->l1_groups.push_back({p->L1_off[n1], n - n1, p->L1[n1]});
+    n1 = n;
+  }
+
+  // ---- spectra (support-limited; threshold 1e-10 absolute, DESIGN R26)
+  std::vector<float>& V = p->spec_vals;
+  for (int n1 = 0; n1 < N1; ++n1) p->psi1_sup.push_back(support_of(p->psi1[n1], 0, p->N_pad, &V));
+  for (int k = 0; k <= log2T; ++k) p->phiT_sup.push_back(support_of(p->phiT, k, p->N_pad >> k, &V));
+  p->psi2_sup.assign(p->blocks.size() * (log2T + 1), Support{0, 0, 0, 0});
+  for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
+    auto& b = p->blocks[bi];
+    for (int k = 0; k <= std::min(b.j2 - 1, log2T); ++k)
+      p->psi2_sup[bi * (log2T + 1) + k] = support_of(p->psi2[b.n2], k, p->N_pad >> k, &V);
+  }
+
+  // gather jobs: layer 1, S0, S1 time part, layer 2
+  for (int n1 = 0; n1 < N1; ++n1) {
+    auto& sp = p->psi1_sup[n1];
+    int k1 = std::min(p->psi1[n1].j, log2T);
+    p->l1_jobs.push_back({0, p->N_pad, sp.lo, sp.len, sp.off, p->L1_off[n1], p->L1[n1],
+                          (float)std::ldexp(1.0, -k1), 0});
+  }
+  {
+    auto& sp = p->phiT_sup[0];
+    p->s0_job = {0, p->N_pad, sp.lo, sp.len, sp.off, 0, p->Ft, (float)std::ldexp(1.0, -log2T), 0};
+  }
+  for (int n1 = 0; n1 < N1; ++n1) {
+    int k1 = std::min(p->psi1[n1].j, log2T);
+    auto& sp = p->phiT_sup[k1];
+    p->s1_jobs.push_back({p->L1_off[n1], p->L1[n1], sp.lo, sp.len, sp.off, (int64_t)n1 * p->Ft, p->Ft,
+                          (float)std::ldexp(1.0, -(log2T - k1)), 0});
+  }
+  int64_t yoff = 0;
+  for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
+    auto& b = p->blocks[bi];
+    BlockInfo bf{};
+    bf.y_off = yoff; bf.T2 = p->N_pad >> b.s2; bf.s2 = b.s2; bf.D = 1 << (log2T - b.s2);
+    for (int n1 = 0; n1 < b.n1_max; ++n1) {
+      int k1 = std::min(p->psi1[n1].j, log2T);
+      auto& sp = p->psi2_sup[bi * (log2T + 1) + k1];
+      p->l2_jobs.push_back({p->L1_off[n1], p->L1[n1], sp.lo, sp.len, sp.off, yoff + n1 * bf.T2, bf.T2,
+                            (float)std::ldexp(1.0, -(b.s2 - k1)), 0});
+    }
+    p->y2_groups.push_back({yoff, b.n1_max, bf.T2});
+    yoff += (int64_t)b.n1_max * bf.T2;
+    p->binfo.push_back(bf);
+  }
+  p->sumY2 = yoff;
+
+  // ---- frequential row kernels h_f on the P grid (closed form, complex) for all of L_fr
+  const int nfr = (int)p->L_fr.size();
+  p->hfr.resize((size_t)nfr * p->P * 2);
+  for (int f = 0; f < nfr; ++f)
+    for (int64_t n = 0; n < p->P; ++n) {
+      double re, im;
+      time_kernel(p->L_fr[f], p->P, 0, n, &re, &im);
+      p->hfr[((size_t)f * p->P + n) * 2] = (float)re;
+      p->hfr[((size_t)f * p->P + n) * 2 + 1] = (float)im;
+    }
+  // phi_F kernels at levels k = 0..log2F on P>>k grids; truncation half-widths (1e-9 rel)
+  std::vector<int64_t> HF(log2F + 1);
+  for (int k = 0; k <= log2F; ++k) {
+    int64_t L = p->P >> k;
+    p->phiF_off.push_back((int64_t)p->phiF_k.size());
+    double mx = 0;
+    std::vector<double> g(L);
+    for (int64_t n = 0; n < L; ++n) {
+      double re, im;
+      time_kernel(p->phiF, p->P, k, n, &re, &im);
+      g[n] = re; mx = std::max(mx, std::fabs(re));
+    }
+    int64_t H = 0;
+    for (int64_t n = 0; n <= L / 2; ++n)
+      if (std::fabs(g[n]) >= 1e-9 * mx) H = n;
+    HF[k] = H;
+    for (int64_t n = 0; n < L; ++n) p->phiF_k.push_back((float)g[n]);
+  }
+  // phi_T half kernels at levels s = 0..log2T (grid N_pad>>s), truncated at 1e-9 relative
+  for (int sl = 0; sl <= log2T; ++sl) {
+    int64_t L = p->N_pad >> sl;
+    std::vector<double> t;
+    double mx = 0;
+    for (int64_t n = 0; n <= L / 2; ++n) {
+      double re, im;
+      time_kernel(p->phiT, p->N_pad, sl, n, &re, &im);
+      t.push_back(re); mx = std::max(mx, std::fabs(re));
+    }
+    int64_t H = 0;
+    for (int64_t n = 0; n <= L / 2; ++n)
+      if (std::fabs(t[n]) >= 1e-9 * mx) H = n;
+    p->phiT_off.push_back((int64_t)p->phiT_half.size());
+    p->phiT_H.push_back(H);
+    p->phiT_L.push_back(L);
+    for (int64_t n = 0; n <= H; ++n) p->phiT_half.push_back((float)t[n]);
+  }
+  // needed columns per block (exact halo pruning, R26): kept frames at m*D, reach H_s
+  int64_t m0 = p->pad_left / T;
+  for (auto& bf : p->binfo) {
+    int64_t H = p->phiT_H[bf.s2];
+    int64_t a = m0 * bf.D - H, b = (m0 + p->frames - 1) * bf.D + H;
+    if (b - a + 1 >= bf.T2) { bf.c_lo = 0; bf.n_cols = bf.T2; }
+    else { bf.c_lo = pmod(a, bf.T2); bf.n_cols = b - a + 1; }
+  }
+  // order-2 units in path order; needed rows per unit
+  int64_t ooff = 0;
+  int path = 1 + nfr1;
+  for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
+    auto& b = p->blocks[bi];
+    for (int f = 0; f < nfr; ++f, ++path) {
+      JointUnit u{};
+      u.bi = (int)bi; u.f = f; u.kf = std::min(p->L_fr[f].j, log2F); u.d = log2F - u.kf;
+      u.n1_max = b.n1_max; u.rows_out = (int)ceil_div(b.n1_max, F);
+      u.Lf = p->P >> u.kf;
+      int64_t H = HF[u.kf];
+      int64_t a = -H, c = (int64_t)(u.rows_out - 1) * (int64_t(1) << u.d) + H;
+      if (c - a + 1 >= u.Lf) { u.r_lo = 0; u.n_rows = u.Lf; }
+      else { u.r_lo = pmod(a, u.Lf); u.n_rows = c - a + 1; }
+      u.o_off = ooff; u.path = path;
+      ooff += (int64_t)u.rows_out * p->binfo[bi].n_cols;
+      p->units.push_back(u);
+    }
+  }
+  p->o_size = ooff;
+  // order-1 needed rows
+  p->o1_rows_out = rows1;
+  for (int f = 0; f < nfr1; ++f) {
+    int kf = std::min(p->L_fr[f].j, log2F), d = log2F - kf;
+    int64_t Lf = p->P >> kf, H = HF[kf];
+    int64_t a = -H, c = (int64_t)(rows1 - 1) * (int64_t(1) << d) + H;
+    if (f == 0) { a = 0; c = rows1 - 1; }   // phi_F path keeps rows directly (no modulus)
+    if (c - a + 1 >= Lf) { p->o1_rlo.push_back(0); p->o1_nrows.push_back(Lf); }
+    else { p->o1_rlo.push_back(pmod(a, Lf)); p->o1_nrows.push_back(c - a + 1); }
+  }
+  // adjoint d/dx spectrum gather: CSR of n1 touching each tile of N_pad bins
+  int64_t ntile = ceil_div(p->N_pad, p->gx_tile);
+  p->gx_tile_start.push_back(0);
+  for (int64_t t = 0; t < ntile; ++t) {
+    int64_t a = t * p->gx_tile, b = a + p->gx_tile;   // [a, b)
+    for (int n1 = 0; n1 < N1; ++n1) {
+      auto& sp = p->psi1_sup[n1];
+      bool hit = false;
+      if (sp.len >= p->N_pad) hit = true;
+      else {
+        int64_t lo = pmod(sp.lo, p->N_pad);
+        // interval [lo, lo+len) modulo N_pad intersects [a, b)?
+        for (int w = -1; w <= 1 && !hit; ++w) {
+          int64_t l = lo + w * p->N_pad, h = l + sp.len;
+          if (l < b && h > a) hit = true;
+        }
+      }
+      if (hit) p->gx_list.push_back(n1);
+    }
+    p->gx_tile_start.push_back((int32_t)p->gx_list.size());
+  }
+  return 0;
+}
+
+}  // namespace jtfs

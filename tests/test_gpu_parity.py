@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA path through the C ABI vs the float64 oracle, element by element.
+Bars (BASELINE.json north_star): rel-L2 <= 1e-4 on coefficients, <= 1e-3 on gradients."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.jtfs import Oracle
+from oracle import metamer as om
+from synth import CONFIGS, TINY, plan_args, noise, batch
+
+pytestmark = pytest.mark.gpu
+ALL = {**CONFIGS, **TINY}
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def plans():
+    from paper_2602_11896_b200 import Plan
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = Plan(*plan_args(ALL[name]))
+        return cache[name]
+    return get
+
+
+def inputs(name, B=2):
+    cfg = ALL[name]
+    if name in TINY:
+        return noise(cfg["N"], B, seed=31), noise(cfg["N"], B, seed=32)
+    return batch(name, B), batch(name, B, which="y")
+
+
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1"])
+def test_stage_U1_S1t_Y2(plans, name):
+    p = plans(name)
+    o = Oracle(plan_args(ALL[name]))
+    x, _ = inputs(name)
+    xd = torch.from_numpy(x).cuda()
+    S0, U1h, S1t = o.layer1(torch.from_numpy(x).double())
+    U1 = torch.cat([torch.fft.ifft(u).real for u in U1h], dim=1).numpy()
+    g1 = p.debug_stage(1, xd).cpu().numpy()
+    assert rel(g1, U1) <= 1e-5
+    g2 = p.debug_stage(2, xd).cpu().numpy()
+    assert rel(g2, S1t.numpy()) <= 1e-5
+    if o.plan.blocks:
+        g3 = p.debug_stage(3, xd).cpu().numpy()
+        Y2 = torch.cat([o.layer2_block(U1h, bi).reshape(x.shape[0], -1) for bi in range(len(o.plan.blocks))],
+                       dim=1).numpy()
+        assert rel(g3, Y2) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1"])
+def test_forward_parity(plans, name):
+    p = plans(name)
+    o = Oracle(plan_args(ALL[name]))
+    x, _ = inputs(name)
+    S = p.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    So = o.forward(x).numpy()
+    assert rel(S, So) <= 1e-4
+    # every path individually (the small ones too)
+    for q in o.plan.paths:
+        sl = slice(q.offset, q.offset + q.rows * q.frames)
+        assert rel(S[:, sl], So[:, sl]) <= 1e-3, q
+
+
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1"])
+def test_loss_grad_parity(plans, name):
+    p = plans(name)
+    o = Oracle(plan_args(ALL[name]))
+    x, y = inputs(name)
+    So = o.forward(x)
+    Eo, go = o.loss_grad(y, So)
+    St = torch.from_numpy(So.numpy().astype(np.float32)).cuda()
+    loss, g = p.loss_grad(torch.from_numpy(y).cuda(), St)
+    assert rel(loss.cpu().numpy(), Eo.numpy()) <= 1e-4
+    assert rel(g.cpu().numpy(), go.numpy()) <= 1e-3
+
+
+def test_nullity_and_determinism(plans):
+    p = plans("spec")
+    x, _ = inputs("spec")
+    xd = torch.from_numpy(x).cuda()
+    S = p.forward(xd)
+    S2 = p.forward(xd)
+    assert torch.equal(S, S2)
+    loss, g = p.loss_grad(xd, S)
+    assert float(loss.abs().max()) == 0.0 and float(g.abs().max()) == 0.0
+    l1, g1 = p.loss_grad(xd * 0.5, S)
+    l2, g2 = p.loss_grad(xd * 0.5, S)
+    assert torch.equal(g1, g2) and torch.equal(l1, l2)
+
+
+def test_microbatch_and_shards_sum(plans):
+    p = plans("c1")
+    x, y = inputs("c1", B=3)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    S = p.forward(xd)
+    loss, g = p.loss_grad(yd, S)
+    # micro-batch of one signal through a minimal workspace: bitwise the same per signal
+    ws = torch.empty(p.workspace_size(1, True), dtype=torch.uint8, device="cuda")
+    l1, g1 = p.loss_grad(yd, S, ws=ws)
+    assert torch.equal(g1, g) and torch.equal(l1, loss)
+    # path shards sum to the whole (order of summation differs only)
+    ls, gs = 0, 0
+    for sh in range(3):
+        l_, g_ = p.loss_grad(yd, S, shard=sh, n_shards=3)
+        ls, gs = ls + l_, gs + g_
+    assert rel(gs.cpu().numpy(), g.cpu().numpy()) <= 1e-6
+    assert rel(ls.cpu().numpy(), loss.cpu().numpy()) <= 1e-6
+
+
+def test_metamer_step_parity(plans):
+    name = "t2"
+    p = plans(name)
+    o = Oracle(plan_args(ALL[name]))
+    x, y = inputs(name)
+    So = o.forward(x)
+    St = torch.from_numpy(So.numpy().astype(np.float32)).cuda()
+    st = p.metamer_state(torch.from_numpy(y).cuda())
+    ost = om.init_state(y)
+    for it in range(4):
+        E, g = o.loss_grad(ost["y"], So)
+        ost = om.step(ost, E.numpy(), g.numpy())
+        p.metamer_step(st, St)
+        torch.cuda.synchronize()
+        assert st["accepted"].cpu().tolist() == ost["accepted"].tolist()
+        assert rel(st["mu"].cpu().numpy(), ost["mu"]) <= 1e-6
+        # compare the accumulated update y - y0 (the quantity the step computes)
+        assert rel(st["y"].cpu().numpy() - y, ost["y"] - y) <= 1e-3, it
