@@ -148,6 +148,20 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
 /* Number of kernels the library has launched in this process (for launch-count reporting). */
 int64_t jtfs_launch_count(void);
 
+/* Algorithmic cost per signal (for roofline reporting): out[0] = FP32 flops of the
+ * joint-stage forward kernels (8*K per modulus value for the dense lambda_1 contraction, + 3 for the
+ * modulus + 2*rows_out for phi_F, over the pruned rows x columns), out[1] = same for the joint
+ * backward (16*K + 2*rows_out + 6), out[2] = number of modulus values, out[3] = HBM bytes of the
+ * joint stage (Y2 read fwd + Y2 read bwd + g_Y2 write + o write/read). cap >= 4. */
+jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap);
+
+/* Profiling hook used by bench.py: when enabled, CUDA events are recorded on the launch stream
+ * around the joint-stage kernels (id 0 = forward, 1 = backward). jtfs_prof_read synchronises on the
+ * recorded events, returns the summed elapsed milliseconds and the number of timed launches of
+ * `id`, and clears them. */
+void jtfs_prof_enable(int on);
+jtfs_status jtfs_prof_read(int id, double* total_ms, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

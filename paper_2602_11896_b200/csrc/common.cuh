@@ -7,6 +7,9 @@ namespace jtfs {
 
 // Count of kernel launches issued by the library (reported by bench.py as gpu_launches).
 void count_launch(int n = 1);
+// Profiling hooks (jtfs_prof_enable): CUDA events around the joint-stage kernels.
+void prof_begin(cudaStream_t st, int id);
+void prof_end(cudaStream_t st, int id);
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

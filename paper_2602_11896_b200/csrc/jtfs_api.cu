@@ -18,6 +18,27 @@
 namespace jtfs {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches += n; }
+
+// ---- profiling hooks: events around the dominant kernels, on their launch stream
+static std::atomic<int> g_prof{0};
+static std::mutex g_prof_mu;
+struct ProfRec { int id; cudaEvent_t a, b; };
+static std::vector<ProfRec> g_prof_recs;
+static thread_local cudaEvent_t t_open[2] = {nullptr, nullptr};
+void prof_begin(cudaStream_t st, int id) {
+  if (!g_prof.load()) return;
+  cudaEventCreate(&t_open[id]);
+  cudaEventRecord(t_open[id], st);
+}
+void prof_end(cudaStream_t st, int id) {
+  if (!g_prof.load() || !t_open[id]) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_recs.push_back({id, t_open[id], b});
+  t_open[id] = nullptr;
+}
 }  // namespace jtfs
 
 using namespace jtfs;
@@ -328,6 +349,47 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
 extern "C" {
 
 const char* jtfs_last_error(void) { return t_err.c_str(); }
+
+void jtfs_prof_enable(int on) { jtfs::g_prof.store(on ? 1 : 0); }
+
+jtfs_status jtfs_prof_read(int id, double* total_ms, int64_t* count) {
+  if (!total_ms || !count) return fail(JTFS_ERR_SIZE, "NULL argument");
+  std::lock_guard<std::mutex> lk(jtfs::g_prof_mu);
+  double tot = 0;
+  int64_t n = 0;
+  std::vector<jtfs::ProfRec> keep;
+  for (auto& r : jtfs::g_prof_recs) {
+    if (r.id != id) { keep.push_back(r); continue; }
+    CK(cudaEventSynchronize(r.b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    tot += ms;
+    ++n;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  jtfs::g_prof_recs.swap(keep);
+  *total_ms = tot;
+  *count = n;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap) {
+  if (!plan || !out || cap < 4) return fail(JTFS_ERR_SIZE, "NULL argument or cap < 4");
+  const Plan& p = plan->p;
+  double ff = 0, fb = 0, nm = 0, by = 0;
+  for (auto& u : p.units) {
+    double cells = (double)u.n_rows * (double)p.binfo[u.bi].n_cols;
+    nm += cells;
+    ff += cells * (8.0 * u.n1_max + 3.0 + 2.0 * u.rows_out);
+    fb += cells * (16.0 * u.n1_max + 6.0 + 2.0 * u.rows_out);
+    by += 2.0 * 4.0 * u.rows_out * p.binfo[u.bi].n_cols;   // o written (fwd) and g_o read (bwd)
+  }
+  for (size_t bi = 0; bi < p.blocks.size(); ++bi)
+    by += 3.0 * 8.0 * p.blocks[bi].n1_max * p.binfo[bi].n_cols;  // Y2 read fwd, read bwd, g_Y2 write
+  out[0] = ff; out[1] = fb; out[2] = nm; out[3] = by;
+  return JTFS_OK;
+}
 int64_t jtfs_launch_count(void) { return jtfs::g_launches.load(); }
 
 jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, jtfs_plan_t* out) {

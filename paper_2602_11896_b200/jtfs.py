@@ -199,3 +199,19 @@ class Plan:
 
     def launch_count(self) -> int:
         return self.lib.jtfs_launch_count()
+
+    def cost(self) -> dict:
+        """Algorithmic per-signal cost of the joint stage (see include/jtfs.h jtfs_plan_cost)."""
+        out = np.zeros(4)
+        check(self.lib.jtfs_plan_cost(self.h, out.ctypes.data, 4))
+        return {"joint_fwd_flops": out[0], "joint_bwd_flops": out[1], "modulus_values": out[2],
+                "joint_hbm_bytes": out[3]}
+
+    def prof_enable(self, on: bool) -> None:
+        self.lib.jtfs_prof_enable(1 if on else 0)
+
+    def prof_read(self, kid: int) -> tuple[float, int]:
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        check(self.lib.jtfs_prof_read(kid, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value

@@ -13,8 +13,8 @@ ALL = {**CONFIGS, **TINY}
 
 
 def rel(a, b):
-    a = np.asarray(a, np.float64)
-    b = np.asarray(b, np.float64)
+    a = np.asarray(a).astype(np.complex128 if np.iscomplexobj(a) or np.iscomplexobj(b) else np.float64)
+    b = np.asarray(b).astype(a.dtype)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
