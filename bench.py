@@ -120,7 +120,9 @@ def run_reference(args) -> None:
     x = batch(args.config, 1)
     y = batch(args.config, 1, which="y")
     St = o.forward(x)
-    steps = args.steps
+    # one reference step = fwd+grad of ONE signal (~1 min on 16 cores); capped at 2 steps so the
+    # arm ends within a few minutes whatever --steps says (reported as "steps")
+    steps = max(1, min(args.steps, 2))
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -154,6 +156,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--path-shards", type=int, default=1,
+                    help="ranks per path group (order-2 units split, dE/dx all-reduced over NVLink)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -173,17 +177,28 @@ def main() -> None:
     plan = Plan(*plan_args(cfg))
     stream = torch.cuda.current_stream()
     plan.prepare(stream)
-    # per-rank batch: independent signals (weak scaling); target S(x) computed once, untimed
-    x = torch.from_numpy(batch(args.config, B, start=rank * B)).to(dev)
-    y = torch.from_numpy(batch(args.config, B, which="y", start=rank * B)).to(dev)
+    ps = max(1, args.path_shards)
+    group_id = rank // ps                     # batch group (signals) of this rank
+    n_groups = world // ps
+    # per-group batch: independent signals (weak scaling); target S(x) computed once, untimed
+    x = torch.from_numpy(batch(args.config, B, start=group_id * B)).to(dev)
+    y = torch.from_numpy(batch(args.config, B, which="y", start=group_id * B)).to(dev)
     St = plan.forward(x)
     ws = plan.workspace(B, True, dev)
     loss = torch.empty(B, device=dev)
     grad = torch.empty_like(y)
     mb = ws.numel() // plan.workspace_size(1, True)
+    if ps > 1:
+        from paper_2602_11896_b200.dist import DistJTFS
+        dj = DistJTFS(plan, path_shards=ps,
+                      compute=lambda yy, SS, s, n: plan.loss_grad(yy, SS, shard=s, n_shards=n, loss=loss,
+                                                                  grad=grad, ws=ws))
 
     def step():
-        plan.loss_grad(y, St, loss=loss, grad=grad, ws=ws)
+        if ps > 1:
+            dj.loss_grad(y, St)
+        else:
+            plan.loss_grad(y, St, loss=loss, grad=grad, ws=ws)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -215,11 +230,11 @@ def main() -> None:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * B * cfg["N"] * args.steps / (ms / 1000.0)
+    value = n_groups * B * cfg["N"] * args.steps / (ms / 1000.0)
 
     # end-to-end through the host-buffer C-ABI call (pinned host memory, copies inside)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and ps == 1:
         yh = torch.from_numpy(batch(args.config, B, which="y", start=rank * B)).pin_memory()
         Sth = St.cpu().pin_memory()
         wsh = plan.workspace_host(B, dev)
@@ -241,7 +256,7 @@ def main() -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             hms = float(t.item())
         del wsh
-        e2e = {"value": world * B * cfg["N"] * args.steps / (hms / 1000.0), "unit": UNIT,
+        e2e = {"value": n_groups * B * cfg["N"] * args.steps / (hms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(B * cfg["N"] * 4 + B * plan.n_coef * 4),
                "d2h_bytes_per_step": int(B * 4 + B * cfg["N"] * 4)}
 
@@ -267,7 +282,7 @@ def main() -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {_describe(args.config)} per rank",
                    "l2": "per-step working set > 126 MB L2 (no flush needed)",
-                   "micro_batch": int(mb)},
+                   "micro_batch": int(mb), "parallelism": f"batch{n_groups}xpath{ps}"},
         "roofline": {"kernel": "k_joint_bwd", "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak_tflops, "unit": "TFLOP/s",
                      "frac": (achieved / fp32_peak_tflops) if achieved else None, "traffic": None,

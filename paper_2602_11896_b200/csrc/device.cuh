@@ -25,6 +25,7 @@ struct DeviceTables {
   BlockInfo* binfo = nullptr;       int n_blocks = 0;
   // forward unit lists per rows_out class KAP in {1,2,4,8,16,32}: unit indices + tile prefix
   int32_t* fwd_ulist[6] = {};       int64_t* fwd_tiles[6] = {};    int fwd_n[6] = {};  int64_t fwd_ntiles[6] = {};
+  int fwd_kmax[6] = {};
   int32_t* kf_of = nullptr;         // [n_fr] k_f per frequential filter
   int32_t* blk_nmax = nullptr;      // [n_blocks]
   int64_t* ucoef = nullptr;         // [n_units] coefficient offset of the unit's path - o2_start

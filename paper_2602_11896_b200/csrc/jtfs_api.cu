@@ -137,6 +137,7 @@ static cudaError_t upload(Plan& p) {
       if (cls != c) continue;
       ul.push_back((int32_t)u);
       cnt.push_back((p.binfo[p.units[u].bi].n_cols + kJC - 1) / kJC);
+      d->fwd_kmax[c] = std::max(d->fwd_kmax[c], p.units[u].n1_max);
     }
     d->fwd_n[c] = (int)ul.size();
     if (!ul.empty()) {

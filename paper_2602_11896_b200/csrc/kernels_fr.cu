@@ -605,15 +605,15 @@ void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t
   count_launch(2);
 }
 
-static size_t joint_fwd_smem(const Plan& p, const DeviceTables& d, int kap) {
-  return (size_t)d.Kmax * kJC * 8 + (size_t)p.P * 8 + (size_t)d.maxLf * 4 + (size_t)16 * kap * kJC * 4;
+static size_t joint_fwd_smem(const Plan& p, const DeviceTables& d, int ci, int kap) {
+  return (size_t)d.fwd_kmax[ci] * kJC * 8 + (size_t)p.P * 8 + (size_t)d.maxLf * 4 + (size_t)16 * kap * kJC * 4;
 }
 
 template <int KAP>
 static void launch_joint_fwd_kap(const Plan& p, const DeviceTables& d, int ci, const float2* Y2, int64_t y_sb,
                                  float* o, int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st) {
   if (d.fwd_n[ci] == 0) return;
-  size_t sm = joint_fwd_smem(p, d, KAP);
+  size_t sm = joint_fwd_smem(p, d, ci, KAP);
   cudaFuncSetAttribute(k_joint_fwd<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)d.fwd_ntiles[ci], (unsigned)B);
   k_joint_fwd<KAP><<<g, 256, sm, st>>>(Y2, y_sb, o, o_sb, d.units, d.fwd_ulist[ci], d.fwd_tiles[ci], d.fwd_n[ci],

@@ -1,0 +1,93 @@
+"""Multi-GPU glue: one process per GPU, torch.distributed over NCCL.
+
+Two ways to split the work of jtfs_loss_grad:
+  * batch sharding — signals are independent (R27): each rank owns B/G signals, no data-path
+    collective (weak scaling). Only per-signal losses may be gathered for logging.
+  * path sharding — the order-2 units (block n2 x frequential filter) of ONE signal are split
+    across the ranks of a path group: unit u goes to shard u mod n_shards, order 1 to shard 0
+    (the rule implemented by jtfs_loss_grad, include/jtfs.h). Every rank recomputes layer 1.
+    The partial dE/dx and losses sum exactly, so the only exchange is ONE all_reduce(SUM) of
+    [grad | loss] per micro-batch over NVLink.
+Ranks are laid out as (batch_group, path_shard) with path_shard = rank % path_shards.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def batch_slice(B_total: int, world: int, rank: int) -> slice:
+    """Contiguous, balanced split of B_total signals over `world` batch groups."""
+    base, rem = divmod(B_total, world)
+    start = rank * base + min(rank, rem)
+    return slice(start, start + base + (1 if rank < rem else 0))
+
+
+def unit_shard(unit: int, n_shards: int) -> int:
+    """Owner shard of order-2 unit `unit` (paths in yield order after S0 and order 1)."""
+    return unit % n_shards
+
+
+def path_owner(paths: list[dict], n_shards: int) -> list[int]:
+    """Owner shard of every path: -1 for S0 (not in the loss), 0 for order 1, u mod n for order 2."""
+    out, u = [], 0
+    for q in paths:
+        if q["order"] == 0:
+            out.append(-1)
+        elif q["order"] == 1:
+            out.append(0)
+        else:
+            out.append(unit_shard(u, n_shards))
+            u += 1
+    return out
+
+
+class DistJTFS:
+    """Sharded loss + gradient. `compute(y, S_target, shard, n_shards) -> (loss, grad)` defaults to
+    the CUDA plan's jtfs_loss_grad; it is injectable only so the CPU gloo tests can exercise the
+    collective logic."""
+
+    def __init__(self, plan=None, path_shards: int = 1, group=None,
+                 compute: Callable | None = None):
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world % path_shards:
+            raise ValueError("world size must be a multiple of path_shards")
+        self.path_shards = path_shards
+        self.shard = self.rank % path_shards
+        self.batch_group = self.rank // path_shards
+        self.n_batch_groups = self.world // path_shards
+        self.plan = plan
+        self.compute = compute or (lambda y, St, s, n: plan.loss_grad(y, St, shard=s, n_shards=n))
+        # one process group per path group (every rank must create every group, same order)
+        self.path_group = None
+        if path_shards > 1:
+            ranks_all = dist.get_process_group_ranks(group) if group is not None else list(range(self.world))
+            for g in range(self.n_batch_groups):
+                ranks = ranks_all[g * path_shards:(g + 1) * path_shards]
+                pg = dist.new_group(ranks)
+                if g == self.batch_group:
+                    self.path_group = pg
+
+    def my_signals(self, B_total: int) -> slice:
+        return batch_slice(B_total, self.n_batch_groups, self.batch_group)
+
+    def loss_grad(self, y: torch.Tensor, S_target: torch.Tensor):
+        """(loss, grad) of this rank's signals, complete (summed over the path group)."""
+        loss, grad = self.compute(y, S_target, self.shard, self.path_shards)
+        if self.path_shards > 1:
+            B = grad.shape[0]
+            buf = torch.cat([grad.reshape(-1), loss.reshape(-1).to(grad.dtype)])
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.path_group)
+            grad = buf[: grad.numel()].view_as(grad)
+            loss = buf[grad.numel():].view(B).to(loss.dtype)
+        return loss, grad
+
+    def gather_losses(self, loss: torch.Tensor, B_total: int) -> torch.Tensor:
+        """All per-signal losses (logging only), ordered by signal index."""
+        out = [torch.zeros_like(loss) for _ in range(self.world)]
+        dist.all_gather(out, loss)
+        parts = [out[g * self.path_shards] for g in range(self.n_batch_groups)]
+        return torch.cat(parts)[:B_total]

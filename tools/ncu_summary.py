@@ -1,0 +1,66 @@
+"""Summarise ncu outputs brought back in gpurun_out/ into text files under profiles/.
+
+  python tools/ncu_summary.py launches <launches.csv> <out.txt>    # per-kernel time shares
+  python tools/ncu_summary.py full <report.ncu-rep> <out.txt>       # key metrics per captured launch
+"""
+import collections
+import csv
+import subprocess
+import sys
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    tot = 0.0
+    for r in rows[hdr + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", ""))
+        v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[ui], 1e-6)
+        name = r[ki].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += v
+        tot += v
+    with open(out, "w") as f:
+        f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
+        f.write(f"# source: {path}\n# kernel, launches, total ms, share\n")
+        for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            f.write(f"{k:45s} {n:6d} {v:12.3f} {100 * v / tot:7.2f}%\n")
+        f.write(f"TOTAL {tot:.3f} ms\n")
+
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
+        "smsp__pcsamp_warps_issue_stalled_short_scoreboard", "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
+        "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle", "smsp__pcsamp_warps_issue_stalled_barrier",
+        "smsp__pcsamp_warps_issue_stalled_wait", "smsp__pcsamp_warps_issue_stalled_not_selected",
+        "smsp__pcsamp_warps_issue_stalled_selected", "smsp__pcsamp_warps_issue_stalled_mio_throttle"]
+
+
+def full(path, out):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    h, units = rows[0], rows[1]
+    with open(out, "w") as f:
+        f.write(f"# ncu --set full summary of {path}\n")
+        for r in rows[2:]:
+            d = dict(zip(h, r))
+            f.write(f"\n== {d.get('Kernel Name', '?')[:100]}  grid={d.get('Grid Size', '')} block={d.get('Block Size', '')}\n")
+            for k in KEYS:
+                for col in h:
+                    if col == k and d.get(col, "") != "":
+                        f.write(f"  {k:75s} {d[col]} {units[h.index(col)]}\n")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
