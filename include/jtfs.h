@@ -145,6 +145,11 @@ const char* jtfs_last_error(void);
 jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_t B, void* out,
                              size_t out_bytes, void* ws, size_t ws_bytes, jtfs_stream_t stream);
 
+/* Test-only: one-CTA tcgen05 kind::tf32 GEMM D[128][N] = A[128][K] . B[N][K]^T (3xTF32 if three)
+ * with B given as a device image in the canonical K-major layout ([hi | lo], see tc.cuh). */
+jtfs_status jtfs_debug_tc_gemm(const float* A, const float* Bimg, float* D, int N, int K, int three,
+                               jtfs_stream_t stream);
+
 /* Number of kernels the library has launched in this process (for launch-count reporting). */
 int64_t jtfs_launch_count(void);
 

@@ -9,6 +9,14 @@
 
 namespace jtfs {
 
+struct TcClass {
+  TcBlock* blocks = nullptr;
+  int64_t* tiles = nullptr;
+  int n_blocks = 0;
+  int64_t ntiles = 0;
+  int K2max = 0;
+};
+
 struct DeviceTables {
   float* spec_vals = nullptr;
   GatherJob* l1_jobs = nullptr;     int64_t* l1_tiles = nullptr;   int n_l1 = 0;   int64_t l1_ntiles = 0;
@@ -41,6 +49,11 @@ struct DeviceTables {
   int64_t* o1_rlo = nullptr;        int64_t* o1_nrows = nullptr;
   float2* tw = nullptr;
   int Kmax = 0;
+  // tensor-core joint stage
+  float* tc_img = nullptr;
+  float* tc_wts = nullptr;
+  TcUnit* tc_units = nullptr;
+  TcClass tc[kTcClasses];
 };
 
 constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels
@@ -88,6 +101,8 @@ void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S
                  cudaStream_t st);
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
                      int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);
+void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
+                         int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, int shard, int n_shards, int B,
                       cudaStream_t st);

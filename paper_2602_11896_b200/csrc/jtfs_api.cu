@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -16,6 +17,12 @@
 #include "fft.cuh"
 
 namespace jtfs {
+// JTFS_TC=0 in the environment keeps the joint-stage forward on the FP32 CUDA-core kernel (A/B
+// comparison in tests and profiling); both are GPU kernels of this library.
+static const bool g_use_tc = [] {
+  const char* e = std::getenv("JTFS_TC");
+  return !(e && e[0] == '0');
+}();
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches += n; }
 
@@ -88,6 +95,13 @@ static void free_tables(DeviceTables* d) {
     if (d->fwd_ulist[c]) cudaFree(d->fwd_ulist[c]);
     if (d->fwd_tiles[c]) cudaFree(d->fwd_tiles[c]);
   }
+  for (int c = 0; c < kTcClasses; ++c) {
+    if (d->tc[c].blocks) cudaFree(d->tc[c].blocks);
+    if (d->tc[c].tiles) cudaFree(d->tc[c].tiles);
+  }
+  if (d->tc_img) cudaFree(d->tc_img);
+  if (d->tc_wts) cudaFree(d->tc_wts);
+  if (d->tc_units) cudaFree(d->tc_units);
   delete d;
 }
 
@@ -132,6 +146,7 @@ static cudaError_t upload(Plan& p) {
     std::vector<int64_t> cnt;
     for (size_t u = 0; u < p.units.size(); ++u) {
       int ro = p.units[u].rows_out;
+      if (g_use_tc && p.blk_tc[p.units[u].bi]) continue;   // on the tensor-core path
       int cls = 0;
       while (kaps[cls] < ro) ++cls;
       if (cls != c) continue;
@@ -145,6 +160,29 @@ static cudaError_t upload(Plan& p) {
       UP(ul, fwd_ulist[c]);
       UP(t, fwd_tiles[c]);
       d->fwd_ntiles[c] = t.back();
+    }
+  }
+  // tensor-core classes
+  UP(p.tc_img, tc_img); UP(p.tc_wts, tc_wts); UP(p.tc_units, tc_units);
+  for (int c = 0; c < kTcClasses; ++c) {
+    std::vector<TcBlock> bl;
+    std::vector<int64_t> cnt;
+    int k2 = 0;
+    if (g_use_tc)
+      for (auto& tb : p.tc_blocks)
+        if (tb.cls == c) {
+          bl.push_back(tb);
+          const int CT = c < 3 ? 2 : 1;
+          cnt.push_back((p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT));
+          k2 = std::max(k2, tb.K2);
+        }
+    d->tc[c].n_blocks = (int)bl.size();
+    d->tc[c].K2max = k2;
+    if (!bl.empty()) {
+      t = prefix(cnt);
+      UP(bl, tc[c].blocks);
+      UP(t, tc[c].tiles);
+      d->tc[c].ntiles = t.back();
     }
   }
   std::vector<int32_t> kf;
@@ -300,7 +338,10 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     RET();
     if (stop == 3) return cudaSuccess;
     // A5: joint lambda_1 stage + phi_F; A6: phi_T
+    prof_begin(st, 0);
+    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
     launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
+    prof_end(st, 0);
     launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, shard, n_shards, mb, st);
   }
   RET();

@@ -623,14 +623,12 @@ static void launch_joint_fwd_kap(const Plan& p, const DeviceTables& d, int ci, c
 
 void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
                       int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st) {
-  prof_begin(st, 0);
   launch_joint_fwd_kap<1>(p, d, 0, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
   launch_joint_fwd_kap<2>(p, d, 1, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
   launch_joint_fwd_kap<4>(p, d, 2, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
   launch_joint_fwd_kap<8>(p, d, 3, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
   launch_joint_fwd_kap<16>(p, d, 4, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
   launch_joint_fwd_kap<32>(p, d, 5, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
-  prof_end(st, 0);
 }
 
 void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,

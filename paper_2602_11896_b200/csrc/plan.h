@@ -55,7 +55,17 @@ struct BlockInfo {
   int32_t s2, D;                 // level, decimation 2^(log2T - s2)
 };
 
-struct DeviceTables;  // device pointers (plan.cu)
+// Tensor-core (tcgen05) joint-stage tables (kernels_tc.cu)
+struct TcUnit {
+  int64_t img_off, wt_off;   // offsets (floats) of the unit's B images / phi_F weights
+  int32_t NT, pad;           // row tiles of 64 (0 = unit not on the tensor-core path)
+};
+struct TcBlock {
+  int32_t bi, K, K2, cls;    // block, n1_max, padded 2K, launch class
+};
+constexpr int kTcClasses = 6;   // (CT, KAP) = (2,2) (2,4) (2,8) (1,2) (1,4) (1,8)
+
+struct DeviceTables;  // device pointers (jtfs_api.cu)
 
 struct Plan {
   // ---- hyper-parameters
@@ -85,6 +95,11 @@ struct Plan {
   std::vector<Support> psi2_sup;                // [n_blocks][log2T+1] on N_pad>>k (len 0 unused)
   std::vector<Support> phiT_sup;                // [log2T+1] on N_pad>>k
   std::vector<float> hfr;                       // [n_fr_all][P][2] row kernels (complex)
+  std::vector<double> hfr_d;                    // same in float64 (for the tensor-core images)
+  std::vector<TcUnit> tc_units;                 // [n_units]
+  std::vector<TcBlock> tc_blocks;               // tensor-core eligible blocks
+  std::vector<char> blk_tc;                     // [n_blocks] 1 = on the tensor-core path
+  std::vector<float> tc_img, tc_wts;
   std::vector<float> phiF_k;                    // concat over k of P>>k real kernels
   std::vector<int64_t> phiF_off;                // [log2F+1]
   std::vector<float> phiT_half;                 // concat over s of half kernels t_s[0..H_s]

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include <utility>
 #include <vector>
@@ -140,6 +141,88 @@ static int ilog2(int64_t n) {
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static int64_t pmod(int64_t a, int64_t m) { return ((a % m) + m) % m; }
 
+// tf32 rounding identical to cvt.rna.tf32.f32 (nearest, ties away from zero, 13 bits dropped)
+static float tf32_rna_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+static uint32_t core_off_host(uint32_t r, uint32_t k, uint32_t Kc) {
+  return (r >> 3) * (Kc * 32u) + (k >> 2) * 128u + (r & 7u) * 16u + (k & 3u) * 4u;
+}
+
+// Tensor-core images (kernels_tc.cu): for every unit of an eligible block (K <= 60, rows_out <= 8)
+// and every row tile of 64 rows, B = [[Re M, -Im M], [Im M, Re M]] (interleaved) split into tf32
+// hi/lo, in K-chunks of 32 in the canonical K-major layout; plus the phi_F weights per row.
+static void build_tc_tables(Plan* p) {
+  const int nfr = (int)p->L_fr.size();
+  p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0});
+  p->blk_tc.assign(p->blocks.size(), 0);
+  for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
+    const int K = p->blocks[bi].n1_max;
+    const int K2 = ((2 * K + 7) / 8) * 8;
+    int ro_max = 0;
+    for (int f = 0; f < nfr; ++f) ro_max = std::max(ro_max, p->units[bi * nfr + f].rows_out);
+    if (K2 > 120 || ro_max > 8) continue;
+    const int CT = K2 <= 64 ? 2 : 1;
+    const int kap = ro_max <= 2 ? 0 : (ro_max <= 4 ? 1 : 2);
+    p->blk_tc[bi] = 1;
+    p->tc_blocks.push_back({(int32_t)bi, K, K2, (CT == 2 ? 0 : 3) + kap});
+    for (int f = 0; f < nfr; ++f) {
+      const int u = (int)bi * nfr + f;
+      const JointUnit& U = p->units[u];
+      TcUnit tu{};
+      tu.NT = (int32_t)((U.n_rows + 63) / 64);
+      tu.img_off = (int64_t)p->tc_img.size();
+      tu.wt_off = (int64_t)p->tc_wts.size();
+      const double* h = p->hfr_d.data() + (size_t)U.f * p->P * 2;
+      for (int t = 0; t < tu.NT; ++t) {
+        for (int ch = 0; ch * 32 < K2; ++ch) {
+          const int kc = std::min(32, K2 - ch * 32);
+          const size_t base = p->tc_img.size();
+          p->tc_img.resize(base + 2 * 128 * kc, 0.f);
+          for (int nn = 0; nn < 128; ++nn) {
+            const int i = nn / 2, po = nn % 2;
+            const int64_t lr = (int64_t)t * 64 + i;
+            if (lr >= U.n_rows) continue;
+            const int64_t r = (U.r_lo + lr) % U.Lf;
+            for (int kl = 0; kl < kc; ++kl) {
+              const int kk = ch * 32 + kl, n = kk / 2, pi = kk % 2;
+              if (n >= K) continue;
+              const int64_t e = (((r << U.kf) - n) % p->P + p->P) % p->P;
+              const double mr = h[2 * e], mi = h[2 * e + 1];
+              double v;
+              if (po == 0) v = (pi == 0) ? mr : -mi;   // Re W = Re M Re Y - Im M Im Y
+              else v = (pi == 0) ? mi : mr;            // Im W = Im M Re Y + Re M Im Y
+              const float xf = (float)v;
+              const float hi = tf32_rna_host(xf);
+              const float lo = tf32_rna_host(xf - hi);
+              const uint32_t o = core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kc) / 4;
+              p->tc_img[base + o] = hi;
+              p->tc_img[base + 128 * kc + o] = lo;
+            }
+          }
+        }
+      }
+      // phi_F weights g_kf[(rho 2^d - r) mod L_f] per (rho, local row), 0 beyond n_rows
+      const float* g = p->phiF_k.data() + p->phiF_off[U.kf];
+      for (int rho = 0; rho < U.rows_out; ++rho)
+        for (int64_t lr = 0; lr < (int64_t)tu.NT * 64; ++lr) {
+          float w = 0.f;
+          if (lr < U.n_rows) {
+            const int64_t r = (U.r_lo + lr) % U.Lf;
+            w = g[((((int64_t)rho << U.d) - r) % U.Lf + U.Lf) % U.Lf];
+          }
+          p->tc_wts.push_back(w);
+        }
+      p->tc_units[u] = tu;
+    }
+  }
+}
+
 int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, Plan* p,
               std::string* err) {
   auto ispow2 = [](int64_t v) { return v >= 1 && (v & (v - 1)) == 0; };
@@ -276,6 +359,8 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
       time_kernel(p->L_fr[f], p->P, 0, n, &re, &im);
       p->hfr[((size_t)f * p->P + n) * 2] = (float)re;
       p->hfr[((size_t)f * p->P + n) * 2 + 1] = (float)im;
+      p->hfr_d.push_back(re);
+      p->hfr_d.push_back(im);
     }
   // phi_F kernels at levels k = 0..log2F on P>>k grids; truncation half-widths (1e-9 rel)
   std::vector<int64_t> HF(log2F + 1);
@@ -351,6 +436,7 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     if (c - a + 1 >= Lf) { p->o1_rlo.push_back(0); p->o1_nrows.push_back(Lf); }
     else { p->o1_rlo.push_back(pmod(a, Lf)); p->o1_nrows.push_back(c - a + 1); }
   }
+  build_tc_tables(p);
   // adjoint d/dx spectrum gather: CSR of n1 touching each tile of N_pad bins
   int64_t ntile = ceil_div(p->N_pad, p->gx_tile);
   p->gx_tile_start.push_back(0);
