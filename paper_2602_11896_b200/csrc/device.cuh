@@ -54,6 +54,8 @@ struct DeviceTables {
   float* tc_wts = nullptr;
   TcUnit* tc_units = nullptr;
   TcClass tc[kTcClasses];
+  float* tc_img2 = nullptr;
+  TcClass tcb[3];
 };
 
 constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels
@@ -103,6 +105,9 @@ void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64
                      int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
                          int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
+void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
+                         int64_t go_sb, float2* gY, int64_t gy_sb, int shard, int n_shards, int B,
+                         cudaStream_t st);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, int shard, int n_shards, int B,
                       cudaStream_t st);

@@ -100,6 +100,11 @@ static void free_tables(DeviceTables* d) {
     if (d->tc[c].tiles) cudaFree(d->tc[c].tiles);
   }
   if (d->tc_img) cudaFree(d->tc_img);
+  if (d->tc_img2) cudaFree(d->tc_img2);
+  for (int c = 0; c < 3; ++c) {
+    if (d->tcb[c].blocks) cudaFree(d->tcb[c].blocks);
+    if (d->tcb[c].tiles) cudaFree(d->tcb[c].tiles);
+  }
   if (d->tc_wts) cudaFree(d->tc_wts);
   if (d->tc_units) cudaFree(d->tc_units);
   delete d;
@@ -185,6 +190,27 @@ static cudaError_t upload(Plan& p) {
       d->tc[c].ntiles = t.back();
     }
   }
+  UP(p.tc_img2, tc_img2);
+  for (int c = 0; c < 3; ++c) {
+    std::vector<TcBlock> bl;
+    std::vector<int64_t> cnt;
+    int k2 = 0;
+    if (g_use_tc)
+      for (auto& tb : p.tcb_blocks)
+        if (tb.cls == c) {
+          bl.push_back(tb);
+          cnt.push_back((p.binfo[tb.bi].n_cols + 127) / 128);
+          k2 = std::max(k2, tb.K2);
+        }
+    d->tcb[c].n_blocks = (int)bl.size();
+    d->tcb[c].K2max = k2;
+    if (!bl.empty()) {
+      t = prefix(cnt);
+      UP(bl, tcb[c].blocks);
+      UP(t, tcb[c].tiles);
+      d->tcb[c].ntiles = t.back();
+    }
+  }
   std::vector<int32_t> kf;
   for (auto& f : p.L_fr) kf.push_back(std::min(f.j, p.log2F));
   UP(kf, kf_of);
@@ -196,7 +222,7 @@ static cudaError_t upload(Plan& p) {
     d->Kmax = std::max(d->Kmax, p.blocks[bi].n1_max);
     int64_t ntc = (p.binfo[bi].n_cols + kJC - 1) / kJC;
     int64_t nr = (p.blocks[bi].n1_max + kJN - 1) / kJN;
-    bt.push_back(ntc * nr);
+    bt.push_back((g_use_tc && p.blk_tcb[bi]) ? 0 : ntc * nr);   // TC-backward blocks: no SIMT tiles
   }
   UP(nm, blk_nmax);
   t = prefix(bt); UP(t, bwd_tiles); d->bwd_ntiles = t.back();
@@ -358,7 +384,10 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     // A7: phi_T adjoint (r -> g_o, reusing o), joint adjoint (-> g_Y2 in A)
     launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, shard, n_shards, mb, st);
     if ((e = cudaMemsetAsync(w.A, 0, (size_t)w.s_A * 8 * mb, st))) return e;
+    prof_begin(st, 1);
+    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, shard, n_shards, mb, st);
     launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, shard, n_shards, mb, st);
+    prof_end(st, 1);
     // FFT of g_Y2 rows -> G_Y (into Y2)
     for (auto& g : p.y2_groups) {
       Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};

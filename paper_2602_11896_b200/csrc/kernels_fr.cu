@@ -665,12 +665,11 @@ void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, in
   size_t sm = (size_t)d.Kmax * kJC * 8 + (size_t)p.P * 8 + (size_t)kJR * kJC * 8 + (size_t)d.maxLf * 4 +
               (size_t)32 * kJC * 4 + 64 * 4;
   cudaFuncSetAttribute(k_joint_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (d.bwd_ntiles == 0) return;
   dim3 g((unsigned)d.bwd_ntiles, (unsigned)B);
-  prof_begin(st, 1);
   k_joint_bwd<<<g, 256, sm, st>>>(Y2, y_sb, go, go_sb, gY2, gy_sb, d.units, (int)p.L_fr.size(), d.bwd_tiles,
                                   d.n_blocks, d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, shard, n_shards,
                                   d.maxLf);
-  prof_end(st, 1);
   count_launch();
 }
 

@@ -18,6 +18,8 @@
 #include "device.cuh"
 #include "tc.cuh"
 
+#include <algorithm>
+
 namespace jtfs {
 
 constexpr int kTcRows = 64;         // lambda_1 rows per row tile (N = 128)
@@ -272,6 +274,333 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
       case 3: launch_tc<1, 2>(a, C.K2max, C.ntiles, B, st); break;
       case 4: launch_tc<1, 4>(a, C.K2max, C.ntiles, B, st); break;
       case 5: launch_tc<1, 8>(a, C.K2max, C.ntiles, B, st); break;
+    }
+  }
+}
+
+
+// =====================================================================================
+// Joint stage BACKWARD on tcgen05 (R20-R22): per 32-row tile of each filter f
+//   GEMM1  D1[c][2r+po]  = W recomputed (same B images as the forward, N = 64)
+//   epi    g_v = Phi_F^T g_o, g_W = (W/|W|) g_v  -> A2[c][2r+pi] (tf32 hi/lo, SMEM)
+//   GEMM2  D2[c][2n+po] += sum_kk A2[c][kk] B2[2n+po][kk],  B2 = [[Re M, Im M], [-Im M, Re M]]^T
+//          i.e. g_Y2^T += g_W^T conj(M_f), accumulated in TMEM over all filters and row tiles.
+// The MMA warp issues GEMM1 of tile g+1 before GEMM2 of tile g so the tensor core works while the
+// epilogue turns D1(g) into A2(g). 3xTF32 for both products.
+// =====================================================================================
+constexpr int kBwRows = 32;          // rows per backward tile (GEMM1 N = 64, GEMM2 K = 64)
+constexpr int kBwN1 = 2 * kBwRows;
+
+struct TcBwArgs {
+  const float2* Y2; int64_t y_sb;
+  const float* go; int64_t go_sb;
+  float2* gY; int64_t gy_sb;
+  const JointUnit* units; const BlockInfo* binfo;
+  const TcBlock* blocks; const int64_t* tiles; int n_tc_blocks;
+  const float* img;                 // forward B images (64-row tiles, 32-wide chunks)
+  const float* img2;                // backward B2 images [unit][tile32][hi|lo][N2 x 64]
+  const float* wts;
+  const TcUnit* tcu;
+  int nfr, shard, n_shards;
+};
+
+template <int KAP>
+__global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS, int STG) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull[2], tempty[2], a2full, a2empty, d2full;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int jb = find_tc(a.tiles, a.n_tc_blocks, blockIdx.x);
+  const TcBlock TB = a.blocks[jb];
+  const BlockInfo bf = a.binfo[TB.bi];
+  const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)128;
+  const int b = blockIdx.y;
+  const int K = TB.K, K2 = TB.K2;
+  const int N2 = ((2 * K + 15) / 16) * 16;
+  float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2]
+  float* a_lo = a_hi + 128 * K2;
+  float* a2_hi = a_lo + 128 * K2;                       // [128][64]
+  float* a2_lo = a2_hi + 128 * 64;
+  float* bst = a2_lo + 128 * 64;                        // NS x STG floats
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
+    tc::mbar_init(&a2full, 8);
+    tc::mbar_init(&a2empty, 1);
+    tc::mbar_init(&d2full, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, 256);
+  const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off;
+  for (int idx = tid; idx < 128 * (K2 / 2); idx += kTcThreads) {
+    const int c = idx & 127;
+    const int n = idx >> 7;
+    const int64_t col = col0 + c;
+    float2 v = make_float2(0.f, 0.f);
+    if (n < K && col < bf.n_cols) v = ysrc[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2];
+    float h0, l0, h1, l1;
+    tc::split_tf32(v.x, h0, l0);
+    tc::split_tf32(v.y, h1, l1);
+    const uint32_t o = tc::core_off((uint32_t)c, (uint32_t)(2 * n), (uint32_t)K2) / 4;
+    *reinterpret_cast<float2*>(a_hi + o) = make_float2(h0, h1);
+    *reinterpret_cast<float2*>(a_lo + o) = make_float2(l0, l1);
+  }
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const uint32_t d2 = tbase + 128;               // D2 accumulator columns [128, 128 + N2)
+  const int nchunks = (K2 + kTcKc - 1) / kTcKc;
+
+  if (warp == 0) {
+    // ===================== producer: B1(g+1) before B2(g), matching the MMA issue order
+    int stage = 0;
+    uint32_t ph = 0;
+    auto push_b1 = [&](const TcUnit& tu, int t32) {
+      // half (rows 32*(t32&1) ..) of the forward 64-row image, all chunks, hi then lo per chunk
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      if (tc::elect_one()) {
+        uint32_t total = (uint32_t)(2 * kBwN1 * K2 * 4);
+        tc::mbar_expect_tx(&full[stage], total);
+        const float* src = a.img + tu.img_off + (int64_t)(t32 >> 1) * (2 * kTcN * K2);
+        float* dst = bst + stage * STG;
+        const int half = t32 & 1;
+        for (int ch = 0; ch < nchunks; ++ch) {
+          const int kc = min(kTcKc, K2 - ch * kTcKc);
+          const uint32_t hb = (uint32_t)(kBwN1 * kc * 4);
+          tc::bulk_g2s(dst, src + half * kBwN1 * kc, hb, &full[stage]);                     // hi half
+          tc::bulk_g2s(dst + kBwN1 * kc, src + kTcN * kc + half * kBwN1 * kc, hb, &full[stage]);  // lo half
+          dst += 2 * kBwN1 * kc;
+          src += 2 * kTcN * kc;
+        }
+      }
+      __syncwarp();
+      if (++stage == NS) { stage = 0; ph ^= 1; }
+    };
+    auto push_b2 = [&](const TcUnit& tu, int t32) {
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      if (tc::elect_one()) {
+        const uint32_t bytes = (uint32_t)(2 * N2 * 64 * 4);
+        tc::mbar_expect_tx(&full[stage], bytes);
+        tc::bulk_g2s(bst + stage * STG, a.img2 + tu.img2_off + (int64_t)t32 * (2 * N2 * 64), bytes, &full[stage]);
+      }
+      __syncwarp();
+      if (++stage == NS) { stage = 0; ph ^= 1; }
+    };
+    bool have_prev = false;
+    TcUnit pu{};
+    int pt = 0;
+    for (int f = 0; f < a.nfr; ++f) {
+      const int u = TB.bi * a.nfr + f;
+      if (u % a.n_shards != a.shard) continue;
+      const TcUnit tu = a.tcu[u];
+      const int NT32 = (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
+      for (int t = 0; t < NT32; ++t) {
+        push_b1(tu, t);                    // B1(g) ...
+        if (have_prev) push_b2(pu, pt);    // ... then B2(g-1)
+        have_prev = true; pu = tu; pt = t;
+      }
+    }
+    if (have_prev) push_b2(pu, pt);
+  } else if (warp == 1) {
+    // ===================== MMA issuer
+    const uint32_t idesc1 = tc::idesc_tf32(128, kBwN1);
+    const uint32_t idesc2 = tc::idesc_tf32(128, (uint32_t)N2);
+    const uint32_t sboA = (uint32_t)K2 * 32u;
+    const uint64_t dA_hi = tc::sdesc(tc::smem_u32(a_hi), 128, sboA);
+    const uint64_t dA_lo = tc::sdesc(tc::smem_u32(a_lo), 128, sboA);
+    const uint64_t dA2_hi = tc::sdesc(tc::smem_u32(a2_hi), 128, 64u * 32u);
+    const uint64_t dA2_lo = tc::sdesc(tc::smem_u32(a2_lo), 128, 64u * 32u);
+    const uint32_t bst_s = tc::smem_u32(bst);
+    int stage = 0, buf = 0;
+    uint32_t ph = 0, bph = 0;
+    int g2 = 0;   // GEMM2 count
+    auto gemm1 = [&]() {
+      tc::mbar_wait(&tempty[buf], bph ^ 1);
+      tc::mbar_wait(&full[stage], ph);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        uint32_t off = bst_s + (uint32_t)(stage * STG * 4);
+        const uint32_t d = tbase + (uint32_t)(buf * kBwN1);
+        for (int ch = 0; ch < nchunks; ++ch) {
+          const int kc = min(kTcKc, K2 - ch * kTcKc);
+          const uint64_t dbh = tc::sdesc(off, 128, (uint32_t)kc * 32u);
+          const uint64_t dbl = tc::sdesc(off + (uint32_t)(kBwN1 * kc * 4), 128, (uint32_t)kc * 32u);
+          for (int ks = 0; ks < kc / 8; ++ks) {
+            const uint32_t kg = (uint32_t)(ch * (kTcKc / 8) + ks);
+            tc::mma_tf32(d, dA_hi + 16u * kg, dbh + 16u * ks, idesc1, (ch > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_tf32(d, dA_hi + 16u * kg, dbl + 16u * ks, idesc1, 1u);
+            tc::mma_tf32(d, dA_lo + 16u * kg, dbh + 16u * ks, idesc1, 1u);
+          }
+          off += (uint32_t)(2 * kBwN1 * kc * 4);
+        }
+        tc::mma_commit(&empty[stage]);
+        tc::mma_commit(&tfull[buf]);
+      }
+      __syncwarp();
+      if (++stage == NS) { stage = 0; ph ^= 1; }
+      if (++buf == 2) { buf = 0; bph ^= 1; }
+    };
+    auto gemm2 = [&]() {
+      tc::mbar_wait(&a2full, (uint32_t)(g2 & 1));
+      tc::mbar_wait(&full[stage], ph);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t bh = bst_s + (uint32_t)(stage * STG * 4);
+        const uint64_t dbh = tc::sdesc(bh, 128, 64u * 32u);
+        const uint64_t dbl = tc::sdesc(bh + (uint32_t)(N2 * 64 * 4), 128, 64u * 32u);
+        for (int ks = 0; ks < 8; ++ks) {
+          tc::mma_tf32(d2, dA2_hi + 16u * ks, dbh + 16u * ks, idesc2, (g2 > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_tf32(d2, dA2_hi + 16u * ks, dbl + 16u * ks, idesc2, 1u);
+          tc::mma_tf32(d2, dA2_lo + 16u * ks, dbh + 16u * ks, idesc2, 1u);
+        }
+        tc::mma_commit(&empty[stage]);
+        tc::mma_commit(&a2empty);
+      }
+      __syncwarp();
+      if (++stage == NS) { stage = 0; ph ^= 1; }
+      ++g2;
+    };
+    int G = 0;
+    for (int f = 0; f < a.nfr; ++f) {
+      const int u = TB.bi * a.nfr + f;
+      if (u % a.n_shards != a.shard) continue;
+      G += (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
+    }
+    if (G > 0) gemm1();
+    for (int g = 0; g < G; ++g) {
+      if (g + 1 < G) gemm1();
+      gemm2();
+    }
+    if (tc::elect_one()) tc::mma_commit(&d2full);
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===================== epilogue
+    const int e = warp - 4;
+    const int q = e & 3, h = e >> 2;        // lane quadrant, row half (16 rows)
+    const int c = q * 32 + lane;
+    const int64_t colg = col0 + c;
+    int buf = 0;
+    uint32_t bph = 0;
+    int g = 0;
+    for (int f = 0; f < a.nfr; ++f) {
+      const int u = TB.bi * a.nfr + f;
+      if (u % a.n_shards != a.shard) continue;
+      const JointUnit U = a.units[u];
+      const TcUnit tu = a.tcu[u];
+      const int ro = U.rows_out;
+      const float* wt = a.wts + tu.wt_off;
+      const int ldw = tu.NT * kTcRows;
+      float gor[KAP];
+#pragma unroll
+      for (int r = 0; r < KAP; ++r)
+        gor[r] = (r < ro && colg < bf.n_cols) ? a.go[b * a.go_sb + U.o_off + (int64_t)r * bf.n_cols + colg] : 0.f;
+      const int NT32 = (int)((U.n_rows + kBwRows - 1) / kBwRows);
+      for (int t = 0; t < NT32; ++t, ++g) {
+        // lanes 0..15 hold the weights of rows t*32 + h*16 + lane
+        float wl[KAP];
+#pragma unroll
+        for (int r = 0; r < KAP; ++r)
+          wl[r] = (r < ro && lane < 16) ? __ldg(wt + r * ldw + t * kBwRows + h * 16 + lane) : 0.f;
+        tc::mbar_wait(&tfull[buf], bph);
+        tc::tc_fence_after();
+        float v[32];
+        const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kBwN1 + h * 32);
+        tc::tmem_ld16_nowait(ta, v);
+        tc::tmem_ld16_nowait(ta + 16, v + 16);
+        tc::tmem_wait_ld();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        if (++buf == 2) { buf = 0; bph ^= 1; }
+        float gw[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float gv = 0.f;
+#pragma unroll
+          for (int r = 0; r < KAP; ++r) gv = fmaf(__shfl_sync(0xffffffffu, wl[r], i), gor[r], gv);
+          const float re = v[2 * i], im = v[2 * i + 1];
+          const float m2 = fmaf(re, re, im * im);
+          const float s = m2 > 1.17549435e-38f ? gv * rsqrtf(m2) : 0.f;
+          gw[2 * i] = re * s;
+          gw[2 * i + 1] = im * s;
+        }
+        // A2 is free once GEMM2(g-1) completed
+        tc::mbar_wait(&a2empty, (uint32_t)((g & 1) ^ 1));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 hv, lv;
+          tc::split_tf32(gw[4 * j + 0], hv.x, lv.x);
+          tc::split_tf32(gw[4 * j + 1], hv.y, lv.y);
+          tc::split_tf32(gw[4 * j + 2], hv.z, lv.z);
+          tc::split_tf32(gw[4 * j + 3], hv.w, lv.w);
+          const uint32_t o = tc::core_off((uint32_t)c, (uint32_t)(h * 32 + 4 * j), 64u) / 4;
+          *reinterpret_cast<float4*>(a2_hi + o) = hv;
+          *reinterpret_cast<float4*>(a2_lo + o) = lv;
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&a2full);
+      }
+    }
+    // final: D2 (g_Y2^T for this column tile) -> g_Y2[n][col]
+    if (g > 0) {
+      tc::mbar_wait(&d2full, 0);
+      tc::tc_fence_after();
+    }
+    if (h == 0) {
+      float2* dst = a.gY + b * a.gy_sb + bf.y_off + (bf.c_lo + (colg < bf.n_cols ? colg : 0)) % bf.T2;
+      for (int c0 = 0; c0 < N2; c0 += 16) {
+        float v[16];
+        if (g > 0) {
+          tc::tmem_ld16(d2 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (colg < bf.n_cols) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int n = c0 / 2 + i;
+            if (n < K) dst[(int64_t)n * bf.T2] = make_float2(v[2 * i], v[2 * i + 1]);
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 256);
+}
+
+template <int KAP>
+static void launch_tc_bwd(const TcBwArgs& a, int K2max, int64_t ntiles, int B, cudaStream_t st) {
+  const int N2max = ((K2max + 15) / 16) * 16;
+  const int STG = std::max(2 * kBwN1 * K2max, 2 * N2max * 64);
+  int NS = kTcMaxStages;
+  auto smem = [&](int ns) { return (size_t)(2 * 128 * K2max + 2 * 128 * 64 + ns * STG) * 4 + 1024; };
+  while (NS > 2 && smem(NS) > 225 * 1024) --NS;
+  const size_t sm = smem(NS);
+  cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 g((unsigned)ntiles, (unsigned)B);
+  k_joint_bwd_tc<KAP><<<g, kTcThreads, sm, st>>>(a, NS, STG);
+  count_launch();
+}
+
+void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
+                         int64_t go_sb, float2* gY, int64_t gy_sb, int shard, int n_shards, int B,
+                         cudaStream_t st) {
+  for (int cls = 0; cls < 3; ++cls) {
+    const TcClass& C = d.tcb[cls];
+    if (C.n_blocks == 0) continue;
+    TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
+               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards};
+    switch (cls) {
+      case 0: launch_tc_bwd<2>(a, C.K2max, C.ntiles, B, st); break;
+      case 1: launch_tc_bwd<4>(a, C.K2max, C.ntiles, B, st); break;
+      case 2: launch_tc_bwd<8>(a, C.K2max, C.ntiles, B, st); break;
     }
   }
 }

@@ -58,6 +58,7 @@ struct BlockInfo {
 // Tensor-core (tcgen05) joint-stage tables (kernels_tc.cu)
 struct TcUnit {
   int64_t img_off, wt_off;   // offsets (floats) of the unit's B images / phi_F weights
+  int64_t img2_off;          // offset of the backward B2 images (32-row tiles)
   int32_t NT, pad;           // row tiles of 64 (0 = unit not on the tensor-core path)
 };
 struct TcBlock {
@@ -98,8 +99,10 @@ struct Plan {
   std::vector<double> hfr_d;                    // same in float64 (for the tensor-core images)
   std::vector<TcUnit> tc_units;                 // [n_units]
   std::vector<TcBlock> tc_blocks;               // tensor-core eligible blocks
-  std::vector<char> blk_tc;                     // [n_blocks] 1 = on the tensor-core path
-  std::vector<float> tc_img, tc_wts;
+  std::vector<char> blk_tc;                     // [n_blocks] 1 = forward on the tensor-core path
+  std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
+  std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class 0..2)
+  std::vector<float> tc_img, tc_wts, tc_img2;
   std::vector<float> phiF_k;                    // concat over k of P>>k real kernels
   std::vector<int64_t> phiF_off;                // [log2F+1]
   std::vector<float> phiT_half;                 // concat over s of half kernels t_s[0..H_s]

@@ -159,8 +159,9 @@ static uint32_t core_off_host(uint32_t r, uint32_t k, uint32_t Kc) {
 // hi/lo, in K-chunks of 32 in the canonical K-major layout; plus the phi_F weights per row.
 static void build_tc_tables(Plan* p) {
   const int nfr = (int)p->L_fr.size();
-  p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0});
+  p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0, 0});
   p->blk_tc.assign(p->blocks.size(), 0);
+  p->blk_tcb.assign(p->blocks.size(), 0);
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
     const int K = p->blocks[bi].n1_max;
     const int K2 = ((2 * K + 7) / 8) * 8;
@@ -171,6 +172,12 @@ static void build_tc_tables(Plan* p) {
     const int kap = ro_max <= 2 ? 0 : (ro_max <= 4 ? 1 : 2);
     p->blk_tc[bi] = 1;
     p->tc_blocks.push_back({(int32_t)bi, K, K2, (CT == 2 ? 0 : 3) + kap});
+    const bool bwd = K2 <= 80;
+    if (bwd) {
+      p->blk_tcb[bi] = 1;
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap});
+    }
+    const int N2 = ((2 * K + 15) / 16) * 16;
     for (int f = 0; f < nfr; ++f) {
       const int u = (int)bi * nfr + f;
       const JointUnit& U = p->units[u];
@@ -203,6 +210,37 @@ static void build_tc_tables(Plan* p) {
               const uint32_t o = core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kc) / 4;
               p->tc_img[base + o] = hi;
               p->tc_img[base + 128 * kc + o] = lo;
+            }
+          }
+        }
+      }
+      // backward B2 images: per 32-row tile, [hi | lo] of N2 x 64 (canonical K-major),
+      // B2[2n][2i] = Re M, B2[2n][2i+1] = Im M, B2[2n+1][2i] = -Im M, B2[2n+1][2i+1] = Re M
+      if (bwd) {
+        tu.img2_off = (int64_t)p->tc_img2.size();
+        const int NT32 = (int)((U.n_rows + 31) / 32);
+        for (int t = 0; t < NT32; ++t) {
+          const size_t base = p->tc_img2.size();
+          p->tc_img2.resize(base + 2 * (size_t)N2 * 64, 0.f);
+          for (int nn = 0; nn < N2; ++nn) {
+            const int n = nn / 2, po = nn % 2;
+            if (n >= K) continue;
+            for (int kk = 0; kk < 64; ++kk) {
+              const int i = kk / 2, pi = kk % 2;
+              const int64_t lr = (int64_t)t * 32 + i;
+              if (lr >= U.n_rows) continue;
+              const int64_t r = (U.r_lo + lr) % U.Lf;
+              const int64_t e = (((r << U.kf) - n) % p->P + p->P) % p->P;
+              const double mr = h[2 * e], mi = h[2 * e + 1];
+              double v;
+              if (po == 0) v = (pi == 0) ? mr : mi;      // Re g_Y = Re M Re g_W + Im M Im g_W
+              else v = (pi == 0) ? -mi : mr;             // Im g_Y = -Im M Re g_W + Re M Im g_W
+              const float xf = (float)v;
+              const float hi = tf32_rna_host(xf);
+              const float lo = tf32_rna_host(xf - hi);
+              const uint32_t o = core_off_host((uint32_t)nn, (uint32_t)kk, 64u) / 4;
+              p->tc_img2[base + o] = hi;
+              p->tc_img2[base + (size_t)N2 * 64 + o] = lo;
             }
           }
         }
