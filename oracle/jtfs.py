@@ -51,6 +51,33 @@ class _Recompute(torch.autograd.Function):
         return gx, None
 
 
+# Reading R22 (modulus subgradient, after SPEC S:372's relative eps_mod): the phase z/|z| used by
+# the modulus adjoint is set to 0 where |z| <= MOD_TAU * max_t |y_b(t)| (per signal). The gradient
+# of |z| is ill-conditioned at |z| -> 0 (the phase of a vanishing quantity); the dead zone gives
+# both implementations one well-conditioned definition. The forward value |z| is unchanged.
+MOD_TAU = 1e-6
+
+
+class _ModulusDZ(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, z, thr):
+        a = z.abs()
+        ctx.save_for_backward(z, a, thr)
+        return a
+
+    @staticmethod
+    def backward(ctx, g):
+        z, a, thr = ctx.saved_tensors
+        keep = a > thr
+        phase = torch.where(keep, z / torch.where(keep, a, torch.ones_like(a)), torch.zeros_like(z))
+        return g * phase, None
+
+
+def modulus(z: torch.Tensor, thr: torch.Tensor) -> torch.Tensor:
+    """Complex modulus (Eq.2) with the R22 adjoint; thr broadcasts per signal."""
+    return _ModulusDZ.apply(z, thr.reshape((-1,) + (1,) * (z.dim() - 1)).to(z.real.dtype))
+
+
 def subsample_fourier(X: torch.Tensor, k: int, dim: int = -1) -> torch.Tensor:
     """P:199, P:208 'subsampling ... in the Fourier domain by reshaping and summation';
     SPEC S:65: out[m] = (1/k) sum_b X[m + b L/k] (equals decimation in time)."""
@@ -137,6 +164,7 @@ class Oracle:
     def layer1(self, x: torch.Tensor):
         """Padding (R10) + first layer + S0 + time-averaged S1 (Eq.3 time part)."""
         p = self.plan
+        self._thr = MOD_TAU * x.detach().abs().amax(dim=1)                  # R22 dead zone
         xp = x[:, self.src]
         U0_hat = torch.fft.fft(xp.to(C128))                                  # P:203 (rfft, full circle)
         S0 = torch.fft.ifft(subsample_fourier(U0_hat * self.phiT().to(C128), p.T)).real
@@ -145,7 +173,7 @@ class Oracle:
             k1 = p.k1(n1)
             U1_c = U0_hat * self.psi1(n1).to(C128)                           # P:207 cdgmm
             U1_hat = subsample_fourier(U1_c, 2 ** k1)
-            U1_m = torch.fft.ifft(U1_hat).abs()
+            U1_m = modulus(torch.fft.ifft(U1_hat), self._thr)
             U1_hat = torch.fft.fft(U1_m.to(C128))                            # P:211 (rfft, full circle)
             U1_hats.append(U1_hat)
             # S1 time part: U1 * phi_T at level k1, stride T (Eq.3; R14)
@@ -166,7 +194,7 @@ class Oracle:
             if f == 0:      # beta = 0: S1 = U1 *t phi_T *lambda phi_F  (Eq.3)
                 Y = W.real
             else:           # alpha = 0, beta > 0: phi_F * phi_T * |psi_beta * (phi_T * U1)|  (R14)
-                V = W.abs()
+                V = modulus(W, self._thr)
                 Vh = torch.fft.fft(V.to(C128), dim=-1)
                 V = torch.fft.ifft(Vh * self.lev(self.phiT(), p.log2T).to(C128), dim=-1).real
                 Y = self._phiF_rows(V, p.k_fr(f))
@@ -194,7 +222,7 @@ class Oracle:
         X_hat = torch.fft.fft(X_pad, dim=1)                                  # P:282 cfft
         outs = []
         for f in range(len(p.L_fr)):
-            V = self._freq_filter(X_hat, f).abs()                            # |U1 *t psi_a *l psi_b|
+            V = modulus(self._freq_filter(X_hat, f), self._thr)             # |U1 *t psi_a *l psi_b|
             outs.append(self._phiF_rows(V, p.k_fr(f))[:, :rows, :])
         return torch.stack(outs, dim=1)
 
@@ -254,12 +282,30 @@ class Oracle:
         r = (S_y - torch.as_tensor(S_target).to(F64)) * self.loss_weights()
         return 0.5 * (r * r).sum(dim=1)
 
+    def loss_grad_subset(self, y, S_target, blocks):
+        """R19's loss restricted to order 1 and the order-2 paths of `blocks` (used to sample the
+        large configurations): (E [B], dE/dy [B, N]) by reverse-mode autodiff."""
+        w = _subset_weights(self.plan, blocks)
+        y = torch.as_tensor(y).to(F64).detach().requires_grad_(True)
+        r = (self.forward(y, blocks=blocks) - torch.as_tensor(S_target).to(F64)) * w
+        E = 0.5 * (r * r).sum(dim=1)
+        (g,) = torch.autograd.grad(E.sum(), y)
+        return E.detach(), g.detach()
+
     def loss_grad(self, y, S_target):
         """(E [B], dE/dy [B, N]) — true gradient (R20), by reverse-mode autodiff."""
         y = torch.as_tensor(y).to(F64).detach().requires_grad_(True)
         E = self.loss(self.forward(y), S_target)
         (g,) = torch.autograd.grad(E.sum(), y)
         return E.detach(), g.detach()
+
+
+def _subset_weights(plan, blocks) -> torch.Tensor:
+    w = torch.zeros(plan.n_coef, dtype=F64)
+    for q in plan.paths:
+        if q.order == 1 or (q.order == 2 and q.block in blocks):
+            w[q.offset:q.offset + q.rows * q.frames] = 1.0
+    return w
 
 
 def coefficients(plan_args, x) -> np.ndarray:

@@ -48,6 +48,7 @@ struct DeviceTables {
   int32_t* gx_tile_start = nullptr; int32_t* gx_list = nullptr;
   int64_t* o1_rlo = nullptr;        int64_t* o1_nrows = nullptr;
   float2* tw = nullptr;
+  double2* twd = nullptr;
   int Kmax = 0;
   // tensor-core joint stage
   float* tc_img = nullptr;
@@ -64,9 +65,13 @@ constexpr int kJR = 64;            // joint stage: rows per chunk
 constexpr int kJN = 64;            // joint backward: n1 rows per CTA
 
 // ---- kernels_time.cu
-void launch_reflect_pad(const float* x, int64_t sx, float2* xp, const Plan& p, int B, cudaStream_t st);
+void launch_reflect_pad(const float* x, int64_t sx, double2* xp, const Plan& p, int B, cudaStream_t st);
 void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
                    const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
+void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
+                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
+void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
+                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
 void launch_modulus(const float2* z, int64_t zsb, float2* u, int64_t usb, int64_t n_per_b, int B,
                     cudaStream_t st);
 void launch_real_rows(const float2* in, int64_t in_sb, int64_t in_off, float* out, int64_t out_sb,
@@ -77,7 +82,10 @@ void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS
                           const float2* GY, int64_t GY_sb, float2* out, int64_t out_sb, int B,
                           cudaStream_t st);
 void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
-                      int B, cudaStream_t st);
+                      const float* thr, int B, cudaStream_t st);
+// reading R22: the modulus adjoint uses phase 0 where |z| <= kModTau * max_t |y_b(t)|
+constexpr float kModTau = 1e-6f;
+void launch_absmax(const float* y, int64_t N, float tau, float* thr, int B, cudaStream_t st);
 void launch_adj_gather_x(const Plan& p, const DeviceTables& d, const float2* GZ, int64_t GZ_sb, float2* out,
                          int64_t out_sb, int B, cudaStream_t st);
 void launch_real_to_complex(const float* in, int64_t in_sb, float2* out, int64_t out_sb, int64_t n, int B,
@@ -93,7 +101,7 @@ void launch_o1_fwd(const Plan& p, const DeviceTables& d, const float* S1t, int64
                    int64_t W1_sb, float* V2, int64_t V2_sb, float* S, int64_t S_sb, int B, cudaStream_t st);
 void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float2* W1,
                    int64_t W1_sb, float* V2, int64_t V2_sb, const float* S1t, int64_t S1t_sb, float* gS1t,
-                   int64_t gS1t_sb, int B, cudaStream_t st);
+                   int64_t gS1t_sb, const float* thr, int B, cudaStream_t st);
 void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
                       int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
 void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,
@@ -106,10 +114,10 @@ void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
                          int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                         int64_t go_sb, float2* gY, int64_t gy_sb, int shard, int n_shards, int B,
-                         cudaStream_t st);
+                         int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
+                         int B, cudaStream_t st);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                      int64_t go_sb, float2* gY2, int64_t gy_sb, int shard, int n_shards, int B,
+                      int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st);
 
 }  // namespace jtfs

@@ -88,7 +88,7 @@ static void free_tables(DeviceTables* d) {
                   d->s0_job, d->s0_tiles, d->psi1_sup, d->psi2_sup, d->phiT_sup, d->hfr, d->phiF_k,
                   d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
                   d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_owner_unit, d->l1_off,
-                  d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw};
+                  d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw, d->twd};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int c = 0; c < 6; ++c) {
@@ -252,6 +252,8 @@ static cudaError_t upload(Plan& p) {
   UP(p.o1_rlo, o1_rlo); UP(p.o1_nrows, o1_nrows);
   std::vector<float2> tw = fft_twiddle_table();
   UP(tw, tw);
+  std::vector<double2> twd = fft_twiddle_table_d();
+  UP(twd, twd);
   d->maxLf = (int)p.P;
 #undef UP
   p.dev = d;
@@ -274,16 +276,20 @@ static jtfs_status ensure_device(jtfs_plan_s* h) {
 // ------------------------------------------------------------------------------ workspace layout
 struct Layout {
   // per-signal sizes in bytes (each 256-aligned) of every buffer, in this order
-  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss;
-  size_t per_signal() const { return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss; }
+  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss, thr;
+  size_t per_signal() const {
+    return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss + thr;
+  }
 };
 static size_t al(size_t b) { return (b + 255) / 256 * 256; }
 static Layout layout(const Plan& p, int with_grad) {
   Layout L{};
   const int64_t nfr1 = 1 + (int64_t)p.psi_fr_plus.size();
   const int64_t N1 = (int64_t)p.psi1.size();
-  L.xp = al(p.N_pad * 8); L.Xh = al(p.N_pad * 8);
-  L.A = al(std::max(p.sumL1, p.sumY2) * 8);
+  // xp, Xh hold complex128 in the forward (float64 first layer), complex64 views in the backward;
+  // A holds the complex128 layer-1 spectra (sum L1) or complex64 (sum Y2, sum L1)
+  L.xp = al(p.N_pad * 16); L.Xh = al(p.N_pad * 16);
+  L.A = al(std::max(2 * p.sumL1, p.sumY2) * 8);
   L.Z1 = al(p.sumL1 * 8); L.U1h = al(p.sumL1 * 8); L.Y2 = al(std::max<int64_t>(p.sumY2, 1) * 8);
   L.cs = al((1 + N1) * p.Ft * 8); L.ct = L.cs;
   L.S1t = al(N1 * p.Ft * 4);
@@ -294,12 +300,13 @@ static Layout layout(const Plan& p, int with_grad) {
   L.gS1t = al(N1 * p.Ft * 4);
   L.g = with_grad ? al(p.N * 4) : 0;
   L.loss = 256;
+  L.thr = 256;
   return L;
 }
 
 struct Bufs {
   float2 *xp, *Xh, *A, *Z1, *U1h, *Y2, *cs, *ct, *W1;
-  float *S1t, *V2, *o, *S, *r, *gS1t, *g, *loss;
+  float *S1t, *V2, *o, *S, *r, *gS1t, *g, *loss, *thr;
   // per-signal strides in elements
   int64_t s_xp, s_A, s_L1, s_Y2, s_c, s_S1t, s_W1, s_V2, s_o, s_S, s_g;
 };
@@ -312,6 +319,8 @@ static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
   b.S1t = (float*)take(L.S1t); b.W1 = (float2*)take(L.W1); b.V2 = (float*)take(L.V2); b.o = (float*)take(L.o);
   b.S = (float*)take(L.S); b.r = (float*)take(L.r); b.gS1t = (float*)take(L.gS1t); b.g = (float*)take(L.g);
   b.loss = (float*)take(L.loss);
+  b.thr = (float*)take(L.thr);   // one float per signal (mb contiguous floats at the start)
+  // strides in complex64 units (complex128 views: half)
   b.s_xp = L.xp / 8; b.s_A = L.A / 8; b.s_L1 = L.Z1 / 8; b.s_Y2 = L.Y2 / 8; b.s_c = L.cs / 8;
   b.s_S1t = L.S1t / 4; b.s_W1 = L.W1 / 8; b.s_V2 = L.V2 / 4; b.s_o = L.o / 4; b.s_S = L.S / 4; b.s_g = L.g / 4;
   (void)p;
@@ -330,13 +339,23 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   const DeviceTables& d = *p.dev;
   cudaError_t e;
 #define RET() if ((e = cudaGetLastError()) != cudaSuccess) return e
-  // A1: reflect pad + FFT
-  launch_reflect_pad(x, sx, w.xp, p, mb, st);
-  if ((e = fft_rows(p, w.xp, w.s_xp, w.Xh, w.s_xp, 0, 1, p.N_pad, mb, false, st))) return e;
-  // A2: layer 1: cdgmm + subsample_fourier, ifft, modulus, fft
-  launch_gather(w.Xh, w.s_xp, w.A, w.s_A, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals, mb, st);
-  for (auto& g : p.l1_groups)
-    if ((e = fft_rows(p, w.A, w.s_A, w.Z1, w.s_L1, g.off, g.count, g.L, mb, true, st))) return e;
+  // A1: reflect pad + FFT in float64
+  double2* xpd = reinterpret_cast<double2*>(w.xp);
+  double2* Xhd = reinterpret_cast<double2*>(w.Xh);
+  double2* Ad = reinterpret_cast<double2*>(w.A);
+  const int64_t sd = w.s_xp / 2, sAd = w.s_A / 2;
+  launch_reflect_pad(x, sx, xpd, p, mb, st);
+  {
+    Rows ri{sd, 0, 1, p.N_pad}, ro{sd, 0, 1, p.N_pad};
+    if ((e = fft_launch_dd(xpd, Xhd, ri, ro, mb, false, d.twd, st))) return e;
+  }
+  // A2: layer 1: cdgmm + subsample_fourier (float64), ifft (float64 -> complex64 Z1),
+  // modulus, fft (complex64)
+  launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals, mb, st);
+  for (auto& g : p.l1_groups) {
+    Rows ri{sAd, g.off, g.count, g.L}, ro{w.s_L1, g.off, g.count, g.L};
+    if ((e = fft_launch_df(Ad, w.Z1, ri, ro, mb, true, d.twd, st))) return e;
+  }
   launch_modulus(w.Z1, w.s_L1, w.A, w.s_A, p.sumL1, mb, st);  // A rows use the L1 layout
   RET();
   if (stop == 1) return cudaSuccess;
@@ -345,7 +364,7 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     if ((e = fft_launch(w.A, w.U1h, ri, ro, mb, false, d.tw, st))) return e;
   }
   // S0 and S1 time averages (Eq.3 time part)
-  launch_gather(w.Xh, w.s_xp, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
+  launch_gather_df(Xhd, sd, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
   launch_gather(w.U1h, w.s_L1, w.cs + p.Ft, w.s_c, d.s1_jobs, d.s1_tiles, d.n_s1, d.s1_ntiles, d.spec_vals, mb, st);
   if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, 1 + (int64_t)p.psi1.size(), p.Ft, mb, true, st))) return e;
   launch_s0_out(w.ct, w.s_c, S, S_sb, p, mb, st);
@@ -385,8 +404,8 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, shard, n_shards, mb, st);
     if ((e = cudaMemsetAsync(w.A, 0, (size_t)w.s_A * 8 * mb, st))) return e;
     prof_begin(st, 1);
-    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, shard, n_shards, mb, st);
-    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, shard, n_shards, mb, st);
+    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
+    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
     prof_end(st, 1);
     // FFT of g_Y2 rows -> G_Y (into Y2)
     for (auto& g : p.y2_groups) {
@@ -395,7 +414,7 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     }
   }
   // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)
-  launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, mb, st);
+  launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, w.thr, mb, st);
   launch_real_to_complex(w.gS1t, w.s_S1t, w.cs, w.s_c, N1 * p.Ft, mb, st);
   if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, N1, p.Ft, mb, false, st))) return e;
   // A8: g_hat_U1 -> U1h ; g_U1 = Re IFFT -> A
@@ -405,7 +424,7 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, true, d.tw, st))) return e;
   }
   // A9: modulus adjoint, FFT, layer-1 adjoint gather, IFFT, reflect adjoint
-  launch_phase_mul(w.Z1, w.A, w.s_A, w.U1h, p.sumL1, w.s_L1, mb, st);  // Z1, U1h share the L1 stride
+  launch_phase_mul(w.Z1, w.A, w.s_A, w.U1h, p.sumL1, w.s_L1, w.thr, mb, st);  // Z1, U1h share the L1 stride
   for (auto& g : p.l1_groups) {
     Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
     if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, false, d.tw, st))) return e;
@@ -607,6 +626,7 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
     CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, shard, n_shards, st));
     float* lossp = mstate ? mstate->loss + b0 : loss + b0;
     launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, shard, n_shards, n, st);
+    launch_absmax(y + b0 * p.N, p.N, kModTau, w.thr, n, st);
     float* gp = mstate ? w.g : grad + b0 * p.N;
     int64_t sg = mstate ? w.s_g : p.N;
     CK(run_backward(p, w, gp, sg, n, shard, n_shards, st));
@@ -697,11 +717,20 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
     CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 3));
     if (p.sumY2 > 0)
       CK(cudaMemcpy2DAsync(out, p.sumY2 * 8, w.Y2, w.s_Y2 * 8, p.sumY2 * 8, B, cudaMemcpyDeviceToDevice, st));
+  } else if (stage == 5 || stage == 6) {
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 1));
+    if (stage == 5) {   // X_hat, complex128 [B][N_pad]
+      if (out_bytes < (size_t)B * p.N_pad * 16) return fail(JTFS_ERR_SIZE, "out too small");
+      CK(cudaMemcpy2DAsync(out, p.N_pad * 16, w.Xh, w.s_xp * 8, p.N_pad * 16, B, cudaMemcpyDeviceToDevice, st));
+    } else {            // Z1, complex64 [B][sum L1]
+      if (out_bytes < (size_t)B * p.sumL1 * 8) return fail(JTFS_ERR_SIZE, "out too small");
+      CK(cudaMemcpy2DAsync(out, p.sumL1 * 8, w.Z1, w.s_L1 * 8, p.sumL1 * 8, B, cudaMemcpyDeviceToDevice, st));
+    }
   } else if (stage == 4) {
     if (out_bytes < (size_t)B * p.n_coef * 4) return fail(JTFS_ERR_SIZE, "out too small");
     CK(run_forward(p, x, p.N, n, (float*)out, p.n_coef, w, 0, 1, st, 0));
   } else {
-    return fail(JTFS_ERR_SIZE, "stage must be 1..4");
+    return fail(JTFS_ERR_SIZE, "stage must be 1..6");
   }
   CK(cudaGetLastError());
   return JTFS_OK;

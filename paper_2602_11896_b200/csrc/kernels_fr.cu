@@ -144,7 +144,7 @@ __global__ void k_o1_bwd_rows(const float* __restrict__ rres, int64_t r_sb, floa
 __global__ void k_o1_bwd_time(const float* __restrict__ rres, int64_t r_sb, float2* __restrict__ W1,
                               int64_t W1_sb, const float* __restrict__ V2, int64_t V2_sb,
                               const int64_t* __restrict__ nrows, const float* __restrict__ tT, int64_t H, int P,
-                              int64_t Ft, int64_t frames, int64_t m0) {
+                              int64_t Ft, int64_t frames, int64_t m0, const float* __restrict__ thr) {
   const int f = blockIdx.y, b = blockIdx.z;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = q / Ft, tau = q % Ft;
@@ -164,7 +164,8 @@ __global__ void k_o1_bwd_time(const float* __restrict__ rres, int64_t r_sb, floa
   }
   float2 v = *w;
   float m2 = v.x * v.x + v.y * v.y;
-  float s = m2 > FLT_MIN ? (float)acc * rsqrtf(m2) : 0.f;
+  const float th = thr[b];
+  float s = (m2 > FLT_MIN && m2 > th * th) ? (float)acc * rsqrtf(m2) : 0.f;
   *w = make_float2(v.x * s, v.y * s);
 }
 
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd(
     float2* __restrict__ gY2, int64_t gy_sb, const JointUnit* __restrict__ units, int nfr,
     const int64_t* __restrict__ tiles, int n_blocks, const BlockInfo* __restrict__ binfo,
     const float2* __restrict__ hfr, int P, const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off,
-    int shard, int n_shards, int maxLf) {
+    int shard, int n_shards, int maxLf, const float* __restrict__ thr) {
   extern __shared__ float4 smem4[];
   const int bi = find_idx(tiles, n_blocks, blockIdx.x);
   const BlockInfo bf = binfo[bi];
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd(
     for (int c = 0; c < 4; ++c) gacc[i][c] = make_float2(0.f, 0.f);
 
   const int tr = tid >> 4, tc = tid & 15;
+  const float th2 = thr[b] * thr[b];
   for (int f = 0; f < nfr; ++f) {
     const int uidx = bi * nfr + f;
     if (uidx % n_shards != shard) continue;
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd(
               gv = fmaf(gs[((q << U.d) - rr[i]) & (Lf - 1)], Go[q * kJC + tc * 4 + c], gv);
           }
           float m2 = acc[i][c].x * acc[i][c].x + acc[i][c].y * acc[i][c].y;
-          float s = (valid[i] && m2 > FLT_MIN) ? gv * rsqrtf(m2) : 0.f;
+          float s = (valid[i] && m2 > FLT_MIN && m2 > th2) ? gv * rsqrtf(m2) : 0.f;
           Gw[(tr * 4 + i) * kJC + tc * 4 + c] = make_float2(acc[i][c].x * s, acc[i][c].y * s);
         }
       }
@@ -492,14 +494,21 @@ __global__ void k_phiT_fwd(const float* __restrict__ o, int64_t o_sb, float* __r
   const int64_t H = phiT_H[bf.s2];
   const float* t = phiT_half + phiT_off[bf.s2];
   const float* src = o + b * o_sb + U.o_off + rho * bf.n_cols;
-  int64_t jlo, jhi;
-  sym_range(H, bf.T2, &jlo, &jhi);
-  const int64_t cm = (m0 + tp) * bf.D;
   double acc = 0;
-  for (int64_t j = jlo + lane; j <= jhi; j += 32) {
-    int64_t i = (cm + j - bf.c_lo) % bf.T2;
-    if (i < 0) i += bf.T2;
-    acc += (double)__ldg(t + (j < 0 ? -j : j)) * (double)src[i];
+  if (bf.n_cols < bf.T2) {
+    // unwrapped: column index of position m*D + j is (m - m0)*D + H + j (no modulo)
+    const int64_t base = (tp)*bf.D + H;
+    for (int64_t j = -H + lane; j <= H; j += 32)
+      acc += (double)__ldg(t + (j < 0 ? -j : j)) * (double)src[base + j];
+  } else {
+    int64_t jlo, jhi;
+    sym_range(H, bf.T2, &jlo, &jhi);
+    const int64_t cm = (m0 + tp) * bf.D;
+    for (int64_t j = jlo + lane; j <= jhi; j += 32) {
+      int64_t i = (cm + j - bf.c_lo) % bf.T2;
+      if (i < 0) i += bf.T2;
+      acc += (double)__ldg(t + (j < 0 ? -j : j)) * (double)src[i];
+    }
   }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
@@ -522,14 +531,27 @@ __global__ void k_phiT_adj(const float* __restrict__ rres, int64_t r_sb, float* 
   const BlockInfo bf = binfo[U.bi];
   const int64_t loc = q - U.o_off;
   const int64_t rho = loc / bf.n_cols, i = loc % bf.n_cols;
-  const int64_t c = (bf.c_lo + i) % bf.T2;
   const int64_t H = phiT_H[bf.s2];
   const float* t = phiT_half + phiT_off[bf.s2];
   const float* rr = rres + b * r_sb + o2_start + ucoef[u] + rho * frames;
   double acc = 0;
-  for (int64_t tp = 0; tp < frames; ++tp) {
-    int64_t dd = cdist((m0 + tp) * bf.D - c, bf.T2);
-    if (dd <= H) acc += (double)__ldg(t + dd) * (double)rr[tp];
+  if (bf.n_cols < bf.T2) {
+    // unwrapped coordinates: column i sits at x = m0*D - H + i; frame m at m*D
+    const int64_t x = m0 * bf.D - H + i;
+    int64_t mlo = x - H <= 0 ? -((H - x) / bf.D) : (x - H + bf.D - 1) / bf.D;
+    int64_t mhi = (x + H) >= 0 ? (x + H) / bf.D : -((-(x + H) + bf.D - 1) / bf.D);
+    mlo = mlo < m0 ? m0 : mlo;
+    mhi = mhi > m0 + frames - 1 ? m0 + frames - 1 : mhi;
+    for (int64_t m = mlo; m <= mhi; ++m) {
+      const int64_t dd = m * bf.D - x;
+      acc += (double)__ldg(t + (dd < 0 ? -dd : dd)) * (double)rr[m - m0];
+    }
+  } else {
+    const int64_t c = (bf.c_lo + i) % bf.T2;
+    for (int64_t tp = 0; tp < frames; ++tp) {
+      int64_t dd = cdist((m0 + tp) * bf.D - c, bf.T2);
+      if (dd <= H) acc += (double)__ldg(t + dd) * (double)rr[tp];
+    }
   }
   go[b * go_sb + q] = (float)acc;
 }
@@ -585,7 +607,7 @@ void launch_o1_fwd(const Plan& p, const DeviceTables& d, const float* S1t, int64
 
 void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float2* W1,
                    int64_t W1_sb, float* V2, int64_t V2_sb, const float* S1t, int64_t S1t_sb, float* gS1t,
-                   int64_t gS1t_sb, int B, cudaStream_t st) {
+                   int64_t gS1t_sb, const float* thr, int B, cudaStream_t st) {
   (void)S1t; (void)S1t_sb;
   const int nfr1 = 1 + (int)p.psi_fr_plus.size();
   const int P = (int)p.P;
@@ -598,7 +620,7 @@ void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t
   }
   dim3 g2((unsigned)((p.P * p.Ft + 255) / 256), (unsigned)nfr1, (unsigned)B);
   k_o1_bwd_time<<<g2, 256, 0, st>>>(r, r_sb, W1, W1_sb, V2, V2_sb, d.o1_nrows, d.phiT_half + p.phiT_off[p.log2T],
-                                    p.phiT_H[p.log2T], P, p.Ft, p.frames, m0);
+                                    p.phiT_H[p.log2T], P, p.Ft, p.frames, m0, thr);
   dim3 g3((unsigned)((p.psi1.size() * p.Ft + 255) / 256), (unsigned)B);
   k_o1_bwd_S1t<<<g3, 256, 0, st>>>(W1, W1_sb, gS1t, gS1t_sb, d.hfr, d.o1_rlo, d.o1_nrows, d.kf_of, nfr1,
                                    (int)p.psi1.size(), P, p.Ft);
@@ -659,7 +681,7 @@ void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64
 }
 
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                      int64_t go_sb, float2* gY2, int64_t gy_sb, int shard, int n_shards, int B,
+                      int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st) {
   if (d.n_blocks == 0) return;
   size_t sm = (size_t)d.Kmax * kJC * 8 + (size_t)p.P * 8 + (size_t)kJR * kJC * 8 + (size_t)d.maxLf * 4 +
@@ -669,7 +691,7 @@ void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, in
   dim3 g((unsigned)d.bwd_ntiles, (unsigned)B);
   k_joint_bwd<<<g, 256, sm, st>>>(Y2, y_sb, go, go_sb, gY2, gy_sb, d.units, (int)p.L_fr.size(), d.bwd_tiles,
                                   d.n_blocks, d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, shard, n_shards,
-                                  d.maxLf);
+                                  d.maxLf, thr);
   count_launch();
 }
 

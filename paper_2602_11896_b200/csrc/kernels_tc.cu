@@ -302,6 +302,7 @@ struct TcBwArgs {
   const float* wts;
   const TcUnit* tcu;
   int nfr, shard, n_shards;
+  const float* thr;
 };
 
 template <int KAP>
@@ -482,6 +483,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const int q = e & 3, h = e >> 2;        // lane quadrant, row half (16 rows)
     const int c = q * 32 + lane;
     const int64_t colg = col0 + c;
+    const float th2 = a.thr[b] * a.thr[b];
     int buf = 0;
     uint32_t bph = 0;
     int g = 0;
@@ -523,7 +525,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           for (int r = 0; r < KAP; ++r) gv = fmaf(__shfl_sync(0xffffffffu, wl[r], i), gor[r], gv);
           const float re = v[2 * i], im = v[2 * i + 1];
           const float m2 = fmaf(re, re, im * im);
-          const float s = m2 > 1.17549435e-38f ? gv * rsqrtf(m2) : 0.f;
+          const float s = (m2 > 1.17549435e-38f && m2 > th2) ? gv * rsqrtf(m2) : 0.f;
           gw[2 * i] = re * s;
           gw[2 * i + 1] = im * s;
         }
@@ -590,13 +592,13 @@ static void launch_tc_bwd(const TcBwArgs& a, int K2max, int64_t ntiles, int B, c
 }
 
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                         int64_t go_sb, float2* gY, int64_t gy_sb, int shard, int n_shards, int B,
-                         cudaStream_t st) {
+                         int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
+                         int B, cudaStream_t st) {
   for (int cls = 0; cls < 3; ++cls) {
     const TcClass& C = d.tcb[cls];
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
-               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards};
+               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr};
     switch (cls) {
       case 0: launch_tc_bwd<2>(a, C.K2max, C.ntiles, B, st); break;
       case 1: launch_tc_bwd<4>(a, C.K2max, C.ntiles, B, st); break;

@@ -22,7 +22,7 @@ __device__ __forceinline__ int find_job(const int64_t* __restrict__ tiles, int n
 }
 
 // R10 half-sample symmetric extension: xp[i] = x[e(i - pad_left)], e = 2N-periodic even extension.
-__global__ void k_reflect_pad(const float* __restrict__ x, int64_t sx, float2* __restrict__ xp, int64_t N,
+__global__ void k_reflect_pad(const float* __restrict__ x, int64_t sx, double2* __restrict__ xp, int64_t N,
                               int64_t N_pad, int64_t pad_left) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N_pad) return;
@@ -30,10 +30,10 @@ __global__ void k_reflect_pad(const float* __restrict__ x, int64_t sx, float2* _
   int64_t t = (i - pad_left) % (2 * N);
   if (t < 0) t += 2 * N;
   int64_t src = t < N ? t : 2 * N - 1 - t;
-  xp[(int64_t)b * N_pad + i] = make_float2(__ldg(x + b * sx + src), 0.f);
+  xp[(int64_t)b * N_pad + i] = make_double2((double)__ldg(x + b * sx + src), 0.0);
 }
 
-void launch_reflect_pad(const float* x, int64_t sx, float2* xp, const Plan& p, int B, cudaStream_t st) {
+void launch_reflect_pad(const float* x, int64_t sx, double2* xp, const Plan& p, int B, cudaStream_t st) {
   dim3 g((unsigned)((p.N_pad + 255) / 256), (unsigned)B);
   k_reflect_pad<<<g, 256, 0, st>>>(x, sx, xp, p.N, p.N_pad, p.pad_left);
   count_launch();
@@ -41,37 +41,57 @@ void launch_reflect_pad(const float* x, int64_t sx, float2* xp, const Plan& p, i
 
 // out[m] = scale * sum_{s in [lo, lo+len), s = m (mod L_out)} h[s-lo] * in[s mod L_in]
 // i.e. cdgmm with a support-limited real response, then subsample_fourier (fold-mean).
-__global__ void __launch_bounds__(kGatherTile) k_gather(const float2* __restrict__ in, int64_t in_sb,
-                                                         float2* __restrict__ out, int64_t out_sb,
+template <class TI> struct GAcc { using T = float2; using R = float; };
+template <> struct GAcc<double2> { using T = double2; using R = double; };
+__device__ __forceinline__ void st_c(float2* p, double re, double im) { *p = make_float2((float)re, (float)im); }
+__device__ __forceinline__ void st_c(double2* p, double re, double im) { *p = make_double2(re, im); }
+
+template <class TI, class TO>
+__global__ void __launch_bounds__(kGatherTile) k_gather(const TI* __restrict__ in, int64_t in_sb,
+                                                         TO* __restrict__ out, int64_t out_sb,
                                                          const GatherJob* __restrict__ jobs,
                                                          const int64_t* __restrict__ tiles, int njobs,
                                                          const float* __restrict__ vals) {
+  using R = typename GAcc<TI>::R;
   const int64_t tile = blockIdx.x;
   const int b = blockIdx.y;
   const int j = find_job(tiles, njobs, tile);
   const GatherJob J = jobs[j];
   const int64_t m = (tile - tiles[j]) * kGatherTile + threadIdx.x;
   if (m >= J.L_out) return;
-  const float2* src = in + b * in_sb + J.in_off;
+  const TI* src = in + b * in_sb + J.in_off;
   int64_t s = m - floor_div(m - J.lo, J.L_out) * J.L_out;  // smallest s >= lo with s = m mod L_out
-  float2 acc = make_float2(0.f, 0.f);
+  R ax = 0, ay = 0;
   for (; s < J.lo + J.len; s += J.L_out) {
-    float h = __ldg(vals + J.val_off + (s - J.lo));
+    const R h = (R)__ldg(vals + J.val_off + (s - J.lo));
     int64_t si = s % J.L_in;
     if (si < 0) si += J.L_in;
-    float2 v = src[si];
-    acc.x = fmaf(h, v.x, acc.x);
-    acc.y = fmaf(h, v.y, acc.y);
+    const TI v = src[si];
+    ax += h * (R)v.x;
+    ay += h * (R)v.y;
   }
-  out[b * out_sb + J.out_off + m] = cscale(acc, J.scale);
+  st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
 }
 
-void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
-                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+template <class TI, class TO>
+static void gather_t(const TI* in, int64_t in_sb, TO* out, int64_t out_sb, const GatherJob* jobs,
+                     const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   dim3 g((unsigned)ntiles, (unsigned)B);
-  k_gather<<<g, kGatherTile, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
+  k_gather<TI, TO><<<g, kGatherTile, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
   count_launch();
+}
+void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
+                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
+}
+void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
+                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
+}
+void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
+                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
 }
 
 // U1 = |Z1|, stored as a complex row with zero imaginary part for the next FFT.
@@ -174,21 +194,43 @@ void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS
 
 // Modulus adjoint (R22): g_Z1 = (Z1/|Z1|) * Re(g_U1), 0 where |Z1| = 0.
 __global__ void k_phase_mul(const float2* __restrict__ z, const float2* __restrict__ gu, int64_t gsb,
-                            float2* __restrict__ out, int64_t n, int64_t sb) {
+                            float2* __restrict__ out, int64_t n, int64_t sb, const float* __restrict__ thr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t o = blockIdx.y * sb + i;
   float2 v = z[o];
   float m2 = v.x * v.x + v.y * v.y;
   float g = gu[blockIdx.y * gsb + i].x;
-  float s = m2 > 1.17549435e-38f ? g * rsqrtf(m2) : 0.f;
+  const float t = thr[blockIdx.y];
+  float s = (m2 > 1.17549435e-38f && m2 > t * t) ? g * rsqrtf(m2) : 0.f;
   out[o] = make_float2(v.x * s, v.y * s);
 }
 
 void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
-                      int B, cudaStream_t st) {
+                      const float* thr, int B, cudaStream_t st) {
   dim3 g((unsigned)((n_per_b + 255) / 256), (unsigned)B);
-  k_phase_mul<<<g, 256, 0, st>>>(z, gu, gsb, out, n_per_b, sb);
+  k_phase_mul<<<g, 256, 0, st>>>(z, gu, gsb, out, n_per_b, sb, thr);
+  count_launch();
+}
+
+// R22 dead zone of the modulus adjoint: thr[b] = tau * max_t |y_b(t)| (tau = 1e-6)
+__global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ y, int64_t N, float tau,
+                                                float* __restrict__ thr) {
+  __shared__ float red[256];
+  const float* src = y + (int64_t)blockIdx.x * N;
+  float m = 0.f;
+  for (int64_t i = threadIdx.x; i < N; i += 256) m = fmaxf(m, fabsf(src[i]));
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) thr[blockIdx.x] = tau * red[0];
+}
+
+void launch_absmax(const float* y, int64_t N, float tau, float* thr, int B, cudaStream_t st) {
+  k_absmax<<<B, 256, 0, st>>>(y, N, tau, thr);
   count_launch();
 }
 

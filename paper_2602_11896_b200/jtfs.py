@@ -174,6 +174,10 @@ class Plan:
             out = torch.empty(B, info.N1, info.N_pad // (info.N // info.frames), device=x.device)
         elif stage == 3:
             out = torch.empty(B, self._sumY2(), dtype=torch.complex64, device=x.device)
+        elif stage == 5:
+            out = torch.empty(B, info.N_pad, dtype=torch.complex128, device=x.device)
+        elif stage == 6:
+            out = torch.empty(B, self._sumL1(), dtype=torch.complex64, device=x.device)
         else:
             out = torch.empty(B, info.n_coef, device=x.device)
         check(self.lib.jtfs_debug_stage(self.h, stage, _ptr(x), B, _ptr(out), out.numel() * out.element_size(),

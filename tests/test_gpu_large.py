@@ -1,0 +1,63 @@
+"""GPU parity at the BASELINE.json sizes (configs c2..c5), one signal each, in the launch
+configuration bench.py uses. The float64 oracle evaluates a subset of second-order blocks
+(`Oracle.forward(blocks=...)`): the first block (tensor-core path) and/or the last block (CUDA-core
+path), plus S0 and order 1; those coefficients are compared element by element.
+
+Gradient: the loss is restricted to the same subset of paths by giving the GPU a target equal
+to its own (bitwise deterministic) S(y) outside the subset, so its residual is exactly zero
+there; the oracle differentiates the subset loss. Bars: rel-L2 1e-4 (S), 1e-3 (dE/dy)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.jtfs import Oracle
+from synth import CONFIGS, plan_args, batch
+
+pytestmark = pytest.mark.gpu
+
+CASES = {"c2": [0, 9], "c3": [10], "c4": [11], "c5": [11]}
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def subset_mask(plan, blocks):
+    m = np.zeros(plan.n_coef, bool)
+    for q in plan.paths:
+        if q.order == 1 or (q.order == 2 and q.block in blocks) or q.order == 0:
+            m[q.offset:q.offset + q.rows * q.frames] = True
+    return m
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_large_forward_and_gradient(name):
+    from paper_2602_11896_b200 import Plan
+    cfg = CONFIGS[name]
+    args = plan_args(cfg)
+    blocks = CASES[name]
+    p = Plan(*args)
+    o = Oracle(args)
+    x = batch(name, 1)
+    y = batch(name, 1, which="y")
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    # forward: GPU runs everything, the oracle the sampled blocks
+    Sg = p.forward(xd).cpu().numpy()[0]
+    So = o.forward(x, blocks=blocks).numpy()[0]
+    m = subset_mask(o.plan, blocks)
+    assert rel(Sg[m], So[m]) <= 1e-4
+    for q in o.plan.paths:
+        if m[q.offset]:
+            sl = slice(q.offset, q.offset + q.rows * q.frames)
+            assert rel(Sg[sl], So[sl]) <= 2e-3, (name, q)
+    # gradient of the loss restricted to the sampled paths (order 1 + blocks); S0 is never in the loss
+    Sy = p.forward(yd)
+    St = Sy.clone()
+    mt = torch.from_numpy(m).cuda()
+    St[0, mt] = torch.from_numpy(So.astype(np.float32)).cuda()[mt]
+    loss, g = p.loss_grad(yd, St)
+    Eo, go = o.loss_grad_subset(y, So[None], blocks)
+    assert rel(loss.cpu().numpy(), Eo.numpy()) <= 1e-4
+    assert rel(g.cpu().numpy(), go.numpy()) <= 1e-3
