@@ -150,6 +150,10 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
 jtfs_status jtfs_debug_tc_gemm(const float* A, const float* Bimg, float* D, int N, int K, int three,
                                jtfs_stream_t stream);
 
+/* Test-only: same GEMM with A staged in TMEM by tcgen05.st and the TS form of tcgen05.mma. */
+jtfs_status jtfs_debug_tc_gemm_ts(const float* A, const float* Bimg, float* D, int N, int K, int three,
+                                  jtfs_stream_t stream);
+
 /* Number of kernels the library has launched in this process (for launch-count reporting). */
 int64_t jtfs_launch_count(void);
 

@@ -64,6 +64,7 @@ _SIGS = {
     "jtfs_debug_stage": (_I, [_P, _I, _P, _I64, _P, _SZ, _P, _SZ, _P]),
     "jtfs_launch_count": (_I64, []),
     "jtfs_debug_tc_gemm": (_I, [_P, _P, _P, _I, _I, _I, _P]),
+    "jtfs_debug_tc_gemm_ts": (_I, [_P, _P, _P, _I, _I, _I, _P]),
     "jtfs_plan_cost": (_I, [_P, _P, _I64]),
     "jtfs_prof_enable": (None, [_I]),
     "jtfs_prof_read": (_I, [_I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),

@@ -14,7 +14,7 @@ struct TcClass {
   int64_t* tiles = nullptr;
   int n_blocks = 0;
   int64_t ntiles = 0;
-  int K2max = 0;
+  int K2max = 0, Kmax = 0, kcw = 32;
 };
 
 struct DeviceTables {
@@ -56,7 +56,7 @@ struct DeviceTables {
   TcUnit* tc_units = nullptr;
   TcClass tc[kTcClasses];
   float* tc_img2 = nullptr;
-  TcClass tcb[3];
+  TcClass tcb[kTcBwClasses];
 };
 
 constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels

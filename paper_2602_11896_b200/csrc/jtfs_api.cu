@@ -101,7 +101,7 @@ static void free_tables(DeviceTables* d) {
   }
   if (d->tc_img) cudaFree(d->tc_img);
   if (d->tc_img2) cudaFree(d->tc_img2);
-  for (int c = 0; c < 3; ++c) {
+  for (int c = 0; c < kTcBwClasses; ++c) {
     if (d->tcb[c].blocks) cudaFree(d->tcb[c].blocks);
     if (d->tcb[c].tiles) cudaFree(d->tcb[c].tiles);
   }
@@ -167,50 +167,40 @@ static cudaError_t upload(Plan& p) {
       d->fwd_ntiles[c] = t.back();
     }
   }
-  // tensor-core classes
-  UP(p.tc_img, tc_img); UP(p.tc_wts, tc_wts); UP(p.tc_units, tc_units);
-  for (int c = 0; c < kTcClasses; ++c) {
-    std::vector<TcBlock> bl;
-    std::vector<int64_t> cnt;
-    int k2 = 0;
-    if (g_use_tc)
-      for (auto& tb : p.tc_blocks)
-        if (tb.cls == c) {
-          bl.push_back(tb);
-          const int CT = c < 3 ? 2 : 1;
-          cnt.push_back((p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT));
-          k2 = std::max(k2, tb.K2);
-        }
-    d->tc[c].n_blocks = (int)bl.size();
-    d->tc[c].K2max = k2;
-    if (!bl.empty()) {
-      t = prefix(cnt);
-      UP(bl, tc[c].blocks);
-      UP(t, tc[c].tiles);
-      d->tc[c].ntiles = t.back();
+  // tensor-core classes (forward and backward)
+  UP(p.tc_img, tc_img); UP(p.tc_wts, tc_wts); UP(p.tc_units, tc_units); UP(p.tc_img2, tc_img2);
+  auto build_classes = [&](const std::vector<TcBlock>& src, TcClass* cls, int ncls, bool fwd) -> cudaError_t {
+    for (int c = 0; c < ncls; ++c) {
+      std::vector<TcBlock> bl;
+      std::vector<int64_t> cnt;
+      int k2 = 0, kmax = 0, kcw = 32;
+      if (g_use_tc)
+        for (auto& tb : src)
+          if (tb.cls == c) {
+            bl.push_back(tb);
+            const int CT = (fwd && c < 3) ? 2 : 1;
+            cnt.push_back((p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT));
+            k2 = std::max(k2, tb.K2);
+            kmax = std::max(kmax, tb.K);
+            kcw = tb.kcw;
+          }
+      cls[c].n_blocks = (int)bl.size();
+      cls[c].K2max = k2;
+      cls[c].Kmax = kmax;
+      cls[c].kcw = kcw;
+      if (!bl.empty()) {
+        std::vector<int64_t> tt = prefix(cnt);
+        cudaError_t e1 = up(bl, &cls[c].blocks);
+        if (e1 != cudaSuccess) return e1;
+        e1 = up(tt, &cls[c].tiles);
+        if (e1 != cudaSuccess) return e1;
+        cls[c].ntiles = tt.back();
+      }
     }
-  }
-  UP(p.tc_img2, tc_img2);
-  for (int c = 0; c < 3; ++c) {
-    std::vector<TcBlock> bl;
-    std::vector<int64_t> cnt;
-    int k2 = 0;
-    if (g_use_tc)
-      for (auto& tb : p.tcb_blocks)
-        if (tb.cls == c) {
-          bl.push_back(tb);
-          cnt.push_back((p.binfo[tb.bi].n_cols + 127) / 128);
-          k2 = std::max(k2, tb.K2);
-        }
-    d->tcb[c].n_blocks = (int)bl.size();
-    d->tcb[c].K2max = k2;
-    if (!bl.empty()) {
-      t = prefix(cnt);
-      UP(bl, tcb[c].blocks);
-      UP(t, tcb[c].tiles);
-      d->tcb[c].ntiles = t.back();
-    }
-  }
+    return cudaSuccess;
+  };
+  if ((e = build_classes(p.tc_blocks, d->tc, kTcClasses, true)) != cudaSuccess) { free_tables(d); return e; }
+  if ((e = build_classes(p.tcb_blocks, d->tcb, kTcBwClasses, false)) != cudaSuccess) { free_tables(d); return e; }
   std::vector<int32_t> kf;
   for (auto& f : p.L_fr) kf.push_back(std::min(f.j, p.log2F));
   UP(kf, kf_of);

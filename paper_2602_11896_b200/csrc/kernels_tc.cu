@@ -1,4 +1,5 @@
-// kernels_tc.cu — the joint lambda_1 stage forward on the 5th-generation tensor cores (tcgen05).
+// kernels_tc.cu — the joint lambda_1 stage (SURVEY §8(a) A5 forward, A7 backward) on the
+// 5th-generation tensor cores (tcgen05, kind::tf32, accumulators in TMEM).
 //
 // For one block n2 and a tile of 128 time columns, every frequential filter f is the exact dense
 // matrix M_f[r][n] = h_f[(r 2^k_f - n) mod P] (zero-pad to P, circular convolution along n1,
@@ -7,25 +8,36 @@
 // with A[c][2n+pi] = (Re,Im) Y2[n][c] and B = [[Re M, -Im M], [Im M, Re M]] interleaved, so that
 // TMEM lane c (a time column) holds Re/Im W of 64 consecutive lambda_1 rows side by side. 3xTF32:
 // D = A_hi B_hi + A_hi B_lo + A_lo B_hi, fp32 accumulation in TMEM (north_star: "a genuine dense
-// contraction with a 3xTF32 split").
-//   warp 0      producer: cp.async.bulk of pre-split B images (planner, canonical K-major layout)
-//   warp 1      MMA issuer (one thread): tcgen05.mma kind::tf32, M=128, N=128, K=8
-//   warps 4..11 epilogue: tcgen05.ld -> |W| (Eq.2) -> phi_F over rows (Eq.4, R17) in registers
-// A (the Y2 tile, hi/lo) stays resident in SMEM for all filters of the block; TMEM is double
-// buffered so the epilogue of row tile t overlaps the MMAs of row tile t+1.
+// contraction with a 3xTF32 split"). B is the same for every column tile and signal: the planner
+// pre-splits it into tf32 hi/lo images in the canonical K-major layout, streamed by the bulk-copy
+// engine (cp.async.bulk) through an mbarrier ring; A (the Y2 tile) stays resident in SMEM.
+//
+// Forward (k_joint_fwd_tc):  warp 0 producer, warp 1 MMA issuer (elected lane), warps 4..11
+//   epilogue: tcgen05.ld -> |W| (Eq.2) -> phi_F over rows (Eq.4, R17) in registers -> o.
+//   TMEM double buffered: the epilogue of row tile t overlaps the MMAs of row tile t+1.
+// Backward (k_joint_bwd_tc), per 32-row tile g of every filter:
+//   GEMM1  D1 = W recomputed (forward B images, N = 64)
+//   epi    g_W = (W/|W|) Phi_F^T g_o (R22 dead zone) -> tf32 hi/lo -> TMEM (tcgen05.st) = A2
+//   GEMM2  D2[c][2n+po] += sum_kk A2[c][kk] B2[2n+po][kk] (A from TMEM), B2 = conj(M_f) images,
+//          i.e. g_Y2^T += g_W^T conj(M_f), accumulated in TMEM over all filters and row tiles.
+//   The MMA warp issues GEMM1(g+1) before GEMM2(g), so the tensor core works while the epilogue
+//   turns D1(g) into A2(g).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "device.cuh"
 #include "tc.cuh"
 
-#include <algorithm>
-
 namespace jtfs {
 
-constexpr int kTcRows = 64;         // lambda_1 rows per row tile (N = 128)
-constexpr int kTcN = 2 * kTcRows;   // MMA N
-constexpr int kTcKc = 32;           // B chunk (k' elements) per pipeline stage
+constexpr int kTcRows = 64;         // lambda_1 rows per forward row tile (N = 128)
+constexpr int kTcN = 2 * kTcRows;   // forward MMA N
 constexpr int kTcThreads = 384;     // 12 warps
+constexpr int kTcMaxStages = 8;
+constexpr int kBwRows = 32;         // rows per backward tile (GEMM1 N = 64, GEMM2 K = 64)
+constexpr int kBwN1 = 2 * kBwRows;
+constexpr int kB2c = 16;            // B2 chunk width (kk) per stage
 
 __device__ __forceinline__ int find_tc(const int64_t* __restrict__ tiles, int n, int64_t t) {
   int lo = 0, hi = n - 1;
@@ -36,21 +48,40 @@ __device__ __forceinline__ int find_tc(const int64_t* __restrict__ tiles, int n,
   return lo;
 }
 
+// A tile: Y2[n][col0 + c] -> tf32 hi/lo, canonical K-major [128][K2], k' = 2n + (re, im)
+__device__ __forceinline__ void build_a(float* a_hi, float* a_lo, const float2* __restrict__ ysrc,
+                                        const BlockInfo& bf, int64_t col0, int K, int K2, int tid, int nthr) {
+  for (int idx = tid; idx < 128 * (K2 / 2); idx += nthr) {
+    const int c = idx & 127;
+    const int n = idx >> 7;
+    const int64_t col = col0 + c;
+    float2 v = make_float2(0.f, 0.f);
+    if (n < K && col < bf.n_cols) v = ysrc[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2];
+    float h0, l0, h1, l1;
+    tc::split_tf32(v.x, h0, l0);
+    tc::split_tf32(v.y, h1, l1);
+    const uint32_t o = tc::core_off((uint32_t)c, (uint32_t)(2 * n), (uint32_t)K2) / 4;
+    *reinterpret_cast<float2*>(a_hi + o) = make_float2(h0, h1);
+    *reinterpret_cast<float2*>(a_lo + o) = make_float2(l0, l1);
+  }
+}
+
 struct TcArgs {
   const float2* Y2; int64_t y_sb;
   float* o; int64_t o_sb;
   const JointUnit* units; const BlockInfo* binfo;
   const TcBlock* blocks; const int64_t* tiles; int n_tc_blocks;
-  const float* img;                 // B images
+  const float* img;                 // forward B images
   const float* wts;                 // phi_F weights [unit][rho][NT*64]
   const TcUnit* tcu;                // per unit image / weight offsets
   int nfr, shard, n_shards;
 };
 
-constexpr int kTcMaxStages = 8;
-
+// =====================================================================================
+// forward
+// =====================================================================================
 template <int CT, int KAP>
-__global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS, int STG) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
@@ -60,11 +91,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   const BlockInfo bf = a.binfo[TB.bi];
   const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)(128 * CT);
   const int b = blockIdx.y;
-  const int K = TB.K, K2 = TB.K2;
+  const int K = TB.K, K2 = TB.K2, kcw = TB.kcw;
   float* a_hi = reinterpret_cast<float*>(sm);              // [CT][128][K2] canonical
   float* a_lo = a_hi + CT * 128 * K2;
-  float* bst = a_lo + CT * 128 * K2;                        // NS stages x (2 x 128 x kTcKc)
-  float* red = bst + NS * 2 * kTcN * kTcKc;                 // [CT][KAP][128]
+  float* bst = a_lo + CT * 128 * K2;                        // NS stages x STG floats
+  float* red = bst + NS * STG;                              // [CT][KAP][128]
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
@@ -72,31 +103,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, CT == 1 ? 256 : 512);
-  // ---- A: Y2 tile -> tf32 hi/lo, canonical K-major, k' = 2n + (re, im); zero padded
   const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off;
-  for (int idx = tid; idx < CT * 128 * (K2 / 2); idx += kTcThreads) {
-    const int c = idx & 127;
-    const int rest = idx >> 7;
-    const int n = rest % (K2 / 2), m = rest / (K2 / 2);
-    const int64_t col = col0 + m * 128 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (n < K && col < bf.n_cols) v = ysrc[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2];
-    float h0, l0, h1, l1;
-    tc::split_tf32(v.x, h0, l0);
-    tc::split_tf32(v.y, h1, l1);
-    const uint32_t o = (uint32_t)(m * 128 * K2) + tc::core_off((uint32_t)c, (uint32_t)(2 * n), (uint32_t)K2) / 4;
-    *reinterpret_cast<float2*>(a_hi + o) = make_float2(h0, h1);
-    *reinterpret_cast<float2*>(a_lo + o) = make_float2(l0, l1);
-  }
+  for (int m = 0; m < CT; ++m)
+    build_a(a_hi + m * 128 * K2, a_lo + m * 128 * K2, ysrc, bf, col0 + m * 128, K, K2, tid, kTcThreads);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = tmem_base;
-  const int nchunks = (K2 + kTcKc - 1) / kTcKc;
+  const int nchunks = (K2 + kcw - 1) / kcw;
 
   if (warp == 0) {
-    // ===================== producer: B chunks via the bulk-copy engine (whole warp, one lane issues)
+    // ===================== producer: B chunks via the bulk-copy engine (one elected lane issues)
     int stage = 0;
     uint32_t ph = 0;
     for (int f = 0; f < a.nfr; ++f) {
@@ -106,12 +124,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
       const float* src = a.img + tu.img_off;
       for (int t = 0; t < tu.NT; ++t) {
         for (int ch = 0; ch < nchunks; ++ch) {
-          const int kc = min(kTcKc, K2 - ch * kTcKc);
+          const int kc = min(kcw, K2 - ch * kcw);
           const uint32_t bytes = (uint32_t)(2 * kTcN * kc * 4);
           tc::mbar_wait(&empty[stage], ph ^ 1);
           if (tc::elect_one()) {
             tc::mbar_expect_tx(&full[stage], bytes);
-            tc::bulk_g2s(bst + stage * 2 * kTcN * kTcKc, src, bytes, &full[stage]);
+            tc::bulk_g2s(bst + stage * STG, src, bytes, &full[stage]);
           }
           __syncwarp();
           src += 2 * kTcN * kc;
@@ -139,15 +157,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         tc::tc_fence_after();
         const uint32_t dbase = tbase + (uint32_t)(buf * CT * kTcN);
         for (int ch = 0; ch < nchunks; ++ch) {
-          const int kc = min(kTcKc, K2 - ch * kTcKc);
+          const int kc = min(kcw, K2 - ch * kcw);
           tc::mbar_wait(&full[stage], ph);
           tc::tc_fence_after();
-          const uint32_t bh = bst_s + (uint32_t)(stage * 2 * kTcN * kTcKc * 4);
+          const uint32_t bh = bst_s + (uint32_t)(stage * STG * 4);
           const uint64_t dB_hi = tc::sdesc(bh, 128, (uint32_t)kc * 32u);
           const uint64_t dB_lo = tc::sdesc(bh + (uint32_t)(kTcN * kc * 4), 128, (uint32_t)kc * 32u);
           if (tc::elect_one()) {
             for (int ks = 0; ks < kc / 8; ++ks) {
-              const uint32_t kg = (uint32_t)(ch * (kTcKc / 8) + ks);
+              const uint32_t kg = (uint32_t)(ch * (kcw / 8) + ks);
 #pragma unroll
               for (int m = 0; m < CT; ++m) {
                 const uint32_t d = dbase + (uint32_t)(m * kTcN);
@@ -243,19 +261,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   if (warp == 1) tc::tmem_dealloc(tbase, CT == 1 ? 256 : 512);
 }
 
-static size_t tc_smem(int CT, int KAP, int NS, int K2) {
-  return (size_t)(2 * CT * 128 * K2 + NS * 2 * kTcN * kTcKc + CT * KAP * 128) * 4 + 1024;
+static size_t tc_fwd_smem(int CT, int KAP, int NS, int K2, int STG) {
+  return (size_t)(2 * CT * 128 * K2 + NS * STG + CT * KAP * 128) * 4 + 1024;
 }
 
 template <int CT, int KAP>
-static void launch_tc(const TcArgs& a, int K2max, int64_t ntiles, int B, cudaStream_t st) {
-  // as many 32 KB B stages as fit next to the resident A tile (<= 8)
+static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st) {
+  const int STG = 2 * kTcN * C.kcw;
   int NS = kTcMaxStages;
-  while (NS > 2 && tc_smem(CT, KAP, NS, K2max) > 225 * 1024) --NS;
-  size_t sm = tc_smem(CT, KAP, NS, K2max);
+  while (NS > 2 && tc_fwd_smem(CT, KAP, NS, C.K2max, STG) > 224 * 1024) --NS;
+  const size_t sm = tc_fwd_smem(CT, KAP, NS, C.K2max, STG);
   cudaFuncSetAttribute(k_joint_fwd_tc<CT, KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 g((unsigned)ntiles, (unsigned)B);
-  k_joint_fwd_tc<CT, KAP><<<g, kTcThreads, sm, st>>>(a, NS);
+  dim3 g((unsigned)C.ntiles, (unsigned)B);
+  k_joint_fwd_tc<CT, KAP><<<g, kTcThreads, sm, st>>>(a, NS, STG);
   count_launch();
 }
 
@@ -266,39 +284,29 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
     if (C.n_blocks == 0) continue;
     TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
              (int)p.L_fr.size(), shard, n_shards};
-    // class = (CT, KAP): 0:(2,2) 1:(2,4) 2:(2,8) 3:(1,2) 4:(1,4) 5:(1,8)
+    // class = 3 * ct_kind + kap_kind; ct_kind 0: CT=2 (K2<=64), 1: CT=1 kcw 32, 2: CT=1 kcw 16
     switch (cls) {
-      case 0: launch_tc<2, 2>(a, C.K2max, C.ntiles, B, st); break;
-      case 1: launch_tc<2, 4>(a, C.K2max, C.ntiles, B, st); break;
-      case 2: launch_tc<2, 8>(a, C.K2max, C.ntiles, B, st); break;
-      case 3: launch_tc<1, 2>(a, C.K2max, C.ntiles, B, st); break;
-      case 4: launch_tc<1, 4>(a, C.K2max, C.ntiles, B, st); break;
-      case 5: launch_tc<1, 8>(a, C.K2max, C.ntiles, B, st); break;
+      case 0: launch_tc<2, 2>(a, C, B, st); break;
+      case 1: launch_tc<2, 4>(a, C, B, st); break;
+      case 2: launch_tc<2, 8>(a, C, B, st); break;
+      case 3: case 6: launch_tc<1, 2>(a, C, B, st); break;
+      case 4: case 7: launch_tc<1, 4>(a, C, B, st); break;
+      case 5: case 8: launch_tc<1, 8>(a, C, B, st); break;
     }
   }
 }
 
-
 // =====================================================================================
-// Joint stage BACKWARD on tcgen05 (R20-R22): per 32-row tile of each filter f
-//   GEMM1  D1[c][2r+po]  = W recomputed (same B images as the forward, N = 64)
-//   epi    g_v = Phi_F^T g_o, g_W = (W/|W|) g_v  -> A2[c][2r+pi] (tf32 hi/lo, SMEM)
-//   GEMM2  D2[c][2n+po] += sum_kk A2[c][kk] B2[2n+po][kk],  B2 = [[Re M, Im M], [-Im M, Re M]]^T
-//          i.e. g_Y2^T += g_W^T conj(M_f), accumulated in TMEM over all filters and row tiles.
-// The MMA warp issues GEMM1 of tile g+1 before GEMM2 of tile g so the tensor core works while the
-// epilogue turns D1(g) into A2(g). 3xTF32 for both products.
+// backward
 // =====================================================================================
-constexpr int kBwRows = 32;          // rows per backward tile (GEMM1 N = 64, GEMM2 K = 64)
-constexpr int kBwN1 = 2 * kBwRows;
-
 struct TcBwArgs {
   const float2* Y2; int64_t y_sb;
   const float* go; int64_t go_sb;
   float2* gY; int64_t gy_sb;
   const JointUnit* units; const BlockInfo* binfo;
   const TcBlock* blocks; const int64_t* tiles; int n_tc_blocks;
-  const float* img;                 // forward B images (64-row tiles, 32-wide chunks)
-  const float* img2;                // backward B2 images [unit][tile32][hi|lo][N2 x 64]
+  const float* img;                 // forward B images (64-row tiles, kcw-wide chunks)
+  const float* img2;                // backward B2 images [unit][tile32][chunk][hi|lo][N2 x 16]
   const float* wts;
   const TcUnit* tcu;
   int nfr, shard, n_shards;
@@ -316,13 +324,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   const BlockInfo bf = a.binfo[TB.bi];
   const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)128;
   const int b = blockIdx.y;
-  const int K = TB.K, K2 = TB.K2;
+  const int K = TB.K, K2 = TB.K2, kcw = TB.kcw;
   const int N2 = ((2 * K + 15) / 16) * 16;
   float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2]
   float* a_lo = a_hi + 128 * K2;
-  float* a2_hi = a_lo + 128 * K2;                       // [128][64]
-  float* a2_lo = a2_hi + 128 * 64;
-  float* bst = a2_lo + 128 * 64;                        // NS x STG floats
+  float* bst = a_lo + 128 * K2;                         // NS x STG floats
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
@@ -332,63 +338,54 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     tc::mbar_init(&d2full, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, 256);
-  const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off;
-  for (int idx = tid; idx < 128 * (K2 / 2); idx += kTcThreads) {
-    const int c = idx & 127;
-    const int n = idx >> 7;
-    const int64_t col = col0 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (n < K && col < bf.n_cols) v = ysrc[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2];
-    float h0, l0, h1, l1;
-    tc::split_tf32(v.x, h0, l0);
-    tc::split_tf32(v.y, h1, l1);
-    const uint32_t o = tc::core_off((uint32_t)c, (uint32_t)(2 * n), (uint32_t)K2) / 4;
-    *reinterpret_cast<float2*>(a_hi + o) = make_float2(h0, h1);
-    *reinterpret_cast<float2*>(a_lo + o) = make_float2(l0, l1);
-  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, 512);
+  build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kTcThreads);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // TMEM columns: D1 buffers [0,64) [64,128); A2 hi [128,192), lo [192,256); D2 [256, 256+N2)
   const uint32_t tbase = tmem_base;
-  const uint32_t d2 = tbase + 128;               // D2 accumulator columns [128, 128 + N2)
-  const int nchunks = (K2 + kTcKc - 1) / kTcKc;
+  const uint32_t ta2_hi = tbase + 128, ta2_lo = tbase + 192;
+  const uint32_t d2 = tbase + 256;
+  const int nchunks = (K2 + kcw - 1) / kcw;
 
   if (warp == 0) {
     // ===================== producer: B1(g+1) before B2(g), matching the MMA issue order
     int stage = 0;
     uint32_t ph = 0;
     auto push_b1 = [&](const TcUnit& tu, int t32) {
-      // half (rows 32*(t32&1) ..) of the forward 64-row image, all chunks, hi then lo per chunk
-      tc::mbar_wait(&empty[stage], ph ^ 1);
-      if (tc::elect_one()) {
-        uint32_t total = (uint32_t)(2 * kBwN1 * K2 * 4);
-        tc::mbar_expect_tx(&full[stage], total);
-        const float* src = a.img + tu.img_off + (int64_t)(t32 >> 1) * (2 * kTcN * K2);
-        float* dst = bst + stage * STG;
-        const int half = t32 & 1;
-        for (int ch = 0; ch < nchunks; ++ch) {
-          const int kc = min(kTcKc, K2 - ch * kTcKc);
-          const uint32_t hb = (uint32_t)(kBwN1 * kc * 4);
-          tc::bulk_g2s(dst, src + half * kBwN1 * kc, hb, &full[stage]);                     // hi half
-          tc::bulk_g2s(dst + kBwN1 * kc, src + kTcN * kc + half * kBwN1 * kc, hb, &full[stage]);  // lo half
-          dst += 2 * kBwN1 * kc;
-          src += 2 * kTcN * kc;
+      // half (rows 32*(t32&1) ..) of the forward 64-row image, every chunk: [hi half | lo half]
+      const float* src = a.img + tu.img_off + (int64_t)(t32 >> 1) * (2 * kTcN * K2);
+      const int half = t32 & 1;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int kc = min(kcw, K2 - ch * kcw);
+        const uint32_t hb = (uint32_t)(kBwN1 * kc * 4);
+        tc::mbar_wait(&empty[stage], ph ^ 1);
+        if (tc::elect_one()) {
+          tc::mbar_expect_tx(&full[stage], 2 * hb);
+          float* dst = bst + stage * STG;
+          tc::bulk_g2s(dst, src + half * kBwN1 * kc, hb, &full[stage]);
+          tc::bulk_g2s(dst + kBwN1 * kc, src + kTcN * kc + half * kBwN1 * kc, hb, &full[stage]);
         }
+        __syncwarp();
+        src += 2 * kTcN * kc;
+        if (++stage == NS) { stage = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (++stage == NS) { stage = 0; ph ^= 1; }
     };
     auto push_b2 = [&](const TcUnit& tu, int t32) {
-      tc::mbar_wait(&empty[stage], ph ^ 1);
-      if (tc::elect_one()) {
-        const uint32_t bytes = (uint32_t)(2 * N2 * 64 * 4);
-        tc::mbar_expect_tx(&full[stage], bytes);
-        tc::bulk_g2s(bst + stage * STG, a.img2 + tu.img2_off + (int64_t)t32 * (2 * N2 * 64), bytes, &full[stage]);
+      const float* src = a.img2 + tu.img2_off + (int64_t)t32 * (2 * N2 * 64);
+      for (int ch = 0; ch < 64 / kB2c; ++ch) {
+        const uint32_t bytes = (uint32_t)(2 * N2 * kB2c * 4);
+        tc::mbar_wait(&empty[stage], ph ^ 1);
+        if (tc::elect_one()) {
+          tc::mbar_expect_tx(&full[stage], bytes);
+          tc::bulk_g2s(bst + stage * STG, src, bytes, &full[stage]);
+        }
+        __syncwarp();
+        src += 2 * N2 * kB2c;
+        if (++stage == NS) { stage = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (++stage == NS) { stage = 0; ph ^= 1; }
     };
     bool have_prev = false;
     TcUnit pu{};
@@ -412,56 +409,57 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const uint32_t sboA = (uint32_t)K2 * 32u;
     const uint64_t dA_hi = tc::sdesc(tc::smem_u32(a_hi), 128, sboA);
     const uint64_t dA_lo = tc::sdesc(tc::smem_u32(a_lo), 128, sboA);
-    const uint64_t dA2_hi = tc::sdesc(tc::smem_u32(a2_hi), 128, 64u * 32u);
-    const uint64_t dA2_lo = tc::sdesc(tc::smem_u32(a2_lo), 128, 64u * 32u);
     const uint32_t bst_s = tc::smem_u32(bst);
     int stage = 0, buf = 0;
     uint32_t ph = 0, bph = 0;
     int g2 = 0;   // GEMM2 count
     auto gemm1 = [&]() {
       tc::mbar_wait(&tempty[buf], bph ^ 1);
-      tc::mbar_wait(&full[stage], ph);
-      tc::tc_fence_after();
-      if (tc::elect_one()) {
-        uint32_t off = bst_s + (uint32_t)(stage * STG * 4);
-        const uint32_t d = tbase + (uint32_t)(buf * kBwN1);
-        for (int ch = 0; ch < nchunks; ++ch) {
-          const int kc = min(kTcKc, K2 - ch * kTcKc);
-          const uint64_t dbh = tc::sdesc(off, 128, (uint32_t)kc * 32u);
-          const uint64_t dbl = tc::sdesc(off + (uint32_t)(kBwN1 * kc * 4), 128, (uint32_t)kc * 32u);
+      const uint32_t d = tbase + (uint32_t)(buf * kBwN1);
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int kc = min(kcw, K2 - ch * kcw);
+        tc::mbar_wait(&full[stage], ph);
+        tc::tc_fence_after();
+        const uint32_t off = bst_s + (uint32_t)(stage * STG * 4);
+        const uint64_t dbh = tc::sdesc(off, 128, (uint32_t)kc * 32u);
+        const uint64_t dbl = tc::sdesc(off + (uint32_t)(kBwN1 * kc * 4), 128, (uint32_t)kc * 32u);
+        if (tc::elect_one()) {
           for (int ks = 0; ks < kc / 8; ++ks) {
-            const uint32_t kg = (uint32_t)(ch * (kTcKc / 8) + ks);
+            const uint32_t kg = (uint32_t)(ch * (kcw / 8) + ks);
             tc::mma_tf32(d, dA_hi + 16u * kg, dbh + 16u * ks, idesc1, (ch > 0 || ks > 0) ? 1u : 0u);
             tc::mma_tf32(d, dA_hi + 16u * kg, dbl + 16u * ks, idesc1, 1u);
             tc::mma_tf32(d, dA_lo + 16u * kg, dbh + 16u * ks, idesc1, 1u);
           }
-          off += (uint32_t)(2 * kBwN1 * kc * 4);
+          tc::mma_commit(&empty[stage]);
+          if (ch == nchunks - 1) tc::mma_commit(&tfull[buf]);
         }
-        tc::mma_commit(&empty[stage]);
-        tc::mma_commit(&tfull[buf]);
+        __syncwarp();
+        if (++stage == NS) { stage = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (++stage == NS) { stage = 0; ph ^= 1; }
       if (++buf == 2) { buf = 0; bph ^= 1; }
     };
     auto gemm2 = [&]() {
       tc::mbar_wait(&a2full, (uint32_t)(g2 & 1));
-      tc::mbar_wait(&full[stage], ph);
       tc::tc_fence_after();
-      if (tc::elect_one()) {
+      for (int ch = 0; ch < 64 / kB2c; ++ch) {
+        tc::mbar_wait(&full[stage], ph);
+        tc::tc_fence_after();
         const uint32_t bh = bst_s + (uint32_t)(stage * STG * 4);
-        const uint64_t dbh = tc::sdesc(bh, 128, 64u * 32u);
-        const uint64_t dbl = tc::sdesc(bh + (uint32_t)(N2 * 64 * 4), 128, 64u * 32u);
-        for (int ks = 0; ks < 8; ++ks) {
-          tc::mma_tf32(d2, dA2_hi + 16u * ks, dbh + 16u * ks, idesc2, (g2 > 0 || ks > 0) ? 1u : 0u);
-          tc::mma_tf32(d2, dA2_hi + 16u * ks, dbl + 16u * ks, idesc2, 1u);
-          tc::mma_tf32(d2, dA2_lo + 16u * ks, dbh + 16u * ks, idesc2, 1u);
+        const uint64_t dbh = tc::sdesc(bh, 128, (uint32_t)kB2c * 32u);
+        const uint64_t dbl = tc::sdesc(bh + (uint32_t)(N2 * kB2c * 4), 128, (uint32_t)kB2c * 32u);
+        if (tc::elect_one()) {
+          for (int ks = 0; ks < kB2c / 8; ++ks) {
+            const uint32_t kg = (uint32_t)(ch * (kB2c / 8) + ks);
+            tc::mma_tf32_ts(d2, ta2_hi + 8u * kg, dbh + 16u * ks, idesc2, (g2 > 0 || kg > 0) ? 1u : 0u);
+            tc::mma_tf32_ts(d2, ta2_hi + 8u * kg, dbl + 16u * ks, idesc2, 1u);
+            tc::mma_tf32_ts(d2, ta2_lo + 8u * kg, dbh + 16u * ks, idesc2, 1u);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (ch == 64 / kB2c - 1) tc::mma_commit(&a2empty);
         }
-        tc::mma_commit(&empty[stage]);
-        tc::mma_commit(&a2empty);
+        __syncwarp();
+        if (++stage == NS) { stage = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (++stage == NS) { stage = 0; ph ^= 1; }
       ++g2;
     };
     int G = 0;
@@ -484,6 +482,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const int c = q * 32 + lane;
     const int64_t colg = col0 + c;
     const float th2 = a.thr[b] * a.thr[b];
+    const uint32_t lq = (uint32_t)(q * 32) << 16;
     int buf = 0;
     uint32_t bph = 0;
     int g = 0;
@@ -509,7 +508,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
         float v[32];
-        const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kBwN1 + h * 32);
+        const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 32);
         tc::tmem_ld16_nowait(ta, v);
         tc::tmem_ld16_nowait(ta + 16, v + 16);
         tc::tmem_wait_ld();
@@ -517,7 +516,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         if (++buf == 2) { buf = 0; bph ^= 1; }
-        float gw[32];
+        float ghi[32], glo[32];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float gv = 0.f;
@@ -526,23 +525,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           const float re = v[2 * i], im = v[2 * i + 1];
           const float m2 = fmaf(re, re, im * im);
           const float s = (m2 > 1.17549435e-38f && m2 > th2) ? gv * rsqrtf(m2) : 0.f;
-          gw[2 * i] = re * s;
-          gw[2 * i + 1] = im * s;
+          tc::split_tf32(re * s, ghi[2 * i], glo[2 * i]);
+          tc::split_tf32(im * s, ghi[2 * i + 1], glo[2 * i + 1]);
         }
-        // A2 is free once GEMM2(g-1) completed
+        // A2 (TMEM) is free once GEMM2(g-1) completed
         tc::mbar_wait(&a2empty, (uint32_t)((g & 1) ^ 1));
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 hv, lv;
-          tc::split_tf32(gw[4 * j + 0], hv.x, lv.x);
-          tc::split_tf32(gw[4 * j + 1], hv.y, lv.y);
-          tc::split_tf32(gw[4 * j + 2], hv.z, lv.z);
-          tc::split_tf32(gw[4 * j + 3], hv.w, lv.w);
-          const uint32_t o = tc::core_off((uint32_t)c, (uint32_t)(h * 32 + 4 * j), 64u) / 4;
-          *reinterpret_cast<float4*>(a2_hi + o) = hv;
-          *reinterpret_cast<float4*>(a2_lo + o) = lv;
-        }
-        tc::fence_async_smem();
+        tc::tc_fence_after();
+        tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 32), ghi);
+        tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 32 + 16), ghi + 16);
+        tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 32), glo);
+        tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 32 + 16), glo + 16);
+        tc::tmem_wait_st();
+        tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&a2full);
       }
@@ -557,7 +551,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       for (int c0 = 0; c0 < N2; c0 += 16) {
         float v[16];
         if (g > 0) {
-          tc::tmem_ld16(d2 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+          tc::tmem_ld16(d2 + lq + (uint32_t)c0, v);
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -574,19 +568,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, 256);
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
 template <int KAP>
-static void launch_tc_bwd(const TcBwArgs& a, int K2max, int64_t ntiles, int B, cudaStream_t st) {
-  const int N2max = ((K2max + 15) / 16) * 16;
-  const int STG = std::max(2 * kBwN1 * K2max, 2 * N2max * 64);
+static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream_t st) {
+  const int N2max = ((2 * C.Kmax + 15) / 16) * 16;
+  const int STG = std::max(2 * kBwN1 * C.kcw, 2 * N2max * kB2c);
   int NS = kTcMaxStages;
-  auto smem = [&](int ns) { return (size_t)(2 * 128 * K2max + 2 * 128 * 64 + ns * STG) * 4 + 1024; };
-  while (NS > 2 && smem(NS) > 225 * 1024) --NS;
+  auto smem = [&](int ns) { return (size_t)(2 * 128 * C.K2max + ns * STG) * 4 + 1024; };
+  while (NS > 2 && smem(NS) > 224 * 1024) --NS;
   const size_t sm = smem(NS);
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 g((unsigned)ntiles, (unsigned)B);
+  dim3 g((unsigned)C.ntiles, (unsigned)B);
   k_joint_bwd_tc<KAP><<<g, kTcThreads, sm, st>>>(a, NS, STG);
   count_launch();
 }
@@ -594,15 +588,15 @@ static void launch_tc_bwd(const TcBwArgs& a, int K2max, int64_t ntiles, int B, c
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
                          int B, cudaStream_t st) {
-  for (int cls = 0; cls < 3; ++cls) {
+  for (int cls = 0; cls < kTcBwClasses; ++cls) {
     const TcClass& C = d.tcb[cls];
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
                d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr};
-    switch (cls) {
-      case 0: launch_tc_bwd<2>(a, C.K2max, C.ntiles, B, st); break;
-      case 1: launch_tc_bwd<4>(a, C.K2max, C.ntiles, B, st); break;
-      case 2: launch_tc_bwd<8>(a, C.K2max, C.ntiles, B, st); break;
+    switch (cls % 3) {  // class = 3 * kcw_kind + kap_kind
+      case 0: launch_tc_bwd<2>(a, C, B, st); break;
+      case 1: launch_tc_bwd<4>(a, C, B, st); break;
+      case 2: launch_tc_bwd<8>(a, C, B, st); break;
     }
   }
 }

@@ -63,8 +63,12 @@ struct TcUnit {
 };
 struct TcBlock {
   int32_t bi, K, K2, cls;    // block, n1_max, padded 2K, launch class
+  int32_t kcw, pad;          // width (k' elements) of the B-image chunks: 32, or 16 when K2 > 120
 };
-constexpr int kTcClasses = 6;   // (CT, KAP) = (2,2) (2,4) (2,8) (1,2) (1,4) (1,8)
+// forward classes 3*ct_kind + kap_kind (ct_kind: 0 = 2 column tiles, 1 = 1 tile kcw 32,
+// 2 = 1 tile kcw 16; kap_kind: rows_out <= 2, 4, 8); backward classes 3*(kcw == 16) + kap_kind
+constexpr int kTcClasses = 9;
+constexpr int kTcBwClasses = 6;
 
 struct DeviceTables;  // device pointers (jtfs_api.cu)
 

@@ -167,17 +167,20 @@ static void build_tc_tables(Plan* p) {
     const int K2 = ((2 * K + 7) / 8) * 8;
     int ro_max = 0;
     for (int f = 0; f < nfr; ++f) ro_max = std::max(ro_max, p->units[bi * nfr + f].rows_out);
-    if (K2 > 120 || ro_max > 8) continue;
+    if (K2 > 168 || ro_max > 8) continue;   // resident A tile (128 x K2 x 8 B) must fit in SMEM
     const int CT = K2 <= 64 ? 2 : 1;
+    const int kcw = K2 <= 120 ? 32 : 16;
     const int kap = ro_max <= 2 ? 0 : (ro_max <= 4 ? 1 : 2);
+    const int ctk = CT == 2 ? 0 : (kcw == 32 ? 1 : 2);
     p->blk_tc[bi] = 1;
-    p->tc_blocks.push_back({(int32_t)bi, K, K2, (CT == 2 ? 0 : 3) + kap});
-    const bool bwd = K2 <= 80;
+    p->tc_blocks.push_back({(int32_t)bi, K, K2, 3 * ctk + kap, kcw, 0});
+    const int N2 = ((2 * K + 15) / 16) * 16;
+    const int64_t stg = std::max(2 * 64 * kcw, 2 * N2 * 16);
+    const bool bwd = N2 <= 256 && (int64_t)(2 * 128 * K2 + 2 * stg) * 4 + 1024 <= 224 * 1024;
     if (bwd) {
       p->blk_tcb[bi] = 1;
-      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap});
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, 3 * (kcw == 16 ? 1 : 0) + kap, kcw, 0});
     }
-    const int N2 = ((2 * K + 15) / 16) * 16;
     for (int f = 0; f < nfr; ++f) {
       const int u = (int)bi * nfr + f;
       const JointUnit& U = p->units[u];
@@ -186,61 +189,62 @@ static void build_tc_tables(Plan* p) {
       tu.img_off = (int64_t)p->tc_img.size();
       tu.wt_off = (int64_t)p->tc_wts.size();
       const double* h = p->hfr_d.data() + (size_t)U.f * p->P * 2;
+      auto Mval = [&](int64_t lr, int n, double* mr, double* mi) {
+        const int64_t r = (U.r_lo + lr) % U.Lf;
+        const int64_t e = (((r << U.kf) - n) % p->P + p->P) % p->P;
+        *mr = h[2 * e];
+        *mi = h[2 * e + 1];
+      };
+      auto put = [&](std::vector<float>& img, size_t hi_base, size_t lo_base, uint32_t o, double v) {
+        const float xf = (float)v;
+        const float hi = tf32_rna_host(xf);
+        img[hi_base + o] = hi;
+        img[lo_base + o] = tf32_rna_host(xf - hi);
+      };
+      // forward images: per 64-row tile, per kcw-wide chunk: [hi 128 x kc | lo 128 x kc]
       for (int t = 0; t < tu.NT; ++t) {
-        for (int ch = 0; ch * 32 < K2; ++ch) {
-          const int kc = std::min(32, K2 - ch * 32);
+        for (int ch = 0; ch * kcw < K2; ++ch) {
+          const int kc = std::min(kcw, K2 - ch * kcw);
           const size_t base = p->tc_img.size();
           p->tc_img.resize(base + 2 * 128 * kc, 0.f);
           for (int nn = 0; nn < 128; ++nn) {
             const int i = nn / 2, po = nn % 2;
             const int64_t lr = (int64_t)t * 64 + i;
             if (lr >= U.n_rows) continue;
-            const int64_t r = (U.r_lo + lr) % U.Lf;
             for (int kl = 0; kl < kc; ++kl) {
-              const int kk = ch * 32 + kl, n = kk / 2, pi = kk % 2;
+              const int kk = ch * kcw + kl, n = kk / 2, pi = kk % 2;
               if (n >= K) continue;
-              const int64_t e = (((r << U.kf) - n) % p->P + p->P) % p->P;
-              const double mr = h[2 * e], mi = h[2 * e + 1];
-              double v;
-              if (po == 0) v = (pi == 0) ? mr : -mi;   // Re W = Re M Re Y - Im M Im Y
-              else v = (pi == 0) ? mi : mr;            // Im W = Im M Re Y + Re M Im Y
-              const float xf = (float)v;
-              const float hi = tf32_rna_host(xf);
-              const float lo = tf32_rna_host(xf - hi);
-              const uint32_t o = core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kc) / 4;
-              p->tc_img[base + o] = hi;
-              p->tc_img[base + 128 * kc + o] = lo;
+              double mr, mi;
+              Mval(lr, n, &mr, &mi);
+              // Re W = Re M Re Y - Im M Im Y ; Im W = Im M Re Y + Re M Im Y
+              const double v = (po == 0) ? ((pi == 0) ? mr : -mi) : ((pi == 0) ? mi : mr);
+              put(p->tc_img, base, base + 128 * kc, core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kc) / 4, v);
             }
           }
         }
       }
-      // backward B2 images: per 32-row tile, [hi | lo] of N2 x 64 (canonical K-major),
+      // backward B2 images: per 32-row tile, per 16-wide kk chunk: [hi N2 x 16 | lo N2 x 16]
       // B2[2n][2i] = Re M, B2[2n][2i+1] = Im M, B2[2n+1][2i] = -Im M, B2[2n+1][2i+1] = Re M
       if (bwd) {
         tu.img2_off = (int64_t)p->tc_img2.size();
         const int NT32 = (int)((U.n_rows + 31) / 32);
         for (int t = 0; t < NT32; ++t) {
-          const size_t base = p->tc_img2.size();
-          p->tc_img2.resize(base + 2 * (size_t)N2 * 64, 0.f);
-          for (int nn = 0; nn < N2; ++nn) {
-            const int n = nn / 2, po = nn % 2;
-            if (n >= K) continue;
-            for (int kk = 0; kk < 64; ++kk) {
-              const int i = kk / 2, pi = kk % 2;
-              const int64_t lr = (int64_t)t * 32 + i;
-              if (lr >= U.n_rows) continue;
-              const int64_t r = (U.r_lo + lr) % U.Lf;
-              const int64_t e = (((r << U.kf) - n) % p->P + p->P) % p->P;
-              const double mr = h[2 * e], mi = h[2 * e + 1];
-              double v;
-              if (po == 0) v = (pi == 0) ? mr : mi;      // Re g_Y = Re M Re g_W + Im M Im g_W
-              else v = (pi == 0) ? -mi : mr;             // Im g_Y = -Im M Re g_W + Re M Im g_W
-              const float xf = (float)v;
-              const float hi = tf32_rna_host(xf);
-              const float lo = tf32_rna_host(xf - hi);
-              const uint32_t o = core_off_host((uint32_t)nn, (uint32_t)kk, 64u) / 4;
-              p->tc_img2[base + o] = hi;
-              p->tc_img2[base + (size_t)N2 * 64 + o] = lo;
+          for (int ch = 0; ch < 4; ++ch) {
+            const size_t base = p->tc_img2.size();
+            p->tc_img2.resize(base + 2 * (size_t)N2 * 16, 0.f);
+            for (int nn = 0; nn < N2; ++nn) {
+              const int n = nn / 2, po = nn % 2;
+              if (n >= K) continue;
+              for (int kl = 0; kl < 16; ++kl) {
+                const int kk = ch * 16 + kl, i = kk / 2, pi = kk % 2;
+                const int64_t lr = (int64_t)t * 32 + i;
+                if (lr >= U.n_rows) continue;
+                double mr, mi;
+                Mval(lr, n, &mr, &mi);
+                // Re g_Y = Re M Re g_W + Im M Im g_W ; Im g_Y = -Im M Re g_W + Re M Im g_W
+                const double v = (po == 0) ? ((pi == 0) ? mr : mi) : ((pi == 0) ? -mi : mr);
+                put(p->tc_img2, base, base + (size_t)N2 * 16, core_off_host((uint32_t)nn, (uint32_t)kl, 16u) / 4, v);
+              }
             }
           }
         }

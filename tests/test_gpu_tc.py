@@ -47,3 +47,22 @@ def test_tc_gemm(N, K):
         torch.cuda.synchronize()
         err = np.abs(D.cpu().numpy() - ref).max() / np.abs(ref).max()
         assert err < tol, (three, err)
+
+
+@pytest.mark.parametrize("N,K", [(16, 16), (64, 64), (128, 128), (256, 32)])
+def test_tc_gemm_a_in_tmem(N, K):
+    from paper_2602_11896_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(N * 7 + K)
+    A = rng.standard_normal((128, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    Ad = torch.from_numpy(A).cuda()
+    Bd = torch.from_numpy(image(B)).cuda()
+    for three, tol in ((0, 3e-3), (1, 2e-6)):
+        D = torch.zeros(128, N, device="cuda")
+        _lib.check(lib.jtfs_debug_tc_gemm_ts(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), N, K, three,
+                                             torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        err = np.abs(D.cpu().numpy() - ref).max() / np.abs(ref).max()
+        assert err < tol, (three, err)
