@@ -222,8 +222,7 @@ def main() -> None:
     ms = e0.elapsed_time(e1)
     launches = plan.launch_count() - n0
     plan.prof_enable(False)
-    fwd_ms, fwd_n = plan.prof_read(0)
-    bwd_ms, bwd_n = plan.prof_read(1)
+    prof = {k: plan.prof_read(i) for i, k in enumerate(["fwd_tc", "fwd_simt", "bwd_tc", "bwd_simt"])}
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
@@ -268,14 +267,31 @@ def main() -> None:
     pk = peaks()
     cost = plan.cost()
     clock_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    fp32_peak_tflops = N_SM * FP32_LANES_PER_SM * 2 * clock_mhz * 1e6 / 1e12
-    # dominant kernel: the joint-stage backward (k_joint_bwd), one launch per micro-batch
-    per_launch_signals = B / max(1, bwd_n / args.steps)
-    bwd_flops_launch = cost["joint_bwd_flops"] * per_launch_signals
-    bwd_avg_s = (bwd_ms / max(1, bwd_n)) / 1000.0
-    achieved = bwd_flops_launch / bwd_avg_s / 1e12 if bwd_n else None
-    fwd_flops_launch = cost["joint_fwd_flops"] * B / max(1, fwd_n / args.steps)
-    fwd_avg_s = (fwd_ms / max(1, fwd_n)) / 1000.0
+    # peaks: FP32 lanes from the guide's unit counts at the max SM clock; TF32 dense
+    # = measured bf16 burst x nominal tf32/bf16 ratio (1.1/2.25); hi/lo 3xTF32 executes 3 MMAs
+    fp32_peak = N_SM * FP32_LANES_PER_SM * 2 * clock_mhz * 1e6 / 1e12
+    tf32_peak = float(pk.get("bf16_tflops", 1590.0)) * (1.1 / 2.25)
+    kern = {}
+    for k, (kms, kn) in prof.items():
+        if kn == 0:
+            continue
+        flops = cost[k + "_flops"] * B                    # algorithmic flops per step
+        avg_s = (kms / kn) / 1000.0                        # per launch group (one per micro-batch)
+        per_launch = flops / (kn / args.steps)
+        tc = k.endswith("_tc")
+        ach = (3.0 if tc else 1.0) * per_launch / avg_s / 1e12
+        peak = tf32_peak if tc else fp32_peak
+        kern[k] = {"ms_per_step": kms / args.steps, "bound": "tensor" if tc else "alu",
+                   "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"]) if kern else None
+    roof = dict(kern[dom]) if dom else {}
+    roof.update({"kernel": {"bwd_tc": "k_joint_bwd_tc", "bwd_simt": "k_joint_bwd", "fwd_tc": "k_joint_fwd_tc",
+                            "fwd_simt": "k_joint_fwd"}.get(dom, dom),
+                 "traffic": None, "share_of_step": roof.get("ms_per_step", 0) / (ms / args.steps) if ms else None,
+                 "peak_note": ("tensor: TF32 dense = measured bf16 %.0f TF x 1.1/2.25; achieved counts the 3 TF32 "
+                               "MMAs of 3xTF32; alu: FP32 148 SM x 128 lanes x 2 x %.0f MHz" %
+                               (float(pk.get("bf16_tflops", 1590.0)), clock_mhz)),
+                 "joint_kernels": kern})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -283,12 +299,7 @@ def main() -> None:
         "config": {"workload": f"{args.config}: {_describe(args.config)} per rank",
                    "l2": "per-step working set > 126 MB L2 (no flush needed)",
                    "micro_batch": int(mb), "parallelism": f"batch{n_groups}xpath{ps}"},
-        "roofline": {"kernel": "k_joint_bwd", "bound": "alu", "achieved": achieved,
-                     "peak": fp32_peak_tflops, "unit": "TFLOP/s",
-                     "frac": (achieved / fp32_peak_tflops) if achieved else None, "traffic": None,
-                     "peak_note": f"FP32 148 SM x 128 lanes x 2 x {clock_mhz:.0f} MHz (guide units, max clock)",
-                     "share_of_step": (bwd_ms + fwd_ms) / ms if ms else None,
-                     "k_joint_fwd_tflops": (fwd_flops_launch / fwd_avg_s / 1e12) if fwd_n else None},
+        "roofline": roof,
         "clocks": clk, "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
     }
     if e2e:

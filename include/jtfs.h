@@ -157,15 +157,18 @@ jtfs_status jtfs_debug_tc_gemm_ts(const float* A, const float* Bimg, float* D, i
 /* Number of kernels the library has launched in this process (for launch-count reporting). */
 int64_t jtfs_launch_count(void);
 
-/* Algorithmic cost per signal (for roofline reporting): out[0] = FP32 flops of the
- * joint-stage forward kernels (8*K per modulus value for the dense lambda_1 contraction, + 3 for the
- * modulus + 2*rows_out for phi_F, over the pruned rows x columns), out[1] = same for the joint
- * backward (16*K + 2*rows_out + 6), out[2] = number of modulus values, out[3] = HBM bytes of the
- * joint stage (Y2 read fwd + Y2 read bwd + g_Y2 write + o write/read). cap >= 4. */
+/* Algorithmic cost per signal of the joint lambda_1 stage (roofline reporting),
+ * over the pruned rows x columns ("cells", one modulus value each):
+ *  out[0] forward dense-contraction flops on the tensor-core blocks (8 K per cell)
+ *  out[1] forward flops on the CUDA-core blocks (8 K + 3 + 2 rows_out per cell)
+ *  out[2] backward contraction flops on the tensor-core blocks (16 K per cell)
+ *  out[3] backward flops on the CUDA-core blocks (16 K + 6 + 2 rows_out per cell)
+ *  out[4] cells, out[5] HBM bytes of the joint stage (Y2 r fwd + r bwd, g_Y2 w, o w + g_o r). cap >= 8. */
 jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap);
 
 /* Profiling hook used by bench.py: when enabled, CUDA events are recorded on the launch stream
- * around the joint-stage kernels (id 0 = forward, 1 = backward). jtfs_prof_read synchronises on the
+ * around the joint-stage kernels (id 0 = forward tensor-core, 1 = forward CUDA-core,
+ * 2 = backward tensor-core, 3 = backward CUDA-core). jtfs_prof_read synchronises on the
  * recorded events, returns the summed elapsed milliseconds and the number of timed launches of
  * `id`, and clears them. */
 void jtfs_prof_enable(int on);

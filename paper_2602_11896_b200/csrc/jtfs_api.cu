@@ -31,7 +31,7 @@ static std::atomic<int> g_prof{0};
 static std::mutex g_prof_mu;
 struct ProfRec { int id; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof_recs;
-static thread_local cudaEvent_t t_open[2] = {nullptr, nullptr};
+static thread_local cudaEvent_t t_open[4] = {nullptr, nullptr, nullptr, nullptr};
 void prof_begin(cudaStream_t st, int id) {
   if (!g_prof.load()) return;
   cudaEventCreate(&t_open[id]);
@@ -375,8 +375,10 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     // A5: joint lambda_1 stage + phi_F; A6: phi_T
     prof_begin(st, 0);
     launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
-    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
     prof_end(st, 0);
+    prof_begin(st, 1);
+    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
+    prof_end(st, 1);
     launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, shard, n_shards, mb, st);
   }
   RET();
@@ -393,10 +395,12 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     // A7: phi_T adjoint (r -> g_o, reusing o), joint adjoint (-> g_Y2 in A)
     launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, shard, n_shards, mb, st);
     if ((e = cudaMemsetAsync(w.A, 0, (size_t)w.s_A * 8 * mb, st))) return e;
-    prof_begin(st, 1);
+    prof_begin(st, 2);
     launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
+    prof_end(st, 2);
+    prof_begin(st, 3);
     launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
-    prof_end(st, 1);
+    prof_end(st, 3);
     // FFT of g_Y2 rows -> G_Y (into Y2)
     for (auto& g : p.y2_groups) {
       Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
@@ -455,21 +459,23 @@ jtfs_status jtfs_prof_read(int id, double* total_ms, int64_t* count) {
 }
 
 jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap) {
-  if (!plan || !out || cap < 4) return fail(JTFS_ERR_SIZE, "NULL argument or cap < 4");
+  if (!plan || !out || cap < 8) return fail(JTFS_ERR_SIZE, "NULL argument or cap < 8");
   const Plan& p = plan->p;
-  double ff = 0, fb = 0, nm = 0, by = 0;
+  double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (auto& u : p.units) {
-    double cells = (double)u.n_rows * (double)p.binfo[u.bi].n_cols;
-    nm += cells;
-    ff += cells * (8.0 * u.n1_max + 3.0 + 2.0 * u.rows_out);
-    fb += cells * (16.0 * u.n1_max + 6.0 + 2.0 * u.rows_out);
-    by += 2.0 * 4.0 * u.rows_out * p.binfo[u.bi].n_cols;   // o written (fwd) and g_o read (bwd)
+    const double cells = (double)u.n_rows * (double)p.binfo[u.bi].n_cols;
+    const bool tf = g_use_tc && p.blk_tc[u.bi], tb = g_use_tc && p.blk_tcb[u.bi];
+    c[tf ? 0 : 1] += cells * (tf ? 8.0 * u.n1_max : 8.0 * u.n1_max + 3.0 + 2.0 * u.rows_out);
+    c[tb ? 2 : 3] += cells * (tb ? 16.0 * u.n1_max : 16.0 * u.n1_max + 6.0 + 2.0 * u.rows_out);
+    c[4] += cells;
+    c[5] += 2.0 * 4.0 * u.rows_out * p.binfo[u.bi].n_cols;   // o written (fwd) and g_o read (bwd)
   }
   for (size_t bi = 0; bi < p.blocks.size(); ++bi)
-    by += 3.0 * 8.0 * p.blocks[bi].n1_max * p.binfo[bi].n_cols;  // Y2 read fwd, read bwd, g_Y2 write
-  out[0] = ff; out[1] = fb; out[2] = nm; out[3] = by;
+    c[5] += 3.0 * 8.0 * p.blocks[bi].n1_max * p.binfo[bi].n_cols;  // Y2 read fwd, read bwd, g_Y2 write
+  for (int i = 0; i < 8; ++i) out[i] = c[i];
   return JTFS_OK;
 }
+
 int64_t jtfs_launch_count(void) { return jtfs::g_launches.load(); }
 
 jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, jtfs_plan_t* out) {
