@@ -49,7 +49,7 @@ struct DeviceTables {
   int64_t* o1_rlo = nullptr;        int64_t* o1_nrows = nullptr;
   float2* tw = nullptr;
   double2* twd = nullptr;
-  int Kmax = 0;
+  int Kmax = 0, Kmax_simt_bwd = 0;
   // tensor-core joint stage
   float* tc_img = nullptr;
   float* tc_wts = nullptr;

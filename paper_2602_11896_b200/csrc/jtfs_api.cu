@@ -210,9 +210,10 @@ static cudaError_t upload(Plan& p) {
   for (size_t bi = 0; bi < p.blocks.size(); ++bi) {
     nm.push_back(p.blocks[bi].n1_max);
     d->Kmax = std::max(d->Kmax, p.blocks[bi].n1_max);
-    int64_t ntc = (p.binfo[bi].n_cols + kJC - 1) / kJC;
-    int64_t nr = (p.blocks[bi].n1_max + kJN - 1) / kJN;
-    bt.push_back((g_use_tc && p.blk_tcb[bi]) ? 0 : ntc * nr);   // TC-backward blocks: no SIMT tiles
+    // CUDA-core backward: 32-column tiles over all n1 rows; blocks on the tensor-core path: none
+    const bool simt = !(g_use_tc && p.blk_tcb[bi]);
+    bt.push_back(simt ? (p.binfo[bi].n_cols + 31) / 32 : 0);
+    if (simt) d->Kmax_simt_bwd = std::max(d->Kmax_simt_bwd, p.blocks[bi].n1_max);
   }
   UP(nm, blk_nmax);
   t = prefix(bt); UP(t, bwd_tiles); d->bwd_ntiles = t.back();

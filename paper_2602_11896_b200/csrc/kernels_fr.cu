@@ -473,6 +473,144 @@ __global__ void __launch_bounds__(256) k_joint_bwd(
   }
 }
 
+
+// =====================================================================================
+// Joint stage backward on CUDA cores for the blocks the tensor-core kernel does not take (large
+// n1_max, few columns): one CTA = (block, 32-column tile, signal) over ALL K rows of n1, so W is
+// recomputed exactly once; g_Y2 accumulates in SMEM (each thread owns fixed entries: deterministic).
+// =====================================================================================
+constexpr int kB2C = 32;
+__global__ void __launch_bounds__(256) k_joint_bwd2(
+    const float2* __restrict__ Y2, int64_t y_sb, const float* __restrict__ go, int64_t go_sb,
+    float2* __restrict__ gY2, int64_t gy_sb, const JointUnit* __restrict__ units, int nfr,
+    const int64_t* __restrict__ tiles, int n_blocks, const BlockInfo* __restrict__ binfo,
+    const float2* __restrict__ hfr, int P, const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off,
+    int shard, int n_shards, int maxLf, const float* __restrict__ thr) {
+  extern __shared__ float4 smem4[];
+  const int bi = find_idx(tiles, n_blocks, blockIdx.x);
+  const BlockInfo bf = binfo[bi];
+  const int K = units[bi * nfr].n1_max;
+  const int64_t col0 = (int64_t)(blockIdx.x - tiles[bi]) * kB2C;
+  const int b = blockIdx.y;
+  const int tid = threadIdx.x;
+  float2* Ys = reinterpret_cast<float2*>(smem4);     // [K][32]
+  float2* Gy = Ys + K * kB2C;                        // [K][32]
+  float2* hs = Gy + K * kB2C;                        // [P]
+  float2* Gw = hs + P;                               // [64][32]
+  float* gs = reinterpret_cast<float*>(Gw + kJR * kB2C);  // [maxLf]
+  float* Go = gs + maxLf;                            // [32][32]
+  int* hbs = reinterpret_cast<int*>(Go + 32 * kB2C); // [64]
+  const float2* ysrc = Y2 + b * y_sb + bf.y_off;
+  for (int idx = tid; idx < K * kB2C; idx += 256) {
+    const int n = idx / kB2C, c = idx % kB2C;
+    const int64_t col = col0 + c;
+    Ys[idx] = (col < bf.n_cols) ? ysrc[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2] : make_float2(0.f, 0.f);
+    Gy[idx] = make_float2(0.f, 0.f);
+  }
+  const float th2 = thr[b] * thr[b];
+  const int tr = tid >> 4, tc = tid & 15;            // GEMM1: 4 rows x 2 columns per thread
+  const int NG = (K + 3) / 4;                        // GEMM2: tiles of 4 n x 2 columns
+  const int ntile2 = NG * 16;
+  for (int f = 0; f < nfr; ++f) {
+    const int uidx = bi * nfr + f;
+    if (uidx % n_shards != shard) continue;
+    const JointUnit U = units[uidx];
+    const int Lf = (int)U.Lf;
+    __syncthreads();
+    for (int idx = tid; idx < P; idx += 256) hs[idx] = hfr[(int64_t)U.f * P + idx];
+    const float* gsrc = phiF_k + phiF_off[U.kf];
+    for (int idx = tid; idx < Lf; idx += 256) gs[idx] = gsrc[idx];
+    for (int idx = tid; idx < U.rows_out * kB2C; idx += 256) {
+      const int q = idx / kB2C, c = idx % kB2C;
+      const int64_t col = col0 + c;
+      Go[idx] = (col < bf.n_cols) ? go[b * go_sb + U.o_off + (int64_t)q * bf.n_cols + col] : 0.f;
+    }
+    __syncthreads();
+    for (int64_t r0 = 0; r0 < U.n_rows; r0 += kJR) {
+      int hb[4], rr[4];
+      bool valid[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t lr = r0 + tr * 4 + i;
+        valid[i] = lr < U.n_rows;
+        const int r = (int)((U.r_lo + lr) % Lf);
+        rr[i] = r;
+        hb[i] = (r << U.kf) & (P - 1);
+      }
+      if (tc == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hbs[tr * 4 + i] = hb[i];
+      }
+      float2 acc[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+#pragma unroll 2
+      for (int n = 0; n < K; ++n) {
+        const float4 yv = *reinterpret_cast<const float4*>(Ys + n * kB2C + tc * 2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 h = hs[(hb[i] - n) & (P - 1)];
+          acc[i][0].x = fmaf(h.x, yv.x, fmaf(-h.y, yv.y, acc[i][0].x));
+          acc[i][0].y = fmaf(h.x, yv.y, fmaf(h.y, yv.x, acc[i][0].y));
+          acc[i][1].x = fmaf(h.x, yv.z, fmaf(-h.y, yv.w, acc[i][1].x));
+          acc[i][1].y = fmaf(h.x, yv.w, fmaf(h.y, yv.z, acc[i][1].y));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float gv = 0.f;
+          if (valid[i])
+            for (int q = 0; q < U.rows_out; ++q)
+              gv = fmaf(gs[((q << U.d) - rr[i]) & (Lf - 1)], Go[q * kB2C + tc * 2 + c], gv);
+          const float m2 = acc[i][c].x * acc[i][c].x + acc[i][c].y * acc[i][c].y;
+          const float s = (valid[i] && m2 > FLT_MIN && m2 > th2) ? gv * rsqrtf(m2) : 0.f;
+          Gw[(tr * 4 + i) * kB2C + tc * 2 + c] = make_float2(acc[i][c].x * s, acc[i][c].y * s);
+        }
+      }
+      __syncthreads();
+      // GEMM2: Gy[n][c] += sum_i conj(h[(hb_i - n) mod P]) Gw[i][c]
+      const int nrow = (int)((U.n_rows - r0) < kJR ? (U.n_rows - r0) : kJR);
+      for (int t2 = tid; t2 < ntile2; t2 += 256) {
+        const int ng = t2 >> 4, cg = t2 & 15;
+        float2 a2[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a2[j][0] = a2[j][1] = make_float2(0.f, 0.f);
+        for (int i = 0; i < nrow; ++i) {
+          const int hbi = hbs[i];
+          const float4 gw = *reinterpret_cast<const float4*>(Gw + i * kB2C + cg * 2);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 h = hs[(hbi - (ng * 4 + j)) & (P - 1)];
+            a2[j][0].x = fmaf(h.x, gw.x, fmaf(h.y, gw.y, a2[j][0].x));
+            a2[j][0].y = fmaf(h.x, gw.y, fmaf(-h.y, gw.x, a2[j][0].y));
+            a2[j][1].x = fmaf(h.x, gw.z, fmaf(h.y, gw.w, a2[j][1].x));
+            a2[j][1].y = fmaf(h.x, gw.w, fmaf(-h.y, gw.z, a2[j][1].y));
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int n = ng * 4 + j;
+          if (n < K) {
+            float2* g0 = Gy + n * kB2C + cg * 2;
+            g0[0] = cadd(g0[0], a2[j][0]);
+            g0[1] = cadd(g0[1], a2[j][1]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  float2* gdst = gY2 + b * gy_sb + bf.y_off;
+  for (int idx = tid; idx < K * kB2C; idx += 256) {
+    const int n = idx / kB2C, c = idx % kB2C;
+    const int64_t col = col0 + c;
+    if (col < bf.n_cols) gdst[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2] = Gy[idx];
+  }
+}
+
 // =====================================================================================
 // phi_T along time (Eq.4, level s2, stride T) -> packed order-2 coefficients; one warp per output
 // =====================================================================================
@@ -683,15 +821,14 @@ void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st) {
-  if (d.n_blocks == 0) return;
-  size_t sm = (size_t)d.Kmax * kJC * 8 + (size_t)p.P * 8 + (size_t)kJR * kJC * 8 + (size_t)d.maxLf * 4 +
-              (size_t)32 * kJC * 4 + 64 * 4;
-  cudaFuncSetAttribute(k_joint_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (d.bwd_ntiles == 0) return;
+  if (d.n_blocks == 0 || d.bwd_ntiles == 0) return;
+  const size_t sm = (size_t)2 * d.Kmax_simt_bwd * kB2C * 8 + (size_t)p.P * 8 + (size_t)kJR * kB2C * 8 +
+                    (size_t)d.maxLf * 4 + (size_t)32 * kB2C * 4 + 64 * 4;
+  cudaFuncSetAttribute(k_joint_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)d.bwd_ntiles, (unsigned)B);
-  k_joint_bwd<<<g, 256, sm, st>>>(Y2, y_sb, go, go_sb, gY2, gy_sb, d.units, (int)p.L_fr.size(), d.bwd_tiles,
-                                  d.n_blocks, d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, shard, n_shards,
-                                  d.maxLf, thr);
+  k_joint_bwd2<<<g, 256, sm, st>>>(Y2, y_sb, go, go_sb, gY2, gy_sb, d.units, (int)p.L_fr.size(), d.bwd_tiles,
+                                   d.n_blocks, d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, shard, n_shards,
+                                   d.maxLf, thr);
   count_launch();
 }
 
