@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libjtfs.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["planner.cpp", "fft.cu", "kernels_time.cu", "kernels_fr.cu", "jtfs_api.cu", "tc_selftest.cu", "kernels_tc.cu"]
+SOURCES = ["planner.cpp", "fft.cu", "kernels_time.cu", "kernels_fr.cu", "jtfs_api.cu", "tc_selftest.cu", "kernels_tc.cu", "kernels_frfft.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]

@@ -17,6 +17,13 @@ struct TcClass {
   int K2max = 0, Kmax = 0, kcw = 32;
 };
 
+struct FfList {                    // blocks on the FFT route of the joint stage + column-tile prefix
+  int32_t* blist = nullptr;
+  int64_t* tiles = nullptr;
+  int nb = 0;
+  int64_t ntiles = 0;
+};
+
 struct DeviceTables {
   float* spec_vals = nullptr;
   GatherJob* l1_jobs = nullptr;     int64_t* l1_tiles = nullptr;   int n_l1 = 0;   int64_t l1_ntiles = 0;
@@ -57,6 +64,11 @@ struct DeviceTables {
   TcClass tc[kTcClasses];
   float* tc_img2 = nullptr;
   TcClass tcb[kTcBwClasses];
+  // FFT route (kernels_frfft.cu)
+  float* fr_spec = nullptr;
+  float* u_wts = nullptr;
+  int64_t* u_wt_off = nullptr;
+  FfList ffw, ffb;
 };
 
 constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels
@@ -119,5 +131,13 @@ void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st);
+
+// ---- kernels_frfft.cu
+void launch_joint_fft(const Plan& p, const DeviceTables& d, bool bwd, const float2* Y2, int64_t y_sb, float* o,
+                      int64_t o_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
+                      cudaStream_t st);
+int64_t joint_fft_tiles(int64_t n_cols);
+constexpr int kFfMaxP = 1024;      // FFT route: C x P <= 4096 points per CTA
+constexpr int kFfMaxRo = 64;       // FFT route backward: rows_out <= 64
 
 }  // namespace jtfs

@@ -18,107 +18,9 @@
 
 #include "common.cuh"
 #include "fft.cuh"
+#include "fft_dev.cuh"
 
 namespace jtfs {
-
-static constexpr int kTw = 4096;  // twiddle table length
-
-template <class C> struct Cx;
-template <> struct Cx<float2> {
-  using R = float;
-  __device__ static float2 mk(float a, float b) { return make_float2(a, b); }
-};
-template <> struct Cx<double2> {
-  using R = double;
-  __device__ static double2 mk(double a, double b) { return make_double2(a, b); }
-};
-
-template <class C> __device__ __forceinline__ C t_add(C a, C b) { return Cx<C>::mk(a.x + b.x, a.y + b.y); }
-template <class C> __device__ __forceinline__ C t_sub(C a, C b) { return Cx<C>::mk(a.x - b.x, a.y - b.y); }
-template <class C> __device__ __forceinline__ C t_mul(C a, C b) {
-  return Cx<C>::mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-template <class TO, class C> __device__ __forceinline__ TO t_cvt(C v);
-template <> __device__ __forceinline__ float2 t_cvt<float2, float2>(float2 v) { return v; }
-template <> __device__ __forceinline__ double2 t_cvt<double2, double2>(double2 v) { return v; }
-template <> __device__ __forceinline__ float2 t_cvt<float2, double2>(double2 v) {
-  return make_float2((float)v.x, (float)v.y);
-}
-template <> __device__ __forceinline__ double2 t_cvt<double2, float2>(float2 v) {
-  return make_double2(v.x, v.y);
-}
-
-template <class C>
-__device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3, bool inv) {
-  C t0 = t_add(a0, a2), t1 = t_sub(a0, a2), t2 = t_add(a1, a3), t3 = t_sub(a1, a3);
-  a0 = t_add(t0, t2);
-  a2 = t_sub(t0, t2);
-  C mt3 = inv ? Cx<C>::mk(-t3.y, t3.x) : Cx<C>::mk(t3.y, -t3.x);  // (+/-i) * t3
-  a1 = t_add(t1, mt3);
-  a3 = t_sub(t1, mt3);
-}
-
-template <class C>
-__device__ __forceinline__ C twid(const C* __restrict__ tw, int e, bool inv) {
-  C w = tw[e];
-  return inv ? Cx<C>::mk(w.x, -w.y) : w;
-}
-
-// One Stockham pass of radix R over M sequences of length n in SMEM (element i of sequence c at
-// s[i*es + c*ss]). `ileave` = sequences interleaved (ss == 1): consecutive threads -> sequences.
-template <class C, int R, int THREADS>
-__device__ __forceinline__ void stockham_pass(C* s, int n, int M, int es, int ss, bool ileave, int Ns, bool inv,
-                                              const C* __restrict__ tw) {
-  constexpr int MAXB = (R == 4) ? 4 : 8;
-  const int nbr = n / R;
-  const int nb = nbr * M;
-  C v[MAXB][R];
-  int dst[MAXB];
-#pragma unroll
-  for (int i = 0; i < MAXB; ++i) {
-    int q = threadIdx.x + i * THREADS;
-    dst[i] = -1;
-    if (q < nb) {
-      int c, j;
-      if (ileave) { c = q % M; j = q / M; } else { c = q / nbr; j = q % nbr; }
-      int k = j % Ns;
-      int tstep = kTw / (Ns * R);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        C a = s[(j + r * nbr) * es + c * ss];
-        if (r > 0 && k > 0) a = t_mul(a, twid(tw, r * k * tstep, inv));
-        v[i][r] = a;
-      }
-      if (R == 4) {
-        dft4(v[i][0], v[i][1], v[i][2], v[i][3], inv);
-      } else {
-        C a = v[i][0], b = v[i][1];
-        v[i][0] = t_add(a, b);
-        v[i][1] = t_sub(a, b);
-      }
-      dst[i] = ((j / Ns) * Ns * R + k) * es + c * ss;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < MAXB; ++i) {
-    if (dst[i] >= 0) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) s[dst[i] + r * Ns * es] = v[i][r];
-    }
-  }
-  __syncthreads();
-}
-
-template <class C, int THREADS>
-__device__ void smem_fft(C* s, int n, int M, int es, int ss, bool ileave, bool inv, const C* __restrict__ tw) {
-  int Ns = 1;
-  while (Ns * 4 <= n) {
-    stockham_pass<C, 4, THREADS>(s, n, M, es, ss, ileave, Ns, inv, tw);
-    Ns *= 4;
-  }
-  if (Ns < n) stockham_pass<C, 2, THREADS>(s, n, M, es, ss, ileave, Ns, inv, tw);
-}
 
 // ---------------------------------------------------------------- n <= 4096, M rows per CTA
 template <class TI, class TO, class C>

@@ -23,6 +23,25 @@ static const bool g_use_tc = [] {
   const char* e = std::getenv("JTFS_TC");
   return !(e && e[0] == '0');
 }();
+// Route of the joint stage per block: tensor cores (K small enough for a resident A tile), else the
+// FFT route along n1 (kernels_frfft.cu). JTFS_FFT_KMIN=k also sends TC-eligible blocks with K >= k to
+// the FFT route; JTFS_SIMT=1 uses the dense CUDA-core kernels instead of the FFT route (A/B tests).
+static const int g_fft_kmin = [] {
+  const char* e = std::getenv("JTFS_FFT_KMIN");
+  return e ? std::atoi(e) : 1 << 30;
+}();
+static const bool g_force_simt = [] {
+  const char* e = std::getenv("JTFS_SIMT");
+  return e && e[0] == '1';
+}();
+enum Route { kRouteTc = 0, kRouteFft = 1, kRouteSimt = 2 };
+static int route_of(const Plan& p, size_t bi, bool bwd) {
+  const bool tc_ok = g_use_tc && (bwd ? p.blk_tcb[bi] : p.blk_tc[bi]) && p.blocks[bi].n1_max < g_fft_kmin;
+  if (tc_ok) return kRouteTc;
+  const int ro = (int)((p.blocks[bi].n1_max + p.F - 1) / p.F);
+  if (!g_force_simt && p.P <= kFfMaxP && ro <= kFfMaxRo) return kRouteFft;
+  return kRouteSimt;
+}
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches += n; }
 
@@ -88,7 +107,8 @@ static void free_tables(DeviceTables* d) {
                   d->s0_job, d->s0_tiles, d->psi1_sup, d->psi2_sup, d->phiT_sup, d->hfr, d->phiF_k,
                   d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
                   d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_owner_unit, d->l1_off,
-                  d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw, d->twd};
+                  d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw, d->twd,
+                  d->fr_spec, d->u_wts, d->u_wt_off, d->ffw.blist, d->ffw.tiles, d->ffb.blist, d->ffb.tiles};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int c = 0; c < 6; ++c) {
@@ -151,7 +171,7 @@ static cudaError_t upload(Plan& p) {
     std::vector<int64_t> cnt;
     for (size_t u = 0; u < p.units.size(); ++u) {
       int ro = p.units[u].rows_out;
-      if (g_use_tc && p.blk_tc[p.units[u].bi]) continue;   // on the tensor-core path
+      if (route_of(p, p.units[u].bi, false) != kRouteSimt) continue;   // tensor-core or FFT route
       int cls = 0;
       while (kaps[cls] < ro) ++cls;
       if (cls != c) continue;
@@ -174,9 +194,8 @@ static cudaError_t upload(Plan& p) {
       std::vector<TcBlock> bl;
       std::vector<int64_t> cnt;
       int k2 = 0, kmax = 0, kcw = 32;
-      if (g_use_tc)
-        for (auto& tb : src)
-          if (tb.cls == c) {
+      for (auto& tb : src)
+          if (tb.cls == c && route_of(p, tb.bi, !fwd) == kRouteTc) {
             bl.push_back(tb);
             const int CT = (fwd && c < 3) ? 2 : 1;
             cnt.push_back((p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT));
@@ -211,7 +230,7 @@ static cudaError_t upload(Plan& p) {
     nm.push_back(p.blocks[bi].n1_max);
     d->Kmax = std::max(d->Kmax, p.blocks[bi].n1_max);
     // CUDA-core backward: 32-column tiles over all n1 rows; blocks on the tensor-core path: none
-    const bool simt = !(g_use_tc && p.blk_tcb[bi]);
+    const bool simt = route_of(p, bi, true) == kRouteSimt;
     bt.push_back(simt ? (p.binfo[bi].n_cols + 31) / 32 : 0);
     if (simt) d->Kmax_simt_bwd = std::max(d->Kmax_simt_bwd, p.blocks[bi].n1_max);
   }
@@ -246,6 +265,27 @@ static cudaError_t upload(Plan& p) {
   std::vector<double2> twd = fft_twiddle_table_d();
   UP(twd, twd);
   d->maxLf = (int)p.P;
+  // FFT route tables and block lists
+  UP(p.fr_spec, fr_spec); UP(p.u_wts, u_wts); UP(p.u_wt_off, u_wt_off);
+  for (int bw = 0; bw < 2; ++bw) {
+    std::vector<int32_t> bl;
+    std::vector<int64_t> cnt;
+    for (size_t bi = 0; bi < p.blocks.size(); ++bi)
+      if (route_of(p, bi, bw == 1) == kRouteFft) {
+        bl.push_back((int32_t)bi);
+        cnt.push_back(joint_fft_tiles(p.binfo[bi].n_cols));
+      }
+    FfList& L = bw ? d->ffb : d->ffw;
+    L.nb = (int)bl.size();
+    if (!bl.empty()) {
+      t = prefix(cnt);
+      if ((e = up(bl, &L.blist)) != cudaSuccess || (e = up(t, &L.tiles)) != cudaSuccess) {
+        free_tables(d);
+        return e;
+      }
+      L.ntiles = t.back();
+    }
+  }
 #undef UP
   p.dev = d;
   return cudaSuccess;
@@ -378,6 +418,7 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
     prof_end(st, 0);
     prof_begin(st, 1);
+    launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, shard, n_shards, mb, st);
     launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
     prof_end(st, 1);
     launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, shard, n_shards, mb, st);
@@ -400,6 +441,7 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
     prof_end(st, 2);
     prof_begin(st, 3);
+    launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
     launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
     prof_end(st, 3);
     // FFT of g_Y2 rows -> G_Y (into Y2)

@@ -107,6 +107,10 @@ struct Plan {
   std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
   std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class 0..2)
   std::vector<float> tc_img, tc_wts, tc_img2;
+  // FFT route of the joint stage (kernels_frfft.cu)
+  std::vector<float> fr_spec;                   // [n_fr_all][P] level-0 responses of L_fr on the P grid
+  std::vector<float> u_wts;                     // per unit [rows_out][n_rows] phi_F weights
+  std::vector<int64_t> u_wt_off;                // [n_units] offsets into u_wts
   std::vector<float> phiF_k;                    // concat over k of P>>k real kernels
   std::vector<int64_t> phiF_off;                // [log2F+1]
   std::vector<float> phiT_half;                 // concat over s of half kernels t_s[0..H_s]

@@ -479,6 +479,25 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     else { p->o1_rlo.push_back(pmod(a, Lf)); p->o1_nrows.push_back(c - a + 1); }
   }
   build_tc_tables(p);
+  // FFT route (kernels_frfft.cu): level-0 responses of every frequential filter on the P grid
+  // (R4 periodised Morlet / Gaussian, the same response whose inverse DFT is h_f) and per-unit phi_F
+  // weights g_kf[(rho 2^d - r) mod L_f] over the unit's needed rows
+  {
+    std::vector<double> resp;
+    for (int f = 0; f < nfr; ++f) {
+      level_response(p->L_fr[f], p->P, 0, &resp);
+      for (int64_t m = 0; m < p->P; ++m) p->fr_spec.push_back((float)resp[m]);
+    }
+    for (auto& U : p->units) {
+      p->u_wt_off.push_back((int64_t)p->u_wts.size());
+      const float* g = p->phiF_k.data() + p->phiF_off[U.kf];
+      for (int rho = 0; rho < U.rows_out; ++rho)
+        for (int64_t i = 0; i < U.n_rows; ++i) {
+          const int64_t r = (U.r_lo + i) % U.Lf;
+          p->u_wts.push_back(g[((((int64_t)rho << U.d) - r) % U.Lf + U.Lf) % U.Lf]);
+        }
+    }
+  }
   // adjoint d/dx spectrum gather: CSR of n1 touching each tile of N_pad bins
   int64_t ntile = ceil_div(p->N_pad, p->gx_tile);
   p->gx_tile_start.push_back(0);
