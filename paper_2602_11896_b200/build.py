@@ -13,6 +13,7 @@ SOURCES = ["planner.cpp", "fft.cu", "kernels_time.cu", "kernels_fr.cu", "jtfs_ap
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("JTFS_NVCC_EXTRA", "").split()   # e.g. -DJTFS_TC_TRACE for instrumented builds
 
 
 def _stale(obj: str, deps: list[str]) -> bool:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 #include "plan.h"
@@ -14,7 +15,8 @@ struct TcClass {
   int64_t* tiles = nullptr;
   int n_blocks = 0;
   int64_t ntiles = 0;
-  int K2max = 0, Kmax = 0, kcw = 32;
+  int K2max = 0, Kmax = 0, kcw = 32, kb2 = 8;
+  int cls = 0;                     // kernel variant (TcBlock::cls)
 };
 
 struct FfList {                    // blocks on the FFT route of the joint stage + column-tile prefix
@@ -61,9 +63,9 @@ struct DeviceTables {
   float* tc_img = nullptr;
   float* tc_wts = nullptr;
   TcUnit* tc_units = nullptr;
-  TcClass tc[kTcClasses];
+  std::vector<TcClass> tc;         // one launch per tensor-core block (forward)
   float* tc_img2 = nullptr;
-  TcClass tcb[kTcBwClasses];
+  std::vector<TcClass> tcb;        // one launch per tensor-core block (backward)
   // FFT route (kernels_frfft.cu)
   float* fr_spec = nullptr;
   float* u_wts = nullptr;

@@ -115,15 +115,15 @@ static void free_tables(DeviceTables* d) {
     if (d->fwd_ulist[c]) cudaFree(d->fwd_ulist[c]);
     if (d->fwd_tiles[c]) cudaFree(d->fwd_tiles[c]);
   }
-  for (int c = 0; c < kTcClasses; ++c) {
-    if (d->tc[c].blocks) cudaFree(d->tc[c].blocks);
-    if (d->tc[c].tiles) cudaFree(d->tc[c].tiles);
+  for (auto& c : d->tc) {
+    if (c.blocks) cudaFree(c.blocks);
+    if (c.tiles) cudaFree(c.tiles);
   }
   if (d->tc_img) cudaFree(d->tc_img);
   if (d->tc_img2) cudaFree(d->tc_img2);
-  for (int c = 0; c < kTcBwClasses; ++c) {
-    if (d->tcb[c].blocks) cudaFree(d->tcb[c].blocks);
-    if (d->tcb[c].tiles) cudaFree(d->tcb[c].tiles);
+  for (auto& c : d->tcb) {
+    if (c.blocks) cudaFree(c.blocks);
+    if (c.tiles) cudaFree(c.tiles);
   }
   if (d->tc_wts) cudaFree(d->tc_wts);
   if (d->tc_units) cudaFree(d->tc_units);
@@ -189,37 +189,30 @@ static cudaError_t upload(Plan& p) {
   }
   // tensor-core classes (forward and backward)
   UP(p.tc_img, tc_img); UP(p.tc_wts, tc_wts); UP(p.tc_units, tc_units); UP(p.tc_img2, tc_img2);
-  auto build_classes = [&](const std::vector<TcBlock>& src, TcClass* cls, int ncls, bool fwd) -> cudaError_t {
-    for (int c = 0; c < ncls; ++c) {
-      std::vector<TcBlock> bl;
-      std::vector<int64_t> cnt;
-      int k2 = 0, kmax = 0, kcw = 32;
-      for (auto& tb : src)
-          if (tb.cls == c && route_of(p, tb.bi, !fwd) == kRouteTc) {
-            bl.push_back(tb);
-            const int CT = (fwd && c < 3) ? 2 : 1;
-            cnt.push_back((p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT));
-            k2 = std::max(k2, tb.K2);
-            kmax = std::max(kmax, tb.K);
-            kcw = tb.kcw;
-          }
-      cls[c].n_blocks = (int)bl.size();
-      cls[c].K2max = k2;
-      cls[c].Kmax = kmax;
-      cls[c].kcw = kcw;
-      if (!bl.empty()) {
-        std::vector<int64_t> tt = prefix(cnt);
-        cudaError_t e1 = up(bl, &cls[c].blocks);
-        if (e1 != cudaSuccess) return e1;
-        e1 = up(tt, &cls[c].tiles);
-        if (e1 != cudaSuccess) return e1;
-        cls[c].ntiles = tt.back();
-      }
+  // one launch per tensor-core block: each sizes its pipeline for its own K
+  auto build_classes = [&](const std::vector<TcBlock>& src, std::vector<TcClass>* out, bool fwd) -> cudaError_t {
+    for (auto& tb : src) {
+      if (route_of(p, tb.bi, !fwd) != kRouteTc) continue;
+      TcClass c;
+      const int CT = (fwd && tb.cls < 3) ? 2 : 1;
+      std::vector<TcBlock> bl{tb};
+      std::vector<int64_t> tt{0, (p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT)};
+      c.n_blocks = 1;
+      c.K2max = tb.K2;
+      c.Kmax = tb.K;
+      c.kcw = tb.kcw;
+      c.kb2 = tb.kb2;
+      c.cls = tb.cls;
+      c.ntiles = tt.back();
+      cudaError_t e1 = up(bl, &c.blocks);
+      if (e1 == cudaSuccess) e1 = up(tt, &c.tiles);
+      out->push_back(c);
+      if (e1 != cudaSuccess) return e1;
     }
     return cudaSuccess;
   };
-  if ((e = build_classes(p.tc_blocks, d->tc, kTcClasses, true)) != cudaSuccess) { free_tables(d); return e; }
-  if ((e = build_classes(p.tcb_blocks, d->tcb, kTcBwClasses, false)) != cudaSuccess) { free_tables(d); return e; }
+  if ((e = build_classes(p.tc_blocks, &d->tc, true)) != cudaSuccess) { free_tables(d); return e; }
+  if ((e = build_classes(p.tcb_blocks, &d->tcb, false)) != cudaSuccess) { free_tables(d); return e; }
   std::vector<int32_t> kf;
   for (auto& f : p.L_fr) kf.push_back(std::min(f.j, p.log2F));
   UP(kf, kf_of);

@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "tc.cuh"
@@ -35,9 +37,9 @@ constexpr int kTcRows = 64;         // lambda_1 rows per forward row tile (N = 1
 constexpr int kTcN = 2 * kTcRows;   // forward MMA N
 constexpr int kTcThreads = 384;     // 12 warps
 constexpr int kTcMaxStages = 8;
+constexpr int kTcMaxStages2 = 16;   // backward ring 2 (B2 chunks)
 constexpr int kBwRows = 32;         // rows per backward tile (GEMM1 N = 64, GEMM2 K = 64)
 constexpr int kBwN1 = 2 * kBwRows;
-constexpr int kB2c = 16;            // B2 chunk width (kk) per stage
 
 __device__ __forceinline__ int find_tc(const int64_t* __restrict__ tiles, int n, int64_t t) {
   int lo = 0, hi = n - 1;
@@ -265,11 +267,18 @@ static size_t tc_fwd_smem(int CT, int KAP, int NS, int K2, int STG) {
   return (size_t)(2 * CT * 128 * K2 + NS * STG + CT * KAP * 128) * 4 + 1024;
 }
 
+// forward B ring stages that fit (the planner rejects chunk widths that leave fewer than 3)
+int tc_fwd_stages(int CT, int KAP, int K2, int kcw) {
+  const int STG = 2 * kTcN * kcw;
+  int NS = kTcMaxStages;
+  while (NS > 0 && tc_fwd_smem(CT, KAP, NS, K2, STG) > 224 * 1024) --NS;
+  return NS;
+}
+
 template <int CT, int KAP>
 static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st) {
   const int STG = 2 * kTcN * C.kcw;
-  int NS = kTcMaxStages;
-  while (NS > 2 && tc_fwd_smem(CT, KAP, NS, C.K2max, STG) > 224 * 1024) --NS;
+  const int NS = tc_fwd_stages(CT, KAP, C.K2max, C.kcw);
   const size_t sm = tc_fwd_smem(CT, KAP, NS, C.K2max, STG);
   cudaFuncSetAttribute(k_joint_fwd_tc<CT, KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)C.ntiles, (unsigned)B);
@@ -279,13 +288,12 @@ static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st)
 
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
                          int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st) {
-  for (int cls = 0; cls < kTcClasses; ++cls) {
-    const TcClass& C = d.tc[cls];
+  for (const TcClass& C : d.tc) {
     if (C.n_blocks == 0) continue;
     TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
              (int)p.L_fr.size(), shard, n_shards};
     // class = 3 * ct_kind + kap_kind; ct_kind 0: CT=2 (K2<=64), 1: CT=1 kcw 32, 2: CT=1 kcw 16
-    switch (cls) {
+    switch (C.cls) {
       case 0: launch_tc<2, 2>(a, C, B, st); break;
       case 1: launch_tc<2, 4>(a, C, B, st); break;
       case 2: launch_tc<2, 8>(a, C, B, st); break;
@@ -311,12 +319,23 @@ struct TcBwArgs {
   const TcUnit* tcu;
   int nfr, shard, n_shards;
   const float* thr;
+  int expt;                         // timing experiments only (JTFS_TC_EXPT); 0 in production
+  long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
 };
+#ifdef JTFS_TC_TRACE
+#define TC_TRACE(ev, g)                                                                  \
+  do {                                                                                   \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (g) < 512) a.trace[(ev) * 512 + (g)] = clock64(); \
+  } while (0)
+#else
+#define TC_TRACE(ev, g) do {} while (0)
+#endif
 
 template <int KAP>
-__global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS, int STG) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS1, int STG1, int NS2, int STG2) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull[2], tempty[2], a2full, a2empty, d2full;
+  __shared__ uint64_t full1[kTcMaxStages], empty1[kTcMaxStages], full2[kTcMaxStages2], empty2[kTcMaxStages2];
+  __shared__ uint64_t tfull[2], tempty[2], a2full[2], a2empty[2], d2full;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int jb = find_tc(a.tiles, a.n_tc_blocks, blockIdx.x);
@@ -324,17 +343,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   const BlockInfo bf = a.binfo[TB.bi];
   const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)128;
   const int b = blockIdx.y;
-  const int K = TB.K, K2 = TB.K2, kcw = TB.kcw;
+  const int K = TB.K, K2 = TB.K2, kcw = TB.kcw, kB2c = TB.kb2;
   const int N2 = ((2 * K + 15) / 16) * 16;
+  const int nab = N2 <= 128 ? 2 : 1;                   // A2 buffers in TMEM (double when D2 leaves room)
   float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2]
   float* a_lo = a_hi + 128 * K2;
-  float* bst = a_lo + 128 * K2;                         // NS x STG floats
+  float* bst1 = a_lo + 128 * K2;                        // ring 1 (GEMM1 B images): NS1 x STG1 floats
+  float* bst2 = bst1 + NS1 * STG1;                      // ring 2 (GEMM2 B2 images): NS2 x STG2 floats
 
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NS1; ++s) { tc::mbar_init(&full1[s], 1); tc::mbar_init(&empty1[s], 1); }
+    for (int s = 0; s < NS2; ++s) { tc::mbar_init(&full2[s], 1); tc::mbar_init(&empty2[s], 1); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
-    tc::mbar_init(&a2full, 8);
-    tc::mbar_init(&a2empty, 1);
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&a2full[s], 8); tc::mbar_init(&a2empty[s], 1); }
     tc::mbar_init(&d2full, 1);
     tc::fence_mbar_init();
   }
@@ -344,64 +365,63 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  // TMEM columns: D1 buffers [0,64) [64,128); A2 hi [128,192), lo [192,256); D2 [256, 256+N2)
+  // TMEM columns: D1 buffers [0,64) [64,128); A2 buffer j: hi [128+128j, +64), lo [192+128j, +64);
+  // D2 [128+128 nab, +N2)
   const uint32_t tbase = tmem_base;
-  const uint32_t ta2_hi = tbase + 128, ta2_lo = tbase + 192;
-  const uint32_t d2 = tbase + 256;
+  const uint32_t ta2 = tbase + 128;
+  const uint32_t d2 = tbase + 128 + 128 * (uint32_t)nab;
   const int nchunks = (K2 + kcw - 1) / kcw;
 
-  if (warp == 0) {
-    // ===================== producer: B1(g+1) before B2(g), matching the MMA issue order
+  if (warp == 0 || warp == 2) {
+    // ===================== producers: warp 0 streams the GEMM1 B images (ring 1), warp 2 the GEMM2
+    // B2 images (ring 2); separate rings let B2 run ahead while GEMM2 waits for the epilogue
+    const bool p1 = warp == 0;
     int stage = 0;
     uint32_t ph = 0;
-    auto push_b1 = [&](const TcUnit& tu, int t32) {
-      // half (rows 32*(t32&1) ..) of the forward 64-row image, every chunk: [hi half | lo half]
-      const float* src = a.img + tu.img_off + (int64_t)(t32 >> 1) * (2 * kTcN * K2);
-      const int half = t32 & 1;
-      for (int ch = 0; ch < nchunks; ++ch) {
-        const int kc = min(kcw, K2 - ch * kcw);
-        const uint32_t hb = (uint32_t)(kBwN1 * kc * 4);
-        tc::mbar_wait(&empty[stage], ph ^ 1);
-        if (tc::elect_one()) {
-          tc::mbar_expect_tx(&full[stage], 2 * hb);
-          float* dst = bst + stage * STG;
-          tc::bulk_g2s(dst, src + half * kBwN1 * kc, hb, &full[stage]);
-          tc::bulk_g2s(dst + kBwN1 * kc, src + kTcN * kc + half * kBwN1 * kc, hb, &full[stage]);
-        }
-        __syncwarp();
-        src += 2 * kTcN * kc;
-        if (++stage == NS) { stage = 0; ph ^= 1; }
-      }
-    };
-    auto push_b2 = [&](const TcUnit& tu, int t32) {
-      const float* src = a.img2 + tu.img2_off + (int64_t)t32 * (2 * N2 * 64);
-      for (int ch = 0; ch < 64 / kB2c; ++ch) {
-        const uint32_t bytes = (uint32_t)(2 * N2 * kB2c * 4);
-        tc::mbar_wait(&empty[stage], ph ^ 1);
-        if (tc::elect_one()) {
-          tc::mbar_expect_tx(&full[stage], bytes);
-          tc::bulk_g2s(bst + stage * STG, src, bytes, &full[stage]);
-        }
-        __syncwarp();
-        src += 2 * N2 * kB2c;
-        if (++stage == NS) { stage = 0; ph ^= 1; }
-      }
-    };
-    bool have_prev = false;
-    TcUnit pu{};
-    int pt = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
       if (u % a.n_shards != a.shard) continue;
       const TcUnit tu = a.tcu[u];
       const int NT32 = (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
-      for (int t = 0; t < NT32; ++t) {
-        push_b1(tu, t);                    // B1(g) ...
-        if (have_prev) push_b2(pu, pt);    // ... then B2(g-1)
-        have_prev = true; pu = tu; pt = t;
+      for (int t32 = 0; t32 < NT32; ++t32) {
+        if (p1) {
+          // half (rows 32*(t32&1) ..) of the forward 64-row image, every chunk: [hi half | lo half]
+          const float* src = a.img + tu.img_off + (int64_t)(t32 >> 1) * (2 * kTcN * K2);
+          const int half = t32 & 1;
+          for (int ch = 0; ch < nchunks; ++ch) {
+            const int kc = min(kcw, K2 - ch * kcw);
+            const uint32_t hb = (uint32_t)(kBwN1 * kc * 4);
+            tc::mbar_wait(&empty1[stage], ph ^ 1);
+            if ((a.expt & 2) && t32 > 0) {
+              if (tc::elect_one()) tc::mbar_arrive(&full1[stage]);
+            } else if (tc::elect_one()) {
+              tc::mbar_expect_tx(&full1[stage], 2 * hb);
+              float* dst = bst1 + stage * STG1;
+              tc::bulk_g2s(dst, src + half * kBwN1 * kc, hb, &full1[stage]);
+              tc::bulk_g2s(dst + kBwN1 * kc, src + kTcN * kc + half * kBwN1 * kc, hb, &full1[stage]);
+            }
+            __syncwarp();
+            src += 2 * kTcN * kc;
+            if (++stage == NS1) { stage = 0; ph ^= 1; }
+          }
+        } else {
+          const float* src = a.img2 + tu.img2_off + (int64_t)t32 * (2 * N2 * 64);
+          for (int ch = 0; ch < 64 / kB2c; ++ch) {
+            const uint32_t bytes = (uint32_t)(2 * N2 * kB2c * 4);
+            tc::mbar_wait(&empty2[stage], ph ^ 1);
+            if ((a.expt & 2) && t32 > 0) {
+              if (tc::elect_one()) tc::mbar_arrive(&full2[stage]);
+            } else if (tc::elect_one()) {
+              tc::mbar_expect_tx(&full2[stage], bytes);
+              tc::bulk_g2s(bst2 + stage * STG2, src, bytes, &full2[stage]);
+            }
+            __syncwarp();
+            src += 2 * N2 * kB2c;
+            if (++stage == NS2) { stage = 0; ph ^= 1; }
+          }
+        }
       }
     }
-    if (have_prev) push_b2(pu, pt);
   } else if (warp == 1) {
     // ===================== MMA issuer
     const uint32_t idesc1 = tc::idesc_tf32(128, kBwN1);
@@ -409,18 +429,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const uint32_t sboA = (uint32_t)K2 * 32u;
     const uint64_t dA_hi = tc::sdesc(tc::smem_u32(a_hi), 128, sboA);
     const uint64_t dA_lo = tc::sdesc(tc::smem_u32(a_lo), 128, sboA);
-    const uint32_t bst_s = tc::smem_u32(bst);
-    int stage = 0, buf = 0;
-    uint32_t ph = 0, bph = 0;
+    const uint32_t bst1_s = tc::smem_u32(bst1), bst2_s = tc::smem_u32(bst2);
+    int stage1 = 0, stage2 = 0, buf = 0;
+    uint32_t ph1 = 0, ph2 = 0, bph = 0;
     int g2 = 0;   // GEMM2 count
+    int g1 = 0;   // GEMM1 count
     auto gemm1 = [&]() {
+      if (lane == 0) TC_TRACE(0, g1);
       tc::mbar_wait(&tempty[buf], bph ^ 1);
+      if (lane == 0) TC_TRACE(13, g1);
       const uint32_t d = tbase + (uint32_t)(buf * kBwN1);
       for (int ch = 0; ch < nchunks; ++ch) {
         const int kc = min(kcw, K2 - ch * kcw);
-        tc::mbar_wait(&full[stage], ph);
+        tc::mbar_wait(&full1[stage1], ph1);
         tc::tc_fence_after();
-        const uint32_t off = bst_s + (uint32_t)(stage * STG * 4);
+        if (lane == 0 && ch == 0) TC_TRACE(14, g1);
+        const uint32_t off = bst1_s + (uint32_t)(stage1 * STG1 * 4);
         const uint64_t dbh = tc::sdesc(off, 128, (uint32_t)kc * 32u);
         const uint64_t dbl = tc::sdesc(off + (uint32_t)(kBwN1 * kc * 4), 128, (uint32_t)kc * 32u);
         if (tc::elect_one()) {
@@ -430,36 +454,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
             tc::mma_tf32(d, dA_hi + 16u * kg, dbl + 16u * ks, idesc1, 1u);
             tc::mma_tf32(d, dA_lo + 16u * kg, dbh + 16u * ks, idesc1, 1u);
           }
-          tc::mma_commit(&empty[stage]);
+          tc::mma_commit(&empty1[stage1]);
           if (ch == nchunks - 1) tc::mma_commit(&tfull[buf]);
         }
         __syncwarp();
-        if (++stage == NS) { stage = 0; ph ^= 1; }
+        if (++stage1 == NS1) { stage1 = 0; ph1 ^= 1; }
       }
       if (++buf == 2) { buf = 0; bph ^= 1; }
+      if (lane == 0) TC_TRACE(1, g1);
+      ++g1;
     };
     auto gemm2 = [&]() {
-      tc::mbar_wait(&a2full, (uint32_t)(g2 & 1));
+      if (lane == 0) TC_TRACE(2, g2);
+      const int ab = nab == 2 ? (g2 & 1) : 0;
+      const uint32_t aph = (uint32_t)((nab == 2 ? (g2 >> 1) : g2) & 1);
+      const uint32_t ta2_hi = ta2 + 128u * ab, ta2_lo = ta2_hi + 64u;
+      tc::mbar_wait(&a2full[ab], aph);
       tc::tc_fence_after();
+      if (lane == 0) TC_TRACE(3, g2);
       for (int ch = 0; ch < 64 / kB2c; ++ch) {
-        tc::mbar_wait(&full[stage], ph);
+        tc::mbar_wait(&full2[stage2], ph2);
         tc::tc_fence_after();
-        const uint32_t bh = bst_s + (uint32_t)(stage * STG * 4);
+        if (lane == 0 && ch == 0) TC_TRACE(9, g2);
+        if (lane == 0 && ch == 64 / kB2c - 1) TC_TRACE(11, g2);
+        const uint32_t bh = bst2_s + (uint32_t)(stage2 * STG2 * 4);
         const uint64_t dbh = tc::sdesc(bh, 128, (uint32_t)kB2c * 32u);
         const uint64_t dbl = tc::sdesc(bh + (uint32_t)(N2 * kB2c * 4), 128, (uint32_t)kB2c * 32u);
         if (tc::elect_one()) {
-          for (int ks = 0; ks < kB2c / 8; ++ks) {
+          for (int ks = 0; ks < ((a.expt & 4) ? 0 : kB2c / 8); ++ks) {
             const uint32_t kg = (uint32_t)(ch * (kB2c / 8) + ks);
             tc::mma_tf32_ts(d2, ta2_hi + 8u * kg, dbh + 16u * ks, idesc2, (g2 > 0 || kg > 0) ? 1u : 0u);
             tc::mma_tf32_ts(d2, ta2_hi + 8u * kg, dbl + 16u * ks, idesc2, 1u);
             tc::mma_tf32_ts(d2, ta2_lo + 8u * kg, dbh + 16u * ks, idesc2, 1u);
           }
-          tc::mma_commit(&empty[stage]);
-          if (ch == 64 / kB2c - 1) tc::mma_commit(&a2empty);
+          tc::mma_commit(&empty2[stage2]);
+          if (ch == 64 / kB2c - 1) tc::mma_commit(&a2empty[ab]);
         }
         __syncwarp();
-        if (++stage == NS) { stage = 0; ph ^= 1; }
+        if (lane == 0 && ch == 0) TC_TRACE(10, g2);
+        if (lane == 0 && ch == 64 / kB2c - 1) TC_TRACE(12, g2);
+        if (++stage2 == NS2) { stage2 = 0; ph2 ^= 1; }
       }
+      if (lane == 0) TC_TRACE(4, g2);
       ++g2;
     };
     int G = 0;
@@ -481,7 +517,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const int q = e & 3, h = e >> 2;        // lane quadrant, row half (16 rows)
     const int c = q * 32 + lane;
     const int64_t colg = col0 + c;
-    const float th2 = a.thr[b] * a.thr[b];
+    const float th2 = fmaxf(a.thr[b] * a.thr[b], 1.17549435e-38f);   // R22 dead zone (and |w|^2 > FLT_MIN)
     const uint32_t lq = (uint32_t)(q * 32) << 16;
     int buf = 0;
     uint32_t bph = 0;
@@ -507,6 +543,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           wl[r] = (r < ro && lane < 16) ? __ldg(wt + r * ldw + t * kBwRows + h * 16 + lane) : 0.f;
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
+        if (warp == 4 && lane == 0) TC_TRACE(5, g);
         float v[32];
         const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 32);
         tc::tmem_ld16_nowait(ta, v);
@@ -517,6 +554,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         if (++buf == 2) { buf = 0; bph ^= 1; }
         float ghi[32], glo[32];
+        if (a.expt & 1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ghi[i] = glo[i] = v[i] * 0.f;
+        } else
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float gv = 0.f;
@@ -524,13 +565,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           for (int r = 0; r < KAP; ++r) gv = fmaf(__shfl_sync(0xffffffffu, wl[r], i), gor[r], gv);
           const float re = v[2 * i], im = v[2 * i + 1];
           const float m2 = fmaf(re, re, im * im);
-          const float s = (m2 > 1.17549435e-38f && m2 > th2) ? gv * rsqrtf(m2) : 0.f;
-          tc::split_tf32(re * s, ghi[2 * i], glo[2 * i]);
-          tc::split_tf32(im * s, ghi[2 * i + 1], glo[2 * i + 1]);
+          const float s = m2 > th2 ? gv * tc::rsqrt_approx(m2) : 0.f;
+          tc::split_tf32_fast(re * s, ghi[2 * i], glo[2 * i]);
+          tc::split_tf32_fast(im * s, ghi[2 * i + 1], glo[2 * i + 1]);
         }
-        // A2 (TMEM) is free once GEMM2(g-1) completed
-        tc::mbar_wait(&a2empty, (uint32_t)((g & 1) ^ 1));
+        // A2 buffer ab (TMEM) is free once the GEMM2 that last read it completed
+        if (warp == 4 && lane == 0) TC_TRACE(6, g);
+        const int ab = nab == 2 ? (g & 1) : 0;
+        const uint32_t ta2_hi = ta2 + 128u * ab, ta2_lo = ta2_hi + 64u;
+        tc::mbar_wait(&a2empty[ab], (uint32_t)(((nab == 2 ? (g >> 1) : g) & 1) ^ 1));
         tc::tc_fence_after();
+        if (warp == 4 && lane == 0) TC_TRACE(7, g);
         tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 32), ghi);
         tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 32 + 16), ghi + 16);
         tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 32), glo);
@@ -538,7 +583,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&a2full);
+        if (lane == 0) tc::mbar_arrive(&a2full[ab]);
+        if (warp == 4 && lane == 0) TC_TRACE(8, g);
       }
     }
     // final: D2 (g_Y2^T for this column tile) -> g_Y2[n][col]
@@ -571,33 +617,60 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
+// backward B rings (floats per stage, stage counts); the planner picks kb2 with the same rule
+void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2, int* STG2) {
+  const int N2 = ((2 * K + 15) / 16) * 16;
+  *STG1 = 2 * kBwN1 * kcw;
+  *STG2 = 2 * N2 * kb2;
+  const long avail = 224L * 1024 - 1024 - (long)2 * 128 * K2 * 4;
+  // ring 2 holds up to two tiles of B2 chunks (GEMM2 runs a tile behind GEMM1), ring 1 the rest
+  int n2 = std::min(kTcMaxStages2, std::max(2, 128 / kb2));
+  while (n2 > 2 && avail - (long)n2 * *STG2 * 4 < 2L * *STG1 * 4) --n2;
+  *NS2 = n2;
+  *NS1 = (int)std::min<long>(kTcMaxStages, (avail - (long)n2 * *STG2 * 4) / (*STG1 * 4));
+}
+
+static const int g_tc_expt = [] {
+  const char* e = std::getenv("JTFS_TC_EXPT");
+  return e ? std::atoi(e) : 0;
+}();
+
 template <int KAP>
 static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream_t st) {
-  const int N2max = ((2 * C.Kmax + 15) / 16) * 16;
-  const int STG = std::max(2 * kBwN1 * C.kcw, 2 * N2max * kB2c);
-  int NS = kTcMaxStages;
-  auto smem = [&](int ns) { return (size_t)(2 * 128 * C.K2max + ns * STG) * 4 + 1024; };
-  while (NS > 2 && smem(NS) > 224 * 1024) --NS;
-  const size_t sm = smem(NS);
+  int NS1, NS2, STG1, STG2;
+  tc_bwd_rings(C.Kmax, C.K2max, C.kcw, C.kb2, &NS1, &STG1, &NS2, &STG2);
+  const size_t sm = (size_t)(2 * 128 * C.K2max + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)C.ntiles, (unsigned)B);
-  k_joint_bwd_tc<KAP><<<g, kTcThreads, sm, st>>>(a, NS, STG);
+  k_joint_bwd_tc<KAP><<<g, kTcThreads, sm, st>>>(a, NS1, STG1, NS2, STG2);
   count_launch();
 }
 
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
                          int B, cudaStream_t st) {
-  for (int cls = 0; cls < kTcBwClasses; ++cls) {
-    const TcClass& C = d.tcb[cls];
+  for (const TcClass& C : d.tcb) {
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
-               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr};
-    switch (cls % 3) {  // class = 3 * kcw_kind + kap_kind
+               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, nullptr};
+#ifdef JTFS_TC_TRACE
+    static long long* trace = nullptr;
+    if (!trace) cudaMalloc(&trace, 16 * 512 * 8);
+    if (C.Kmax == 18) { cudaMemsetAsync(trace, 0, 16 * 512 * 8, st); a.trace = trace; }
+#endif
+    switch (C.cls % 3) {  // class = 3 * kcw_kind + kap_kind
       case 0: launch_tc_bwd<2>(a, C, B, st); break;
       case 1: launch_tc_bwd<4>(a, C, B, st); break;
       case 2: launch_tc_bwd<8>(a, C, B, st); break;
     }
+#ifdef JTFS_TC_TRACE
+    if (a.trace) {
+      static long long h[16 * 512];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
+      if (FILE* fo = fopen("gpurun_out/tc_trace.bin", "wb")) { fwrite(h, 1, sizeof(h), fo); fclose(fo); }
+    }
+#endif
   }
 }
 

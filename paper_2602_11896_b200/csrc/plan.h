@@ -63,12 +63,13 @@ struct TcUnit {
 };
 struct TcBlock {
   int32_t bi, K, K2, cls;    // block, n1_max, padded 2K, launch class
-  int32_t kcw, pad;          // width (k' elements) of the B-image chunks: 32, or 16 when K2 > 120
+  int32_t kcw, kb2;          // B-image chunk widths: forward/GEMM1 (k' elements), backward B2 (kk elements)
 };
 // forward classes 3*ct_kind + kap_kind (ct_kind: 0 = 2 column tiles, 1 = 1 tile kcw 32,
 // 2 = 1 tile kcw 16; kap_kind: rows_out <= 2, 4, 8); backward classes 3*(kcw == 16) + kap_kind
-constexpr int kTcClasses = 9;
-constexpr int kTcBwClasses = 6;
+// backward B ring sizing shared by the planner (chooses kb2) and the launcher (kernels_tc.cu)
+void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2, int* STG2);
+int tc_fwd_stages(int CT, int KAP, int K2, int kcw);
 
 struct DeviceTables;  // device pointers (jtfs_api.cu)
 

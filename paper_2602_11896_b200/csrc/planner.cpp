@@ -169,17 +169,30 @@ static void build_tc_tables(Plan* p) {
     for (int f = 0; f < nfr; ++f) ro_max = std::max(ro_max, p->units[bi * nfr + f].rows_out);
     if (K2 > 168 || ro_max > 8) continue;   // resident A tile (128 x K2 x 8 B) must fit in SMEM
     const int CT = K2 <= 64 ? 2 : 1;
-    const int kcw = K2 <= 120 ? 32 : 16;
     const int kap = ro_max <= 2 ? 0 : (ro_max <= 4 ? 1 : 2);
+    // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
+    int kcw = 16;
+    for (int w : {K2, 64, 32}) {
+      if (w > 64 || w > K2) continue;
+      if (tc_fwd_stages(CT, 2 << kap, K2, w) >= 3) { kcw = w; break; }
+    }
     const int ctk = CT == 2 ? 0 : (kcw == 32 ? 1 : 2);
     p->blk_tc[bi] = 1;
-    p->tc_blocks.push_back({(int32_t)bi, K, K2, 3 * ctk + kap, kcw, 0});
     const int N2 = ((2 * K + 15) / 16) * 16;
-    const int64_t stg = std::max(2 * 64 * kcw, 2 * N2 * 16);
-    const bool bwd = N2 <= 256 && (int64_t)(2 * 128 * K2 + 2 * stg) * 4 + 1024 <= 224 * 1024;
+    // widest B2 chunk whose rings fit (fewer chunk hand-offs per tile): ring 2 >= 2 stages, ring 1 >= 2
+    int kb2 = 8;
+    for (int w : {64, 32, 16, 8}) {
+      int ns1, s1, ns2, s2;
+      tc_bwd_rings(K, K2, kcw, w, &ns1, &s1, &ns2, &s2);
+      if (ns1 >= 2 && ns2 * w >= 64 + w) { kb2 = w; break; }
+    }
+    p->tc_blocks.push_back({(int32_t)bi, K, K2, 3 * ctk + kap, kcw, kb2});
+    int ns1, s1, ns2, s2;
+    tc_bwd_rings(K, K2, kcw, kb2, &ns1, &s1, &ns2, &s2);
+    const bool bwd = N2 <= 256 && ns1 >= 2 && ns2 >= 2;
     if (bwd) {
       p->blk_tcb[bi] = 1;
-      p->tcb_blocks.push_back({(int32_t)bi, K, K2, 3 * (kcw == 16 ? 1 : 0) + kap, kcw, 0});
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcw, kb2});
     }
     for (int f = 0; f < nfr; ++f) {
       const int u = (int)bi * nfr + f;
@@ -223,27 +236,28 @@ static void build_tc_tables(Plan* p) {
           }
         }
       }
-      // backward B2 images: per 32-row tile, per 16-wide kk chunk: [hi N2 x 16 | lo N2 x 16]
+      // backward B2 images: per 32-row tile, per kb2-wide kk chunk: [hi N2 x kb2 | lo N2 x kb2]
       // B2[2n][2i] = Re M, B2[2n][2i+1] = Im M, B2[2n+1][2i] = -Im M, B2[2n+1][2i+1] = Re M
       if (bwd) {
         tu.img2_off = (int64_t)p->tc_img2.size();
         const int NT32 = (int)((U.n_rows + 31) / 32);
         for (int t = 0; t < NT32; ++t) {
-          for (int ch = 0; ch < 4; ++ch) {
+          for (int ch = 0; ch < 64 / kb2; ++ch) {
             const size_t base = p->tc_img2.size();
-            p->tc_img2.resize(base + 2 * (size_t)N2 * 16, 0.f);
+            p->tc_img2.resize(base + 2 * (size_t)N2 * kb2, 0.f);
             for (int nn = 0; nn < N2; ++nn) {
               const int n = nn / 2, po = nn % 2;
               if (n >= K) continue;
-              for (int kl = 0; kl < 16; ++kl) {
-                const int kk = ch * 16 + kl, i = kk / 2, pi = kk % 2;
+              for (int kl = 0; kl < kb2; ++kl) {
+                const int kk = ch * kb2 + kl, i = kk / 2, pi = kk % 2;
                 const int64_t lr = (int64_t)t * 32 + i;
                 if (lr >= U.n_rows) continue;
                 double mr, mi;
                 Mval(lr, n, &mr, &mi);
                 // Re g_Y = Re M Re g_W + Im M Im g_W ; Im g_Y = -Im M Re g_W + Re M Im g_W
                 const double v = (po == 0) ? ((pi == 0) ? mr : mi) : ((pi == 0) ? -mi : mr);
-                put(p->tc_img2, base, base + (size_t)N2 * 16, core_off_host((uint32_t)nn, (uint32_t)kl, 16u) / 4, v);
+                put(p->tc_img2, base, base + (size_t)N2 * kb2,
+                    core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kb2) / 4, v);
               }
             }
           }

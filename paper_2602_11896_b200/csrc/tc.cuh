@@ -171,6 +171,13 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
+// MUFU reciprocal square root, flush-to-zero (callers guarantee x > FLT_MIN)
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // tf32 split for 3xTF32: x = hi + lo (+ O(2^-22 x)), hi/lo rounded to tf32 (cvt.rna)
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -180,6 +187,12 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
   lo = tf32_rna(x - hi);
+}
+// cheaper split for epilogue operands: lo = x - hi exactly, left for the tensor core to truncate to
+// tf32 (relative error of the pair <= 2^-21 instead of 2^-22; one CVT instead of two)
+__device__ __forceinline__ void split_tf32_fast(float x, float& hi, float& lo) {
+  hi = tf32_rna(x);
+  lo = x - hi;
 }
 
 }  // namespace tc
