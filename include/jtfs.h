@@ -160,15 +160,17 @@ int64_t jtfs_launch_count(void);
 /* Algorithmic cost per signal of the joint lambda_1 stage (roofline reporting),
  * over the pruned rows x columns ("cells", one modulus value each):
  *  out[0] forward dense-contraction flops on the tensor-core blocks (8 K per cell)
- *  out[1] forward flops on the CUDA-core blocks (8 K + 3 + 2 rows_out per cell)
+ *  out[1] forward FP32 flops on the FFT-route blocks (per column: 5 P log2 P for FFT_P of y; per filter
+ *         4 P fold + 5 L_f log2 L_f inverse FFT + 4 n_rows modulus + 2 rows_out n_rows phi_F)
  *  out[2] backward contraction flops on the tensor-core blocks (16 K per cell)
- *  out[3] backward flops on the CUDA-core blocks (16 K + 6 + 2 rows_out per cell)
+ *  out[3] backward FP32 flops on the FFT-route blocks (recompute, phi_F adjoint, phase, DFT, spectrum
+ *         accumulation, final inverse FFT_P)
  *  out[4] cells, out[5] HBM bytes of the joint stage (Y2 r fwd + r bwd, g_Y2 w, o w + g_o r). cap >= 8. */
 jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap);
 
 /* Profiling hook used by bench.py: when enabled, CUDA events are recorded on the launch stream
- * around the joint-stage kernels (id 0 = forward tensor-core, 1 = forward CUDA-core,
- * 2 = backward tensor-core, 3 = backward CUDA-core). jtfs_prof_read synchronises on the
+ * around the joint stage (id 0 = forward, all routes; 2 = backward, all routes; the tensor-core and
+ * FFT-route launches run concurrently on side streams in between). jtfs_prof_read synchronises on the
  * recorded events, returns the summed elapsed milliseconds and the number of timed launches of
  * `id`, and clears them. */
 void jtfs_prof_enable(int on);

@@ -125,11 +125,12 @@ void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S
                  cudaStream_t st);
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
                      int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);
+// the per-block launches go round-robin over the ns streams ss (forked from and joined to the caller's)
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
+                         int64_t o_sb, int shard, int n_shards, int B, const cudaStream_t* ss, int ns);
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
-                         int B, cudaStream_t st);
+                         int B, const cudaStream_t* ss, int ns);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st);

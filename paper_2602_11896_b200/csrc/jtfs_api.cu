@@ -43,6 +43,41 @@ static int route_of(const Plan& p, size_t bi, bool bwd) {
   return kRouteSimt;
 }
 static std::atomic<int64_t> g_launches{0};
+
+// Fan-out of the joint stage: the tensor-core blocks and the FFT-route blocks are independent (disjoint
+// outputs), so they run on side streams forked from and joined back to the caller's stream; the tail
+// of one launch overlaps the next. Streams/events are per host thread and device.
+constexpr int kFanStreams = 3;
+struct Fanout {
+  cudaStream_t s[kFanStreams] = {};
+  cudaEvent_t fork = nullptr, join[kFanStreams] = {};
+};
+static Fanout* fanout_get() {
+  static thread_local std::vector<Fanout*> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1, nullptr);
+  if (!per_dev[dev]) {
+    Fanout* f = new Fanout();
+    for (int i = 0; i < kFanStreams; ++i) {
+      cudaStreamCreateWithFlags(&f->s[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&f->join[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming);
+    per_dev[dev] = f;
+  }
+  return per_dev[dev];
+}
+static void fan_fork(Fanout* f, cudaStream_t st) {
+  cudaEventRecord(f->fork, st);
+  for (int i = 0; i < kFanStreams; ++i) cudaStreamWaitEvent(f->s[i], f->fork, 0);
+}
+static void fan_join(Fanout* f, cudaStream_t st) {
+  for (int i = 0; i < kFanStreams; ++i) {
+    cudaEventRecord(f->join[i], f->s[i]);
+    cudaStreamWaitEvent(st, f->join[i], 0);
+  }
+}
 void count_launch(int n) { g_launches += n; }
 
 // ---- profiling hooks: events around the dominant kernels, on their launch stream
@@ -408,12 +443,13 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     if (stop == 3) return cudaSuccess;
     // A5: joint lambda_1 stage + phi_F; A6: phi_T
     prof_begin(st, 0);
-    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
+    Fanout* fo = fanout_get();
+    fan_fork(fo, st);
+    launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, shard, n_shards, mb, fo->s[0]);
+    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, fo->s + 1, kFanStreams - 1);
+    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, fo->s[0]);
+    fan_join(fo, st);
     prof_end(st, 0);
-    prof_begin(st, 1);
-    launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, shard, n_shards, mb, st);
-    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, st);
-    prof_end(st, 1);
     launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, shard, n_shards, mb, st);
   }
   RET();
@@ -431,12 +467,14 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, shard, n_shards, mb, st);
     if ((e = cudaMemsetAsync(w.A, 0, (size_t)w.s_A * 8 * mb, st))) return e;
     prof_begin(st, 2);
-    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
+    Fanout* fo = fanout_get();
+    fan_fork(fo, st);
+    launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
+    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s + 1,
+                        kFanStreams - 1);
+    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
+    fan_join(fo, st);
     prof_end(st, 2);
-    prof_begin(st, 3);
-    launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
-    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, st);
-    prof_end(st, 3);
     // FFT of g_Y2 rows -> G_Y (into Y2)
     for (auto& g : p.y2_groups) {
       Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
@@ -498,16 +536,33 @@ jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap) {
   if (!plan || !out || cap < 8) return fail(JTFS_ERR_SIZE, "NULL argument or cap < 8");
   const Plan& p = plan->p;
   double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto lg = [](double v) { return std::log2(v); };
+  const double P = (double)p.P;
+  // per-column FFT-route cost (FP32 flops, 5 L log2 L per complex FFT of length L)
+  std::vector<double> ffw(p.blocks.size(), 0.0), ffb(p.blocks.size(), 0.0);
   for (auto& u : p.units) {
-    const double cells = (double)u.n_rows * (double)p.binfo[u.bi].n_cols;
-    const bool tf = g_use_tc && p.blk_tc[u.bi], tb = g_use_tc && p.blk_tcb[u.bi];
-    c[tf ? 0 : 1] += cells * (tf ? 8.0 * u.n1_max : 8.0 * u.n1_max + 3.0 + 2.0 * u.rows_out);
-    c[tb ? 2 : 3] += cells * (tb ? 16.0 * u.n1_max : 16.0 * u.n1_max + 6.0 + 2.0 * u.rows_out);
-    c[4] += cells;
-    c[5] += 2.0 * 4.0 * u.rows_out * p.binfo[u.bi].n_cols;   // o written (fwd) and g_o read (bwd)
+    const double Lf = (double)u.Lf, nr = (double)u.n_rows, ro = (double)u.rows_out;
+    ffw[u.bi] += 4 * P + 5 * Lf * lg(Lf) + 4 * nr + 2 * ro * nr;                       // fold, IFFT, |.|, phi_F
+    ffb[u.bi] += 4 * P + 10 * Lf * lg(Lf) + 2 * ro * nr + 8 * nr + 4 * P;             // + phase, FFT, accumulate
   }
-  for (size_t bi = 0; bi < p.blocks.size(); ++bi)
-    c[5] += 3.0 * 8.0 * p.blocks[bi].n1_max * p.binfo[bi].n_cols;  // Y2 read fwd, read bwd, g_Y2 write
+  for (auto& u : p.units) {
+    const double ncols = (double)p.binfo[u.bi].n_cols;
+    const double cells = (double)u.n_rows * ncols;
+    const int rf = route_of(p, u.bi, false), rb = route_of(p, u.bi, true);
+    // tensor-core route: the complex contraction (8K flops per modulus value forward, 16K backward)
+    if (rf == kRouteTc) c[0] += cells * 8.0 * u.n1_max;
+    else if (rf == kRouteSimt) c[1] += cells * (8.0 * u.n1_max + 3.0 + 2.0 * u.rows_out);
+    if (rb == kRouteTc) c[2] += cells * 16.0 * u.n1_max;
+    else if (rb == kRouteSimt) c[3] += cells * (16.0 * u.n1_max + 6.0 + 2.0 * u.rows_out);
+    c[4] += cells;
+    c[5] += 2.0 * 4.0 * u.rows_out * ncols;   // o written (fwd) and g_o read (bwd)
+  }
+  for (size_t bi = 0; bi < p.blocks.size(); ++bi) {
+    const double ncols = (double)p.binfo[bi].n_cols;
+    if (route_of(p, bi, false) == kRouteFft) c[1] += ncols * (5 * P * lg(P) + ffw[bi]);
+    if (route_of(p, bi, true) == kRouteFft) c[3] += ncols * (10 * P * lg(P) + ffb[bi]);
+    c[5] += 3.0 * 8.0 * p.blocks[bi].n1_max * ncols;  // Y2 read fwd, read bwd, g_Y2 write
+  }
   for (int i = 0; i < 8; ++i) out[i] = c[i];
   return JTFS_OK;
 }

@@ -287,8 +287,10 @@ static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st)
 }
 
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st) {
+                         int64_t o_sb, int shard, int n_shards, int B, const cudaStream_t* ss, int ns) {
+  int li = 0;
   for (const TcClass& C : d.tc) {
+    const cudaStream_t st = ss[li++ % ns];
     if (C.n_blocks == 0) continue;
     TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
              (int)p.L_fr.size(), shard, n_shards};
@@ -648,8 +650,10 @@ static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream
 
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
-                         int B, cudaStream_t st) {
+                         int B, const cudaStream_t* ss, int ns) {
+  int li = 0;
   for (const TcClass& C : d.tcb) {
+    const cudaStream_t st = ss[li++ % ns];
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
                d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, nullptr};

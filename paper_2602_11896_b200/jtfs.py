@@ -208,8 +208,8 @@ class Plan:
         """Algorithmic per-signal cost of the joint stage (see include/jtfs.h jtfs_plan_cost)."""
         out = np.zeros(8)
         check(self.lib.jtfs_plan_cost(self.h, out.ctypes.data, 8))
-        return {"fwd_tc_flops": out[0], "fwd_simt_flops": out[1], "bwd_tc_flops": out[2],
-                "bwd_simt_flops": out[3], "cells": out[4], "joint_hbm_bytes": out[5],
+        return {"fwd_tc_flops": out[0], "fwd_fft_flops": out[1], "bwd_tc_flops": out[2],
+                "bwd_fft_flops": out[3], "cells": out[4], "joint_hbm_bytes": out[5],
                 "joint_fwd_flops": out[0] + out[1], "joint_bwd_flops": out[2] + out[3]}
 
     def prof_enable(self, on: bool) -> None:
