@@ -44,6 +44,9 @@ struct DeviceTables {
   int32_t* fwd_ulist[6] = {};       int64_t* fwd_tiles[6] = {};    int fwd_n[6] = {};  int64_t fwd_ntiles[6] = {};
   int fwd_kmax[6] = {};
   int32_t* kf_of = nullptr;         // [n_fr] k_f per frequential filter
+  int32_t* hfr_H = nullptr;         // [n_fr] support half-width of h_f
+  // phi_T kernels: (unit, rho) rows in unit order and the prefix of their 256-column tiles
+  int32_t* phT_rows_u = nullptr;    int64_t* phT_tiles = nullptr;  int phT_nrows = 0;  int64_t phT_ntiles = 0;
   int32_t* blk_nmax = nullptr;      // [n_blocks]
   int64_t* ucoef = nullptr;         // [n_units] coefficient offset of the unit's path - o2_start
   int64_t* uo = nullptr;            // [n_units] o_off
@@ -74,6 +77,7 @@ struct DeviceTables {
 };
 
 constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels
+constexpr int kPhiTSmem = 12288;   // phi_T half kernel staged in SMEM up to this many taps
 constexpr int kJC = 64;            // joint stage: columns per CTA
 constexpr int kJR = 64;            // joint stage: rows per chunk
 constexpr int kJN = 64;            // joint backward: n1 rows per CTA

@@ -143,7 +143,7 @@ static void free_tables(DeviceTables* d) {
                   d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
                   d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_owner_unit, d->l1_off,
                   d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw, d->twd,
-                  d->fr_spec, d->u_wts, d->u_wt_off, d->ffw.blist, d->ffw.tiles, d->ffb.blist, d->ffb.tiles};
+                  d->fr_spec, d->u_wts, d->u_wt_off, d->hfr_H, d->phT_rows_u, d->phT_tiles, d->ffw.blist, d->ffw.tiles, d->ffb.blist, d->ffb.tiles};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int c = 0; c < 6; ++c) {
@@ -251,6 +251,23 @@ static cudaError_t upload(Plan& p) {
   std::vector<int32_t> kf;
   for (auto& f : p.L_fr) kf.push_back(std::min(f.j, p.log2F));
   UP(kf, kf_of);
+  UP(p.hfr_H, hfr_H);
+  {
+    std::vector<int32_t> ru;
+    std::vector<int64_t> cnt;
+    for (size_t u = 0; u < p.units.size(); ++u)
+      for (int rho = 0; rho < p.units[u].rows_out; ++rho) {
+        ru.push_back((int32_t)u);
+        ru.push_back(rho);
+        cnt.push_back((p.binfo[p.units[u].bi].n_cols + 255) / 256);
+      }
+    d->phT_nrows = (int)cnt.size();
+    t = prefix(cnt);
+    d->phT_ntiles = t.back();
+    t.pop_back();
+    UP(ru, phT_rows_u);
+    UP(t, phT_tiles);
+  }
   std::vector<int32_t> nm;
   std::vector<int64_t> bt;
   d->Kmax = 0;

@@ -42,8 +42,8 @@ __device__ __forceinline__ int64_t cdist(int64_t a, int64_t L) {  // circular |a
 // =====================================================================================
 __global__ void k_o1_W(const float* __restrict__ S1t, int64_t S1t_sb, float2* __restrict__ W1, int64_t W1_sb,
                        const float2* __restrict__ hfr, const int64_t* __restrict__ rlo,
-                       const int64_t* __restrict__ nrows, const int32_t* __restrict__ kf_of, int N1, int P,
-                       int64_t Ft) {
+                       const int64_t* __restrict__ nrows, const int32_t* __restrict__ kf_of,
+                       const int32_t* __restrict__ hH, int N1, int P, int64_t Ft) {
   const int f = blockIdx.y, b = blockIdx.z;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = q / Ft, t = q % Ft;
@@ -55,9 +55,14 @@ __global__ void k_o1_W(const float* __restrict__ S1t, int64_t S1t_sb, float2* __
   const float* x = S1t + b * S1t_sb + t;
   const float2* h = hfr + (int64_t)f * P;
   float2 acc = make_float2(0.f, 0.f);
-  for (int n = 0; n < N1; ++n) {
-    float v = x[(int64_t)n * Ft];
-    float2 hv = __ldg(h + ((hb - n) & (P - 1)));
+  // h_f[(hb - n) mod P] vanishes unless n is within the support half-width H of hb (circularly)
+  const int H = hH[f];
+  const int span = 2 * H + 1 >= P ? P : 2 * H + 1;
+  for (int q = 0; q < span; ++q) {
+    const int n = (hb - H + q) & (P - 1);
+    if (n >= N1) continue;
+    const float v = x[(int64_t)n * Ft];
+    const float2 hv = __ldg(h + ((hb - n) & (P - 1)));
     acc.x = fmaf(hv.x, v, acc.x);
     acc.y = fmaf(hv.y, v, acc.y);
   }
@@ -172,8 +177,8 @@ __global__ void k_o1_bwd_time(const float* __restrict__ rres, int64_t r_sb, floa
 // gS1t[n][tau] = sum_f sum_i Re(conj(h_f[(r_i 2^k_f - n) mod P]) gW1[f][i][tau])
 __global__ void k_o1_bwd_S1t(const float2* __restrict__ W1, int64_t W1_sb, float* __restrict__ gS1t,
                              int64_t gS_sb, const float2* __restrict__ hfr, const int64_t* __restrict__ rlo,
-                             const int64_t* __restrict__ nrows, const int32_t* __restrict__ kf_of, int nfr1,
-                             int N1, int P, int64_t Ft) {
+                             const int64_t* __restrict__ nrows, const int32_t* __restrict__ kf_of,
+                             const int32_t* __restrict__ hH, int nfr1, int N1, int P, int64_t Ft) {
   const int b = blockIdx.y;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = q / Ft, tau = q % Ft;
@@ -185,11 +190,25 @@ __global__ void k_o1_bwd_S1t(const float2* __restrict__ W1, int64_t W1_sb, float
     const float2* h = hfr + (int64_t)f * P;
     const float2* g = W1 + b * W1_sb + (int64_t)f * P * Ft + tau;
     float accf = 0.f;
-    for (int64_t i = 0; i < nrows[f]; ++i) {
-      int64_t r = (rlo[f] + i) % Lf;
-      int hb = (int)((r << kf) & (P - 1));
-      float2 hv = __ldg(h + ((hb - n) & (P - 1)));
-      float2 gv = g[i * Ft];
+    // rows r with |r 2^kf - n| <= H (circular on P): r in [ceil((n-H)/2^kf), floor((n+H)/2^kf)] mod L_f
+    const int H = hH[f];
+    const int nr = (int)nrows[f], r0 = (int)rlo[f], Lm = (int)Lf - 1;
+    int rs, cnt;
+    if (2 * H + 1 >= P) { rs = 0; cnt = (int)Lf; }
+    else {
+      const int s = 1 << kf;
+      const int a = (int)n - H, bnd = (int)n + H;
+      rs = a >= 0 ? (a + s - 1) >> kf : -((-a) >> kf);
+      const int rhi = bnd >> kf;                          // bnd >= 0
+      cnt = min(rhi - rs + 1, (int)Lf);
+    }
+    for (int q = 0; q < cnt; ++q) {
+      const int r = (rs + q) & Lm;
+      const int i = (r - r0) & Lm;
+      if (i >= nr) continue;
+      const int hb = (r << kf) & (P - 1);
+      const float2 hv = __ldg(h + ((hb - (int)n) & (P - 1)));
+      const float2 gv = g[(int64_t)i * Ft];
       accf = fmaf(hv.x, gv.x, fmaf(hv.y, gv.y, accf));
     }
     acc += accf;
@@ -694,6 +713,115 @@ __global__ void k_phiT_adj(const float* __restrict__ rres, int64_t r_sb, float* 
   go[b * go_sb + q] = (float)acc;
 }
 
+// ---- phi_T over time, row-tiled (one CTA per (unit, rho) row and 256-column tile): the tile is located
+// once per CTA from the prefix table rt (rows of all units, in unit order), float accumulation.
+struct PhiTRow {
+  int u, rho;
+  int64_t c0;   // first column of the tile
+};
+__device__ __forceinline__ PhiTRow phiT_row(const int64_t* __restrict__ rt, const int32_t* __restrict__ rt_u,
+                                            int nrows, int64_t tile, int tiles_per_row_shift_unused) {
+  (void)tiles_per_row_shift_unused;
+  int lo = 0, hi = nrows - 1;                       // rt[r] = first tile of row r (prefix)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(rt + mid) <= tile) lo = mid; else hi = mid - 1;
+  }
+  PhiTRow R;
+  R.u = rt_u[2 * lo];
+  R.rho = rt_u[2 * lo + 1];
+  R.c0 = (tile - rt[lo]) * 256;
+  return R;
+}
+
+// g_o[u][rho][i] = sum_{t'} tT_s2[dist((m0+t')D - c_i)] r[path][rho][t']  (adjoint of Eq.4's phi_T + stride)
+__global__ void __launch_bounds__(256) k_phiT_adj2(
+    const float* __restrict__ rres, int64_t r_sb, float* __restrict__ go, int64_t go_sb,
+    const JointUnit* __restrict__ units, const BlockInfo* __restrict__ binfo, const float* __restrict__ phiT_half,
+    const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H, const int64_t* __restrict__ ucoef,
+    const int64_t* __restrict__ rt, const int32_t* __restrict__ rt_u, int nrows, int64_t o2_start, int frames,
+    int64_t m0, int shard, int n_shards) {
+  __shared__ PhiTRow R;
+  __shared__ float rr[256];
+  const int b = blockIdx.y;
+  if (threadIdx.x == 0) R = phiT_row(rt, rt_u, nrows, blockIdx.x, 0);
+  __syncthreads();
+  if (R.u % n_shards != shard) return;
+  const JointUnit U = units[R.u];
+  const BlockInfo bf = binfo[U.bi];
+  const float* rsrc = rres + b * r_sb + o2_start + ucoef[R.u] + (int64_t)R.rho * frames;
+  for (int t = threadIdx.x; t < frames; t += 256) rr[t] = rsrc[t];
+  __syncthreads();
+  const int64_t i = R.c0 + threadIdx.x;
+  if (i >= bf.n_cols) return;
+  const int H = (int)phiT_H[bf.s2];
+  const float* tT = phiT_half + phiT_off[bf.s2];
+  const int D = bf.D;
+  float acc = 0.f;
+  if (bf.n_cols < bf.T2) {
+    // unwrapped coordinates: column i sits at x = m0 D - H + i; frame m at m D; |m D - x| <= H
+    const int64_t x = m0 * D - H + i;
+    const int64_t lo = x - H, hi = x + H;
+    int64_t mlo = lo <= 0 ? -((-lo) / D) : (lo + D - 1) / D;
+    int64_t mhi = hi >= 0 ? hi / D : -((-hi + D - 1) / D);
+    if (mlo < m0) mlo = m0;
+    if (mhi > m0 + frames - 1) mhi = m0 + frames - 1;
+    int dd = (int)(mlo * D - x);
+    for (int64_t m = mlo; m <= mhi; ++m, dd += D) acc = fmaf(__ldg(tT + (dd < 0 ? -dd : dd)), rr[m - m0], acc);
+  } else {
+    const int64_t c = (bf.c_lo + i) % bf.T2;
+    for (int tp = 0; tp < frames; ++tp) {
+      const int64_t dd = cdist((m0 + tp) * D - c, bf.T2);
+      if (dd <= H) acc = fmaf(__ldg(tT + dd), rr[tp], acc);
+    }
+  }
+  go[b * go_sb + U.o_off + (int64_t)R.rho * bf.n_cols + i] = acc;
+}
+
+// S[coef(u, rho, t')] = sum_j tT_s2[|j|] o[u][rho][col(t' D + j)]: one CTA per (unit, rho) row (tile 0 of
+// each row only), the half kernel staged in SMEM when it fits, one warp per frame (lanes stride j)
+__global__ void __launch_bounds__(256) k_phiT_fwd2(
+    const float* __restrict__ o, int64_t o_sb, float* __restrict__ S, int64_t S_sb,
+    const JointUnit* __restrict__ units, const int64_t* __restrict__ ucoef, const BlockInfo* __restrict__ binfo,
+    const float* __restrict__ phiT_half, const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H,
+    const int32_t* __restrict__ rows_u, int64_t o2_start, int frames, int64_t m0, int shard, int n_shards) {
+  extern __shared__ float tsm[];
+  const int u = rows_u[2 * blockIdx.x], rho = rows_u[2 * blockIdx.x + 1];
+  if (u % n_shards != shard) return;
+  const int b = blockIdx.y;
+  const JointUnit U = units[u];
+  const BlockInfo bf = binfo[U.bi];
+  const int H = (int)phiT_H[bf.s2];
+  const float* tg = phiT_half + phiT_off[bf.s2];
+  const bool in_sm = H + 1 <= kPhiTSmem;
+  if (in_sm)
+    for (int j = threadIdx.x; j <= H; j += 256) tsm[j] = tg[j];
+  __syncthreads();
+  const float* tT = in_sm ? tsm : tg;
+  const float* src = o + b * o_sb + U.o_off + (int64_t)rho * bf.n_cols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* dst = S + b * S_sb + o2_start + ucoef[u] + (int64_t)rho * frames;
+  for (int tp = warp; tp < frames; tp += 8) {
+    float acc = 0.f;
+    if (bf.n_cols < bf.T2) {
+      const int64_t base = (int64_t)tp * bf.D + H;       // unwrapped: column of position m D + j
+      for (int j = -H + lane; j <= H; j += 32) acc = fmaf(tT[j < 0 ? -j : j], src[base + j], acc);
+    } else {
+      int64_t jlo, jhi;
+      sym_range(H, bf.T2, &jlo, &jhi);
+      const int64_t cm = (m0 + tp) * bf.D;
+      for (int64_t j = jlo + lane; j <= jhi; j += 32) {
+        int64_t i = (cm + j - bf.c_lo) % bf.T2;
+        if (i < 0) i += bf.T2;
+        acc = fmaf(tT[j < 0 ? -j : j], src[i], acc);
+      }
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+    if (lane == 0) dst[tp] = acc;
+  }
+}
+
 // loss (R19): r = S - St on owned order-1/2 coefficients (0 elsewhere), E_b = 1/2 sum r^2
 __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ S, int64_t S_sb, const float* __restrict__ St,
                                               int64_t St_sb, float* __restrict__ r, int64_t r_sb,
@@ -730,8 +858,8 @@ void launch_o1_fwd(const Plan& p, const DeviceTables& d, const float* S1t, int64
   const int P = (int)p.P;
   const int64_t m0 = p.pad_left / p.T;
   dim3 g1((unsigned)((p.P * p.Ft + 255) / 256), (unsigned)nfr1, (unsigned)B);
-  k_o1_W<<<g1, 256, 0, st>>>(S1t, S1t_sb, W1, W1_sb, d.hfr, d.o1_rlo, d.o1_nrows, d.kf_of, (int)p.psi1.size(), P,
-                             p.Ft);
+  k_o1_W<<<g1, 256, 0, st>>>(S1t, S1t_sb, W1, W1_sb, d.hfr, d.o1_rlo, d.o1_nrows, d.kf_of, d.hfr_H,
+                             (int)p.psi1.size(), P, p.Ft);
   if (nfr1 > 1) {
     dim3 g2((unsigned)((p.P * p.frames + 255) / 256), (unsigned)(nfr1 - 1), (unsigned)B);
     k_o1_time<<<g2, 256, 0, st>>>(W1, W1_sb, V2, V2_sb, d.o1_nrows, d.phiT_half + p.phiT_off[p.log2T],
@@ -760,8 +888,8 @@ void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t
   k_o1_bwd_time<<<g2, 256, 0, st>>>(r, r_sb, W1, W1_sb, V2, V2_sb, d.o1_nrows, d.phiT_half + p.phiT_off[p.log2T],
                                     p.phiT_H[p.log2T], P, p.Ft, p.frames, m0, thr);
   dim3 g3((unsigned)((p.psi1.size() * p.Ft + 255) / 256), (unsigned)B);
-  k_o1_bwd_S1t<<<g3, 256, 0, st>>>(W1, W1_sb, gS1t, gS1t_sb, d.hfr, d.o1_rlo, d.o1_nrows, d.kf_of, nfr1,
-                                   (int)p.psi1.size(), P, p.Ft);
+  k_o1_bwd_S1t<<<g3, 256, 0, st>>>(W1, W1_sb, gS1t, gS1t_sb, d.hfr, d.o1_rlo, d.o1_nrows, d.kf_of, d.hfr_H,
+                                   nfr1, (int)p.psi1.size(), P, p.Ft);
   count_launch(2);
 }
 
@@ -793,10 +921,16 @@ void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, in
 
 void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,
                      int64_t S_sb, int shard, int n_shards, int B, cudaStream_t st) {
-  if (d.n_o2 == 0) return;
-  dim3 g((unsigned)((d.n_o2 + 7) / 8), (unsigned)B);
-  k_phiT_fwd<<<g, 256, 0, st>>>(o, o_sb, S, S_sb, d.units, d.ucoef, d.n_units, d.binfo, d.phiT_half, d.phiT_off,
-                                d.phiT_H, d.o2_start, d.n_o2, p.frames, p.pad_left / p.T, shard, n_shards);
+  if (d.n_o2 == 0 || d.phT_nrows == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_phiT_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, kPhiTSmem * 4);
+    attr = true;
+  }
+  dim3 g((unsigned)d.phT_nrows, (unsigned)B);
+  k_phiT_fwd2<<<g, 256, kPhiTSmem * 4, st>>>(o, o_sb, S, S_sb, d.units, d.ucoef, d.binfo, d.phiT_half, d.phiT_off,
+                                             d.phiT_H, d.phT_rows_u, d.o2_start, (int)p.frames, p.pad_left / p.T,
+                                             shard, n_shards);
   count_launch();
 }
 
@@ -810,11 +944,11 @@ void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S
 
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
                      int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st) {
-  if (p.o_size == 0) return;
-  dim3 g((unsigned)((p.o_size + 255) / 256), (unsigned)B);
-  k_phiT_adj<<<g, 256, 0, st>>>(r, r_sb, go, go_sb, d.units, d.uo, d.n_units, d.binfo, d.phiT_half, d.phiT_off,
-                                d.phiT_H, d.ucoef, d.o2_start, p.o_size, p.frames, p.pad_left / p.T, shard,
-                                n_shards);
+  if (p.o_size == 0 || d.phT_ntiles == 0) return;
+  dim3 g((unsigned)d.phT_ntiles, (unsigned)B);
+  k_phiT_adj2<<<g, 256, 0, st>>>(r, r_sb, go, go_sb, d.units, d.binfo, d.phiT_half, d.phiT_off, d.phiT_H, d.ucoef,
+                                 d.phT_tiles, d.phT_rows_u, d.phT_nrows, d.o2_start, (int)p.frames,
+                                 p.pad_left / p.T, shard, n_shards);
   count_launch();
 }
 

@@ -102,6 +102,7 @@ struct Plan {
   std::vector<Support> phiT_sup;                // [log2T+1] on N_pad>>k
   std::vector<float> hfr;                       // [n_fr_all][P][2] row kernels (complex)
   std::vector<double> hfr_d;                    // same in float64 (for the tensor-core images)
+  std::vector<int32_t> hfr_H;                   // [n_fr_all] support half-width of h_f (1e-9 relative)
   std::vector<TcUnit> tc_units;                 // [n_units]
   std::vector<TcBlock> tc_blocks;               // tensor-core eligible blocks
   std::vector<char> blk_tc;                     // [n_blocks] 1 = forward on the tensor-core path

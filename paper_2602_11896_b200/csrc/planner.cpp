@@ -418,6 +418,18 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
       p->hfr_d.push_back(re);
       p->hfr_d.push_back(im);
     }
+  // support half-widths of h_f on the circle (|h| >= 1e-9 max|h|, R26): row loops skip the rest
+  for (int f = 0; f < nfr; ++f) {
+    const double* h = p->hfr_d.data() + (size_t)f * p->P * 2;
+    double mx = 0;
+    for (int64_t n = 0; n < p->P; ++n) mx = std::max(mx, std::hypot(h[2 * n], h[2 * n + 1]));
+    int64_t H = 0;
+    for (int64_t n = 0; n <= p->P / 2; ++n) {
+      const int64_t m = (p->P - n) % p->P;
+      if (std::hypot(h[2 * n], h[2 * n + 1]) >= 1e-9 * mx || std::hypot(h[2 * m], h[2 * m + 1]) >= 1e-9 * mx) H = n;
+    }
+    p->hfr_H.push_back((int32_t)H);
+  }
   // phi_F kernels at levels k = 0..log2F on P>>k grids; truncation half-widths (1e-9 rel)
   std::vector<int64_t> HF(log2F + 1);
   for (int k = 0; k <= log2F; ++k) {
