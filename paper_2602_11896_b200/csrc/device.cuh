@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fft.cuh"
 #include "plan.h"
 
 namespace jtfs {
@@ -61,6 +62,8 @@ struct DeviceTables {
   int64_t* o1_rlo = nullptr;        int64_t* o1_nrows = nullptr;
   float2* tw = nullptr;
   double2* twd = nullptr;
+  FftTables fftt;                   // views of tw/twd + four-step tables (owned: fs_bufs)
+  std::vector<void*> fs_bufs;
   int Kmax = 0, Kmax_simt_bwd = 0;
   // tensor-core joint stage
   float* tc_img = nullptr;

@@ -1,10 +1,12 @@
 // fft.cu — batched power-of-two complex FFTs for sm_100a, hand written (no cuFFT).
 //
-// Shared-memory Stockham autosort with radix-4 passes (+ one radix-2 pass for odd log2 n); each
-// butterfly is staged in registers so the pass runs in place in SMEM. Lengths <= 4096 run in one
-// kernel (several short rows per CTA); longer lengths L = L1 * 4096 use the four-step scheme:
-//   A) L1-point column transforms in place + twiddle W_L^{n2 k1}   (k_fft_colA)
-//   B) 4096-point row transforms written transposed to the output  (k_fft_rowB)
+// Radix-16 Stockham passes in SMEM (fft_dev.cuh: two radix-4 levels in registers, one radix-8/4/2
+// pass for the remainder) with the loads of the first pass and the stores of the last pass going
+// straight to global memory. Lengths <= 4096 run in one kernel (k_fft_small, 4096 / L rows per CTA);
+// longer lengths L = L1 * 4096 use the four-step scheme:
+//   A) L1-point column transforms in place, times the twiddle W_L^{n2 k1} (k_fft_colA; sequences
+//      interleaved in SMEM so the strided columns load and store coalesced)
+//   B) 4096-point row transforms written transposed to the output (k_fft_rowB)
 // Used for rfft/ifft/cfft of the listings P:203, P:209, P:211, P:235, P:282, P:285 and their
 // adjoints. Forward = exp(-2 pi i k n / L); inverse = exp(+...) / L (numpy convention).
 // Templated on the compute type (float2 or double2) and on the input/output element types: the
@@ -22,79 +24,129 @@
 
 namespace jtfs {
 
-// ---------------------------------------------------------------- n <= 4096, M rows per CTA
+template <class C> struct FftTw;
+template <> struct FftTw<float2> {
+  static const float2* base(const FftTables& t) { return t.tw; }
+  static const float2* lo(const FftTables& t, int lg) { return t.lo_f[lg]; }
+  static const float2* hi(const FftTables& t, int lg) { return t.hi_f[lg]; }
+};
+template <> struct FftTw<double2> {
+  static const double2* base(const FftTables& t) { return t.twd; }
+  static const double2* lo(const FftTables& t, int lg) { return t.lo_d[lg]; }
+  static const double2* hi(const FftTables& t, int lg) { return t.hi_d[lg]; }
+};
+
+// SMEM twiddle table W_L^e, e < L = 2^lgL, from the global 4096-entry table
+template <class C, int NT>
+__device__ __forceinline__ void load_twiddles(C* tws, const C* __restrict__ tw, int lgL) {
+  for (int e = threadIdx.x; e < (1 << lgL); e += NT) tws[e] = tw[e << (12 - lgL)];
+}
+
+// ---------------------------------------------------------------- L <= 4096: 4096 / L rows per CTA
+template <class TI, class C>
+struct LdRows {  // first pass reads global rows (converted to the compute type), zero past the last row
+  const TI* src;
+  int lgL, rows;
+  __device__ __forceinline__ C operator()(int c, int e) const {
+    return c < rows ? t_cvt<C>(src[((int64_t)c << lgL) + e]) : Cx<C>::mk(0, 0);
+  }
+};
+template <class TO, class C>
+struct StRows {  // last pass writes global rows, scaled
+  TO* dst;
+  int lgL, rows;
+  typename Cx<C>::R sc;
+  __device__ __forceinline__ void operator()(int c, int e, C v) const {
+    if (c < rows) dst[((int64_t)c << lgL) + e] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
+  }
+};
+
 template <class TI, class TO, class C>
 __global__ void __launch_bounds__(256) k_fft_small(const TI* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
-                                                   int n, int M, int inv, double scale, const C* __restrict__ tw) {
+                                                   int lgL, int lgM, int inv, double scale,
+                                                   const C* __restrict__ tw) {
   extern __shared__ __align__(16) uint8_t smraw[];
-  C* s = reinterpret_cast<C*>(smraw);
+  C* s = reinterpret_cast<C*>(smraw);          // [M][L] (swizzled sequences)
+  C* tws = s + (1 << (lgL + lgM));             // [L]
   const int b = blockIdx.y;
-  const int64_t r0 = (int64_t)blockIdx.x * M;
-  const int rows = (int)((ri.count - r0) < M ? (ri.count - r0) : M);
-  const TI* src = in + b * ri.stride_b + ri.off + r0 * n;
-  TO* dstp = out + b * ro.stride_b + ro.off + r0 * n;
-  const int tot = rows * n;
-  for (int i = threadIdx.x; i < M * n; i += 256) s[i] = (i < tot) ? t_cvt<C>(src[i]) : Cx<C>::mk(0, 0);
+  const int64_t r0 = (int64_t)blockIdx.x << lgM;
+  const int rows = (int)((ri.count - r0) < (1 << lgM) ? (ri.count - r0) : (1 << lgM));
+  load_twiddles<C, 256>(tws, tw, lgL);
   __syncthreads();
-  smem_fft<C, 256>(s, n, M, 1, n, false, inv != 0, tw);
-  const typename Cx<C>::R sc = (typename Cx<C>::R)scale;
-  for (int i = threadIdx.x; i < tot; i += 256) dstp[i] = t_cvt<TO>(Cx<C>::mk(s[i].x * sc, s[i].y * sc));
+  const LdRows<TI, C> ld{in + b * ri.stride_b + ri.off + (r0 << lgL), lgL, rows};
+  const StRows<TO, C> st{out + b * ro.stride_b + ro.off + (r0 << lgL), lgL, rows, (typename Cx<C>::R)scale};
+  const SeqCol<C> buf{s, 1 << lgL};
+  seq_fft<C, 256, 16>(lgM, lgL, inv != 0, tws, lgL, ld, st, buf);
 }
 
 // ---------------------------------------------------------------- four-step A: columns
-// x viewed as [L1][L2] (n = n1*L2 + n2). For the CTA's CW columns n2: y[k1][n2] =
-// sum_n1 x[n1][n2] W_L1^{n1 k1}, times W_L^{n2 k1}; written back in place.
-__device__ __forceinline__ void sincospi_t(float a, float* s, float* c) { sincospif(a, s, c); }
-__device__ __forceinline__ void sincospi_t(double a, double* s, double* c) { sincospi(a, s, c); }
+// x viewed as [L1][L2] (n = n1 L2 + n2). For the CTA's CW columns n2: y[k1][n2] = sum_n1 x[n1][n2]
+// W_L1^{n1 k1}, times W_L^{n2 k1}, written back in place. W_L^e (e = n2 k1 < L) = lo[e & 4095] hi[e >> 12].
+template <class C>
+struct LdCols {
+  const C* base;   // row n1 at base + n1 * L2
+  int L2;
+  __device__ __forceinline__ C operator()(int c, int n1) const { return base[(int64_t)n1 * L2 + c]; }
+};
+template <class C>
+struct StColsTw {
+  C* base;
+  int L2, c0, inv;
+  const C* lo;
+  const C* hi;
+  __device__ __forceinline__ void operator()(int c, int k1, C v) const {
+    const int e = (c0 + c) * k1;
+    C w = cmul_f(lo[e & 4095], hi[e >> 12]);
+    if (inv) w.y = -w.y;
+    base[(int64_t)k1 * L2 + c] = cmul_f(v, w);
+  }
+};
 
 template <class C>
-__global__ void __launch_bounds__(512) k_fft_colA(C* __restrict__ data, Rows ri, int L1, int L2, int CW, int inv,
-                                                  const C* __restrict__ tw) {
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 1) k_fft_colA(C* __restrict__ data, Rows ri, int lgL1, int L2, int lgCW, int inv,
+                                                  const C* __restrict__ tw, const C* __restrict__ lo,
+                                                  const C* __restrict__ hi) {
   extern __shared__ __align__(16) uint8_t smraw[];
-  C* s = reinterpret_cast<C*>(smraw);
-  using R = typename Cx<C>::R;
+  C* s = reinterpret_cast<C*>(smraw);                  // [L1][CW] interleaved
+  C* tws = s + (1 << (lgL1 + lgCW));                   // [L1]
   const int64_t r = blockIdx.y;
   const int b = blockIdx.z;
-  const int64_t L = (int64_t)L1 * L2;
-  C* base = data + b * ri.stride_b + ri.off + r * L;
-  const int c0 = blockIdx.x * CW;
-  for (int i = threadIdx.x; i < L1 * CW; i += 512) {
-    int n1 = i / CW, c = i % CW;
-    s[i] = base[(int64_t)n1 * L2 + c0 + c];
-  }
+  const int64_t L = (int64_t)L2 << lgL1;
+  const int c0 = blockIdx.x << lgCW;
+  C* base = data + b * ri.stride_b + ri.off + r * L + c0;
+  load_twiddles<C, 256>(tws, tw, lgL1);
   __syncthreads();
-  smem_fft<C, 512>(s, L1, CW, CW, 1, true, inv != 0, tw);
-  const R sgn = inv ? (R)2 : (R)-2;
-  for (int i = threadIdx.x; i < L1 * CW; i += 512) {
-    int k1 = i / CW, c = i % CW;
-    int64_t e = ((int64_t)(c0 + c) * k1) % L;  // exact; 2e/L exact in fp32 (L <= 2^22)
-    R sn, cs;
-    sincospi_t(sgn * (R)e / (R)L, &sn, &cs);
-    base[(int64_t)k1 * L2 + c0 + c] = t_mul(s[i], Cx<C>::mk(cs, sn));
-  }
+  const LdCols<C> ld{base, L2};
+  const StColsTw<C> st{base, L2, c0, inv, lo, hi};
+  const SeqInter<C> buf{s, 1 << lgCW};
+  seq_fft<C, 256, 16>(lgCW, lgL1, inv != 0, tws, lgL1, ld, st, buf);
 }
 
 // ---------------------------------------------------------------- four-step B: rows, transposed out
 // For rows k1 in [k1_0, k1_0 + M): X[k1 + L1 k2] = sum_n2 y[k1][n2] W_L2^{n2 k2}.
-template <class C, class TO>
-__global__ void __launch_bounds__(1024) k_fft_rowB(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
-                                                   int L1, int L2, int M, int inv, double scale,
-                                                   const C* __restrict__ tw) {
+template <class C, class TO, int NPT>
+__global__ void __launch_bounds__(512) k_fft_rowB(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
+                                                  int L1, int lgM, int inv, double scale, const C* __restrict__ tw) {
   extern __shared__ __align__(16) uint8_t smraw[];
-  C* s = reinterpret_cast<C*>(smraw);
+  constexpr int lgL2 = 12, L2 = 4096;
+  C* s = reinterpret_cast<C*>(smraw);                 // [M][L2] swizzled
+  C* tws = s + (L2 << lgM);                           // [L2]
   const int64_t r = blockIdx.y;
   const int b = blockIdx.z;
   const int64_t L = (int64_t)L1 * L2;
+  const int M = 1 << lgM;
   const int k10 = blockIdx.x * M;
   const C* src = in + b * ri.stride_b + ri.off + r * L + (int64_t)k10 * L2;
   TO* dst = out + b * ro.stride_b + ro.off + r * L;
-  for (int i = threadIdx.x; i < M * L2; i += 1024) s[i] = src[i];
+  load_twiddles<C, 512>(tws, tw, lgL2);
   __syncthreads();
-  smem_fft<C, 1024>(s, L2, M, 1, L2, false, inv != 0, tw);
+  const LdRows<C, C> ld{src, lgL2, M};
+  const SeqCol<C> buf{s, L2};
+  seq_fft<C, 512, NPT>(lgM, lgL2, inv != 0, tws, lgL2, ld, buf, buf);
   const typename Cx<C>::R sc = (typename Cx<C>::R)scale;
-  for (int i = threadIdx.x; i < M * L2; i += 1024) {
-    int m = i % M, k2 = i / M;
-    C v = s[m * L2 + k2];
+  for (int i = threadIdx.x; i < (L2 << lgM); i += 512) {
+    const int m = i & (M - 1), k2 = i >> lgM;
+    const C v = buf(m, k2);
     dst[(int64_t)k2 * L1 + k10 + m] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
   }
 }
@@ -113,60 +165,90 @@ static std::vector<T> twiddles() {
 std::vector<float2> fft_twiddle_table() { return twiddles<float2>(); }
 std::vector<double2> fft_twiddle_table_d() { return twiddles<double2>(); }
 
+// four-step twiddles W_L^e = lo[e & 4095] * hi[e >> 12] for L = 2^lgL > 4096 (float64 evaluation)
+template <class T>
+static void fourstep_tables(int lgL, std::vector<T>* lo, std::vector<T>* hi) {
+  const double L = std::ldexp(1.0, lgL);
+  lo->resize(4096);
+  hi->resize((size_t)1 << (lgL - 12));
+  for (int e = 0; e < 4096; ++e) {
+    const double a = -2.0 * 3.14159265358979323846 * (double)e / L;
+    (*lo)[e].x = (decltype((*lo)[e].x))std::cos(a);
+    (*lo)[e].y = (decltype((*lo)[e].y))std::sin(a);
+  }
+  for (size_t e = 0; e < hi->size(); ++e) {
+    const double a = -2.0 * 3.14159265358979323846 * (double)(e * 4096) / L;
+    (*hi)[e].x = (decltype((*hi)[e].x))std::cos(a);
+    (*hi)[e].y = (decltype((*hi)[e].y))std::sin(a);
+  }
+}
+void fft_fourstep_tables_f(int lgL, std::vector<float2>* lo, std::vector<float2>* hi) { fourstep_tables(lgL, lo, hi); }
+void fft_fourstep_tables_d(int lgL, std::vector<double2>* lo, std::vector<double2>* hi) { fourstep_tables(lgL, lo, hi); }
+
+static int ilog2_exact(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
 template <class TI, class TO, class C>
-static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, bool inverse, const C* tw,
+static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,
                                 cudaStream_t st) {
+  constexpr int kRowNPT = 16;                                  // rowB: 2 rows per CTA (2 CTAs per SM)
+  constexpr int kRowLgM = 1;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fft_rowB<C, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (sizeof(C) == 8 ? 4 : 2) * 4096 * (int)sizeof(C));
-    cudaFuncSetAttribute(k_fft_colA<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(C));
-    cudaFuncSetAttribute(k_fft_small<TI, TO, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(C));
+    cudaFuncSetAttribute(k_fft_rowB<C, TO, kRowNPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(((4096 << kRowLgM) + 4096) * sizeof(C)));
+    cudaFuncSetAttribute(k_fft_colA<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * sizeof(C)));
+    cudaFuncSetAttribute(k_fft_small<TI, TO, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(8192 * sizeof(C)));
     attr = true;
   }
   const int64_t L = ri.L;
+  const int lgL = ilog2_exact(L);
   const double scale = inverse ? 1.0 / (double)L : 1.0;
   if (ri.count <= 0 || B <= 0) return cudaSuccess;
+  const C* tw = FftTw<C>::base(T);
   if (L <= 4096) {
-    int M = (int)(L >= 1024 ? 1 : 1024 / L);
-    dim3 grid((unsigned)((ri.count + M - 1) / M), (unsigned)B);
-    k_fft_small<TI, TO, C><<<grid, 256, (size_t)M * L * sizeof(C), st>>>(in, out, ri, ro, (int)L, M,
-                                                                         inverse ? 1 : 0, scale, tw);
+    const int lgM = 12 - lgL;
+    dim3 grid((unsigned)((ri.count + (1 << lgM) - 1) >> lgM), (unsigned)B);
+    k_fft_small<TI, TO, C><<<grid, 256, (size_t)(4096 + L) * sizeof(C), st>>>(in, out, ri, ro, lgL, lgM,
+                                                                           inverse ? 1 : 0, scale, tw);
     count_launch();
     return cudaGetLastError();
   }
   // four-step; step A runs in place on `in` (it is clobbered; requires TI == C), step B writes `out`
   static_assert(sizeof(TI) == sizeof(C), "four-step input must already be in the compute type");
-  const int L2 = 4096, L1 = (int)(L / 4096);
-  // columns per CTA: ~8192 elements per CTA, at least 16 columns (>= 128-byte rows)
-  const int CW = std::max(16, std::min(L2, 8192 / L1));
+  const int L2 = 4096, lgL1 = lgL - 12, L1 = 1 << lgL1;
+  const int lgCW = std::min(12, 12 - lgL1);                   // CW * L1 = 4096 points per CTA
   {
-    dim3 grid((unsigned)(L2 / CW), (unsigned)ri.count, (unsigned)B);
-    k_fft_colA<C><<<grid, 512, (size_t)L1 * CW * sizeof(C), st>>>(reinterpret_cast<C*>(const_cast<TI*>(in)), ri,
-                                                                     L1, L2, CW, inverse ? 1 : 0, tw);
+    dim3 grid((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
+    k_fft_colA<C><<<grid, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(
+        reinterpret_cast<C*>(const_cast<TI*>(in)), ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw, FftTw<C>::lo(T, lgL),
+        FftTw<C>::hi(T, lgL));
   }
   {
-    const int Mmax = sizeof(C) == 8 ? 4 : 2;   // rows per CTA: 128 KB of SMEM
-    const int M = L1 >= Mmax ? Mmax : L1;
-    dim3 grid((unsigned)(L1 / M), (unsigned)ri.count, (unsigned)B);
-    k_fft_rowB<C, TO><<<grid, 1024, (size_t)M * L2 * sizeof(C), st>>>(reinterpret_cast<const C*>(in), out, ri, ro,
-                                                                        L1, L2, M, inverse ? 1 : 0, scale, tw);
+    const int lgM = std::min(kRowLgM, lgL1);
+    dim3 grid((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
+    k_fft_rowB<C, TO, kRowNPT><<<grid, 512, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
+        reinterpret_cast<const C*>(in), out, ri, ro, L1, lgM, inverse ? 1 : 0, scale, tw);
   }
   count_launch(2);
   return cudaGetLastError();
 }
 
-cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse, const float2* tw,
+cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,
                        cudaStream_t st) {
-  return fft_launch_t<float2, float2, float2>(in, out, ri, ro, B, inverse, tw, st);
+  return fft_launch_t<float2, float2, float2>(in, out, ri, ro, B, inverse, T, st);
 }
 cudaError_t fft_launch_dd(const double2* in, double2* out, Rows ri, Rows ro, int B, bool inverse,
-                          const double2* tw, cudaStream_t st) {
-  return fft_launch_t<double2, double2, double2>(in, out, ri, ro, B, inverse, tw, st);
+                          const FftTables& T, cudaStream_t st) {
+  return fft_launch_t<double2, double2, double2>(in, out, ri, ro, B, inverse, T, st);
 }
 cudaError_t fft_launch_df(const double2* in, float2* out, Rows ri, Rows ro, int B, bool inverse,
-                          const double2* tw, cudaStream_t st) {
-  return fft_launch_t<double2, float2, double2>(in, out, ri, ro, B, inverse, tw, st);
+                          const FftTables& T, cudaStream_t st) {
+  return fft_launch_t<double2, float2, double2>(in, out, ri, ro, B, inverse, T, st);
 }
 
 }  // namespace jtfs

@@ -7,16 +7,28 @@
 #include "common.cuh"
 
 namespace jtfs {
+// Device twiddle tables: the 4096-entry W_4096^e tables (float, double) and, per length 2^lg > 4096, the
+// two-level four-step tables W_L^e = lo[e & 4095] * hi[e >> 12].
+struct FftTables {
+  const float2* tw = nullptr;
+  const double2* twd = nullptr;
+  const float2* lo_f[23] = {};
+  const float2* hi_f[23] = {};
+  const double2* lo_d[23] = {};
+  const double2* hi_d[23] = {};
+};
 // Out-of-place batched C2C FFT of B x ri.count rows of length ri.L (power of two, 2..2^22).
 // For L > 4096 the input rows are clobbered (four-step scheme runs its first step in place).
-// `tw` = device twiddle table (fft_twiddle_table / _d). Inverse includes the 1/L factor.
-cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse,
-                       const float2* tw, cudaStream_t st);
+// Inverse includes the 1/L factor.
+cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,
+                       cudaStream_t st);
 // float64 compute: double -> double, double -> float (output rounded to complex64)
 cudaError_t fft_launch_dd(const double2* in, double2* out, Rows ri, Rows ro, int B, bool inverse,
-                          const double2* tw, cudaStream_t st);
+                          const FftTables& T, cudaStream_t st);
 cudaError_t fft_launch_df(const double2* in, float2* out, Rows ri, Rows ro, int B, bool inverse,
-                          const double2* tw, cudaStream_t st);
+                          const FftTables& T, cudaStream_t st);
 std::vector<float2> fft_twiddle_table();
 std::vector<double2> fft_twiddle_table_d();
+void fft_fourstep_tables_f(int lgL, std::vector<float2>* lo, std::vector<float2>* hi);
+void fft_fourstep_tables_d(int lgL, std::vector<double2>* lo, std::vector<double2>* hi);
 }  // namespace jtfs

@@ -150,6 +150,8 @@ static void free_tables(DeviceTables* d) {
     if (d->fwd_ulist[c]) cudaFree(d->fwd_ulist[c]);
     if (d->fwd_tiles[c]) cudaFree(d->fwd_tiles[c]);
   }
+  for (void* q : d->fs_bufs)
+    if (q) cudaFree(q);
   for (auto& c : d->tc) {
     if (c.blocks) cudaFree(c.blocks);
     if (c.tiles) cudaFree(c.tiles);
@@ -309,6 +311,23 @@ static cudaError_t upload(Plan& p) {
   UP(tw, tw);
   std::vector<double2> twd = fft_twiddle_table_d();
   UP(twd, twd);
+  d->fftt.tw = d->tw;
+  d->fftt.twd = d->twd;
+  for (int lg = 13; lg <= 22 && (int64_t(1) << lg) <= p.N_pad; ++lg) {
+    std::vector<float2> lf, hf;
+    std::vector<double2> ld, hd;
+    fft_fourstep_tables_f(lg, &lf, &hf);
+    fft_fourstep_tables_d(lg, &ld, &hd);
+    float2 *a = nullptr, *b2 = nullptr;
+    double2 *c = nullptr, *e2 = nullptr;
+    if ((e = up(lf, &a)) != cudaSuccess || (e = up(hf, &b2)) != cudaSuccess || (e = up(ld, &c)) != cudaSuccess ||
+        (e = up(hd, &e2)) != cudaSuccess) {
+      free_tables(d);
+      return e;
+    }
+    d->fs_bufs.insert(d->fs_bufs.end(), {(void*)a, (void*)b2, (void*)c, (void*)e2});
+    d->fftt.lo_f[lg] = a; d->fftt.hi_f[lg] = b2; d->fftt.lo_d[lg] = c; d->fftt.hi_d[lg] = e2;
+  }
   d->maxLf = (int)p.P;
   // FFT route tables and block lists
   UP(p.fr_spec, fr_spec); UP(p.u_wts, u_wts); UP(p.u_wt_off, u_wt_off);
@@ -406,7 +425,7 @@ static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
 static cudaError_t fft_rows(const Plan& p, const float2* in, int64_t in_sb, float2* out, int64_t out_sb,
                             int64_t off, int64_t count, int64_t L, int B, bool inv, cudaStream_t st) {
   Rows ri{in_sb, off, count, L}, ro{out_sb, off, count, L};
-  return fft_launch(in, out, ri, ro, B, inv, p.dev->tw, st);
+  return fft_launch(in, out, ri, ro, B, inv, p.dev->fftt, st);
 }
 
 // Forward of one micro-batch. stop: 0 = full; 1 = after U1 (in A); 2 = after S1t; 3 = after Y2.
@@ -423,21 +442,21 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   launch_reflect_pad(x, sx, xpd, p, mb, st);
   {
     Rows ri{sd, 0, 1, p.N_pad}, ro{sd, 0, 1, p.N_pad};
-    if ((e = fft_launch_dd(xpd, Xhd, ri, ro, mb, false, d.twd, st))) return e;
+    if ((e = fft_launch_dd(xpd, Xhd, ri, ro, mb, false, d.fftt, st))) return e;
   }
   // A2: layer 1: cdgmm + subsample_fourier (float64), ifft (float64 -> complex64 Z1),
   // modulus, fft (complex64)
   launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals, mb, st);
   for (auto& g : p.l1_groups) {
     Rows ri{sAd, g.off, g.count, g.L}, ro{w.s_L1, g.off, g.count, g.L};
-    if ((e = fft_launch_df(Ad, w.Z1, ri, ro, mb, true, d.twd, st))) return e;
+    if ((e = fft_launch_df(Ad, w.Z1, ri, ro, mb, true, d.fftt, st))) return e;
   }
   launch_modulus(w.Z1, w.s_L1, w.A, w.s_A, p.sumL1, mb, st);  // A rows use the L1 layout
   RET();
   if (stop == 1) return cudaSuccess;
   for (auto& g : p.l1_groups) {
     Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_L1, g.off, g.count, g.L};
-    if ((e = fft_launch(w.A, w.U1h, ri, ro, mb, false, d.tw, st))) return e;
+    if ((e = fft_launch(w.A, w.U1h, ri, ro, mb, false, d.fftt, st))) return e;
   }
   // S0 and S1 time averages (Eq.3 time part)
   launch_gather_df(Xhd, sd, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
@@ -454,7 +473,7 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     launch_gather(w.U1h, w.s_L1, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st);
     for (auto& g : p.y2_groups) {
       Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
-      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, true, d.tw, st))) return e;
+      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, true, d.fftt, st))) return e;
     }
     RET();
     if (stop == 3) return cudaSuccess;
@@ -495,7 +514,7 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     // FFT of g_Y2 rows -> G_Y (into Y2)
     for (auto& g : p.y2_groups) {
       Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
-      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, false, d.tw, st))) return e;
+      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, false, d.fftt, st))) return e;
     }
   }
   // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)
@@ -506,13 +525,13 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
   launch_adj_gather_u1(p, d, w.ct, w.s_c, w.Y2, w.s_Y2, w.U1h, w.s_L1, mb, st);
   for (auto& g : p.l1_groups) {
     Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
-    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, true, d.tw, st))) return e;
+    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, true, d.fftt, st))) return e;
   }
   // A9: modulus adjoint, FFT, layer-1 adjoint gather, IFFT, reflect adjoint
   launch_phase_mul(w.Z1, w.A, w.s_A, w.U1h, p.sumL1, w.s_L1, w.thr, mb, st);  // Z1, U1h share the L1 stride
   for (auto& g : p.l1_groups) {
     Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
-    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, false, d.tw, st))) return e;
+    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, false, d.fftt, st))) return e;
   }
   launch_adj_gather_x(p, d, w.A, w.s_A, w.Xh, w.s_xp, mb, st);
   if ((e = fft_rows(p, w.Xh, w.s_xp, w.xp, w.s_xp, 0, 1, p.N_pad, mb, true, st))) return e;
