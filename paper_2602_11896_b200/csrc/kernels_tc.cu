@@ -347,10 +347,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   const int b = blockIdx.y;
   const int K = TB.K, K2 = TB.K2, kcw = TB.kcw, kB2c = TB.kb2;
   const int N2 = ((2 * K + 15) / 16) * 16;
-  const int nab = N2 <= 128 ? 2 : 1;                   // A2 buffers in TMEM (double when D2 leaves room)
-  float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2]
+  int nab, ta;                                         // A2 buffers; Y2 tile in TMEM (GEMM1 TS form)
+  tc_bwd_mode(K, K2, &nab, &ta);
+  float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2] (SMEM mode only)
   float* a_lo = a_hi + 128 * K2;
-  float* bst1 = a_lo + 128 * K2;                        // ring 1 (GEMM1 B images): NS1 x STG1 floats
+  float* bst1 = ta ? a_hi : a_lo + 128 * K2;            // ring 1 (GEMM1 B images): NS1 x STG1 floats
   float* bst2 = bst1 + NS1 * STG1;                      // ring 2 (GEMM2 B2 images): NS2 x STG2 floats
 
   if (tid == 0) {
@@ -362,16 +363,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, 512);
-  build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kTcThreads);
+  if (!ta) build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kTcThreads);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   // TMEM columns: D1 buffers [0,64) [64,128); A2 buffer j: hi [128+128j, +64), lo [192+128j, +64);
-  // D2 [128+128 nab, +N2)
+  // D2 [128+128 nab, +N2); TMEM mode: A hi [D2 end, +K2), A lo [+K2, +K2)
   const uint32_t tbase = tmem_base;
   const uint32_t ta2 = tbase + 128;
   const uint32_t d2 = tbase + 128 + 128 * (uint32_t)nab;
+  const uint32_t taa_hi = d2 + (uint32_t)N2, taa_lo = taa_hi + (uint32_t)K2;
+  if (ta && warp >= 4 && warp < 8) {
+    // Y2 tile -> tf32 hi/lo rows of TMEM (lane = time column, column = k' = 2n + re/im)
+    const uint32_t lq = (uint32_t)((warp & 3) * 32) << 16;
+    const int64_t col = col0 + (warp & 3) * 32 + lane;
+    const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off + (bf.c_lo + (col < bf.n_cols ? col : 0)) % bf.T2;
+    for (int k0 = 0; k0 < K2; k0 += 16) {
+      float hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = k0 / 2 + j;
+        float2 v = make_float2(0.f, 0.f);
+        if (n < K && col < bf.n_cols) v = ysrc[(int64_t)n * bf.T2];
+        tc::split_tf32(v.x, hi[2 * j], lo[2 * j]);
+        tc::split_tf32(v.y, hi[2 * j + 1], lo[2 * j + 1]);
+      }
+      if (K2 - k0 >= 16) {
+        tc::tmem_st16(taa_hi + lq + (uint32_t)k0, hi);
+        tc::tmem_st16(taa_lo + lq + (uint32_t)k0, lo);
+      } else {
+        tc::tmem_st8(taa_hi + lq + (uint32_t)k0, hi);
+        tc::tmem_st8(taa_lo + lq + (uint32_t)k0, lo);
+      }
+    }
+    tc::tmem_wait_st();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
   const int nchunks = (K2 + kcw - 1) / kcw;
 
   if (warp == 0 || warp == 2) {
@@ -424,8 +454,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer
+  } else if (warp == 1 || warp == 3) {
+    // ===================== MMA issuers: warp 1 GEMM1 (recompute W), warp 3 GEMM2 (g_Y2^T accumulation).
+    // Two issuing threads keep the tensor pipe fed: GEMM1 of later tiles queues while GEMM2 waits for
+    // the epilogue's A2 or its B2 chunk (tcgen05.commit tracks each thread's own MMAs).
     const uint32_t idesc1 = tc::idesc_tf32(128, kBwN1);
     const uint32_t idesc2 = tc::idesc_tf32(128, (uint32_t)N2);
     const uint32_t sboA = (uint32_t)K2 * 32u;
@@ -452,9 +484,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         if (tc::elect_one()) {
           for (int ks = 0; ks < kc / 8; ++ks) {
             const uint32_t kg = (uint32_t)(ch * (kcw / 8) + ks);
-            tc::mma_tf32(d, dA_hi + 16u * kg, dbh + 16u * ks, idesc1, (ch > 0 || ks > 0) ? 1u : 0u);
-            tc::mma_tf32(d, dA_hi + 16u * kg, dbl + 16u * ks, idesc1, 1u);
-            tc::mma_tf32(d, dA_lo + 16u * kg, dbh + 16u * ks, idesc1, 1u);
+            if (ta) {
+              tc::mma_tf32_ts(d, taa_hi + 8u * kg, dbh + 16u * ks, idesc1, (ch > 0 || ks > 0) ? 1u : 0u);
+              tc::mma_tf32_ts(d, taa_hi + 8u * kg, dbl + 16u * ks, idesc1, 1u);
+              tc::mma_tf32_ts(d, taa_lo + 8u * kg, dbh + 16u * ks, idesc1, 1u);
+            } else {
+              tc::mma_tf32(d, dA_hi + 16u * kg, dbh + 16u * ks, idesc1, (ch > 0 || ks > 0) ? 1u : 0u);
+              tc::mma_tf32(d, dA_hi + 16u * kg, dbl + 16u * ks, idesc1, 1u);
+              tc::mma_tf32(d, dA_lo + 16u * kg, dbh + 16u * ks, idesc1, 1u);
+            }
           }
           tc::mma_commit(&empty1[stage1]);
           if (ch == nchunks - 1) tc::mma_commit(&tfull[buf]);
@@ -506,13 +544,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       if (u % a.n_shards != a.shard) continue;
       G += (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
     }
-    if (G > 0) gemm1();
-    for (int g = 0; g < G; ++g) {
-      if (g + 1 < G) gemm1();
-      gemm2();
+    if (warp == 1) {
+      for (int g = 0; g < G; ++g) gemm1();
+    } else {
+      for (int g = 0; g < G; ++g) gemm2();
+      if (tc::elect_one()) tc::mma_commit(&d2full);
+      __syncwarp();
     }
-    if (tc::elect_one()) tc::mma_commit(&d2full);
-    __syncwarp();
   } else if (warp >= 4) {
     // ===================== epilogue
     const int e = warp - 4;
@@ -624,9 +662,12 @@ void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2
   const int N2 = ((2 * K + 15) / 16) * 16;
   *STG1 = 2 * kBwN1 * kcw;
   *STG2 = 2 * N2 * kb2;
-  const long avail = 224L * 1024 - 1024 - (long)2 * 128 * K2 * 4;
-  // ring 2 holds up to two tiles of B2 chunks (GEMM2 runs a tile behind GEMM1), ring 1 the rest
-  int n2 = std::min(kTcMaxStages2, std::max(2, 128 / kb2));
+  int nab, ta;
+  tc_bwd_mode(K, K2, &nab, &ta);
+  const long avail = 224L * 1024 - 1024 - (ta ? 0L : (long)2 * 128 * K2 * 4);
+  // ring 2 holds up to three tiles of B2 chunks (GEMM2 runs a tile behind GEMM1 and a B2 tile takes
+  // ~2 us to land from L2), ring 1 the rest
+  int n2 = std::min(kTcMaxStages2, std::max(3, 192 / kb2));
   while (n2 > 2 && avail - (long)n2 * *STG2 * 4 < 2L * *STG1 * 4) --n2;
   *NS2 = n2;
   *NS1 = (int)std::min<long>(kTcMaxStages, (avail - (long)n2 * *STG2 * 4) / (*STG1 * 4));
@@ -641,7 +682,9 @@ template <int KAP>
 static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream_t st) {
   int NS1, NS2, STG1, STG2;
   tc_bwd_rings(C.Kmax, C.K2max, C.kcw, C.kb2, &NS1, &STG1, &NS2, &STG2);
-  const size_t sm = (size_t)(2 * 128 * C.K2max + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
+  int nab, ta;
+  tc_bwd_mode(C.Kmax, C.K2max, &nab, &ta);
+  const size_t sm = (size_t)((ta ? 0 : 2 * 128 * C.K2max) + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)C.ntiles, (unsigned)B);
   k_joint_bwd_tc<KAP><<<g, kTcThreads, sm, st>>>(a, NS1, STG1, NS2, STG2);

@@ -67,6 +67,18 @@ struct TcBlock {
 };
 // forward classes 3*ct_kind + kap_kind (ct_kind: 0 = 2 column tiles, 1 = 1 tile kcw 32,
 // 2 = 1 tile kcw 16; kap_kind: rows_out <= 2, 4, 8); backward classes 3*(kcw == 16) + kap_kind
+// backward TMEM plan (kernels_tc.cu): A2 double-buffered (nab = 2) when D2 leaves room; the Y2 tile A in
+// TMEM (ta = 1, GEMM1 in the TS form) when D1 + A2 + D2 + A_hi + A_lo fit in 512 columns.
+inline
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+void tc_bwd_mode(int K, int K2, int* nab, int* ta) {
+  const int N2 = ((2 * K + 15) / 16) * 16;
+  if (N2 <= 128 && 384 + N2 + 2 * K2 <= 512) { *nab = 2; *ta = 1; }
+  else if (256 + N2 + 2 * K2 <= 512) { *nab = 1; *ta = 1; }
+  else { *nab = N2 <= 128 ? 2 : 1; *ta = 0; }
+}
 // backward B ring sizing shared by the planner (chooses kb2) and the launcher (kernels_tc.cu)
 void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2, int* STG2);
 int tc_fwd_stages(int CT, int KAP, int K2, int kcw);

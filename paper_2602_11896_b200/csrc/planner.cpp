@@ -184,7 +184,7 @@ static void build_tc_tables(Plan* p) {
     for (int w : {64, 32, 16, 8}) {
       int ns1, s1, ns2, s2;
       tc_bwd_rings(K, K2, kcw, w, &ns1, &s1, &ns2, &s2);
-      if (ns1 >= 2 && ns2 * w >= 64 + w) { kb2 = w; break; }
+      if (ns1 >= 2 && ns2 * w >= 128 + w) { kb2 = w; break; }
     }
     p->tc_blocks.push_back({(int32_t)bi, K, K2, 3 * ctk + kap, kcw, kb2});
     int ns1, s1, ns2, s2;
