@@ -39,6 +39,9 @@ constexpr int kTcThreads = 384;     // 12 warps
 constexpr int kTcMaxStages = 8;
 constexpr int kTcMaxStages2 = 16;   // backward ring 2 (B2 chunks)
 constexpr int kBwRows = 32;         // rows per backward tile (GEMM1 N = 64, GEMM2 K = 64)
+constexpr int kBwEpiWarps = 16;     // backward epilogue warps: 4 TMEM lane quadrants x 4 row groups
+constexpr int kBwRpw = kBwRows / (kBwEpiWarps / 4);            // rows per epilogue warp (8)
+constexpr int kBwThreads = 128 + 32 * kBwEpiWarps;             // + producers / MMA issuers (warps 0-3)
 constexpr int kBwN1 = 2 * kBwRows;
 
 __device__ __forceinline__ int find_tc(const int64_t* __restrict__ tiles, int n, int64_t t) {
@@ -334,7 +337,7 @@ struct TcBwArgs {
 #endif
 
 template <int KAP>
-__global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS1, int STG1, int NS2, int STG2) {
+__global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS1, int STG1, int NS2, int STG2) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t full1[kTcMaxStages], empty1[kTcMaxStages], full2[kTcMaxStages2], empty2[kTcMaxStages2];
   __shared__ uint64_t tfull[2], tempty[2], a2full[2], a2empty[2], d2full;
@@ -357,13 +360,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   if (tid == 0) {
     for (int s = 0; s < NS1; ++s) { tc::mbar_init(&full1[s], 1); tc::mbar_init(&empty1[s], 1); }
     for (int s = 0; s < NS2; ++s) { tc::mbar_init(&full2[s], 1); tc::mbar_init(&empty2[s], 1); }
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&a2full[s], 8); tc::mbar_init(&a2empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], kBwEpiWarps); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&a2full[s], kBwEpiWarps); tc::mbar_init(&a2empty[s], 1); }
     tc::mbar_init(&d2full, 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, 512);
-  if (!ta) build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kTcThreads);
+  if (!ta) build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kBwThreads);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -552,9 +555,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       __syncwarp();
     }
   } else if (warp >= 4) {
-    // ===================== epilogue
+    // ===================== epilogue: warp (q, h) owns TMEM lane quadrant q and rows h*8 .. h*8+7 of a tile
     const int e = warp - 4;
-    const int q = e & 3, h = e >> 2;        // lane quadrant, row half (16 rows)
+    const int q = e & 3, h = e >> 2;
     const int c = q * 32 + lane;
     const int64_t colg = col0 + c;
     const float th2 = fmaxf(a.thr[b] * a.thr[b], 1.17549435e-38f);   // R22 dead zone (and |w|^2 > FLT_MIN)
@@ -562,44 +565,64 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     int buf = 0;
     uint32_t bph = 0;
     int g = 0;
-    for (int f = 0; f < a.nfr; ++f) {
-      const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard) continue;
+    // phi_F weights and g_o are prefetched one tile ahead (their L2 latency would otherwise sit on the
+    // epilogue's critical path every tile)
+    auto next_unit = [&](int f) {
+      while (f < a.nfr && (TB.bi * a.nfr + f) % a.n_shards != a.shard) ++f;
+      return f;
+    };
+    auto load_w = [&](int u, int t, float* wl) {
       const JointUnit U = a.units[u];
       const TcUnit tu = a.tcu[u];
-      const int ro = U.rows_out;
       const float* wt = a.wts + tu.wt_off;
       const int ldw = tu.NT * kTcRows;
-      float gor[KAP];
 #pragma unroll
       for (int r = 0; r < KAP; ++r)
-        gor[r] = (r < ro && colg < bf.n_cols) ? a.go[b * a.go_sb + U.o_off + (int64_t)r * bf.n_cols + colg] : 0.f;
+        wl[r] = (r < U.rows_out && lane < kBwRpw) ? __ldg(wt + r * ldw + t * kBwRows + h * kBwRpw + lane) : 0.f;
+    };
+    auto load_go = [&](int u, float* gor) {
+      const JointUnit U = a.units[u];
+#pragma unroll
+      for (int r = 0; r < KAP; ++r)
+        gor[r] = (r < U.rows_out && colg < bf.n_cols) ? a.go[b * a.go_sb + U.o_off + (int64_t)r * bf.n_cols + colg]
+                                                       : 0.f;
+    };
+    int f = next_unit(0);
+    float wl_n[KAP], gor_n[KAP];
+    if (f < a.nfr) { load_w(TB.bi * a.nfr + f, 0, wl_n); load_go(TB.bi * a.nfr + f, gor_n); }
+    for (; f < a.nfr;) {
+      const int u = TB.bi * a.nfr + f;
+      const JointUnit U = a.units[u];
+      float gor[KAP];
+#pragma unroll
+      for (int r = 0; r < KAP; ++r) gor[r] = gor_n[r];
       const int NT32 = (int)((U.n_rows + kBwRows - 1) / kBwRows);
+      const int fn = next_unit(f + 1);
       for (int t = 0; t < NT32; ++t, ++g) {
-        // lanes 0..15 hold the weights of rows t*32 + h*16 + lane
         float wl[KAP];
 #pragma unroll
-        for (int r = 0; r < KAP; ++r)
-          wl[r] = (r < ro && lane < 16) ? __ldg(wt + r * ldw + t * kBwRows + h * 16 + lane) : 0.f;
+        for (int r = 0; r < KAP; ++r) wl[r] = wl_n[r];
+        if (t + 1 < NT32) load_w(u, t + 1, wl_n);
+        else if (fn < a.nfr) { load_w(TB.bi * a.nfr + fn, 0, wl_n); load_go(TB.bi * a.nfr + fn, gor_n); }
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
         if (warp == 4 && lane == 0) TC_TRACE(5, g);
-        float v[32];
-        const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 32);
+        float v[2 * kBwRpw];
+        const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 2 * kBwRpw);
         tc::tmem_ld16_nowait(ta, v);
-        tc::tmem_ld16_nowait(ta + 16, v + 16);
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         if (++buf == 2) { buf = 0; bph ^= 1; }
-        float ghi[32], glo[32];
+        float ghi[2 * kBwRpw], glo[2 * kBwRpw];
         if (a.expt & 1) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ghi[i] = glo[i] = v[i] * 0.f;
+          for (int i = 0; i < 2 * kBwRpw; ++i) ghi[i] = glo[i] = v[i] * 0.f;
         } else
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < kBwRpw; ++i) {
+          // g_W = (W/|W|) Phi_F^T g_o (Eq.4 adjoint, modulus adjoint with the R22 dead zone)
           float gv = 0.f;
 #pragma unroll
           for (int r = 0; r < KAP; ++r) gv = fmaf(__shfl_sync(0xffffffffu, wl[r], i), gor[r], gv);
@@ -616,16 +639,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         tc::mbar_wait(&a2empty[ab], (uint32_t)(((nab == 2 ? (g >> 1) : g) & 1) ^ 1));
         tc::tc_fence_after();
         if (warp == 4 && lane == 0) TC_TRACE(7, g);
-        tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 32), ghi);
-        tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 32 + 16), ghi + 16);
-        tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 32), glo);
-        tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 32 + 16), glo + 16);
+        tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 2 * kBwRpw), ghi);
+        tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 2 * kBwRpw), glo);
         tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&a2full[ab]);
         if (warp == 4 && lane == 0) TC_TRACE(8, g);
       }
+      f = fn;
     }
     // final: D2 (g_Y2^T for this column tile) -> g_Y2[n][col]
     if (g > 0) {
@@ -687,7 +709,7 @@ static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream
   const size_t sm = (size_t)((ta ? 0 : 2 * 128 * C.K2max) + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)C.ntiles, (unsigned)B);
-  k_joint_bwd_tc<KAP><<<g, kTcThreads, sm, st>>>(a, NS1, STG1, NS2, STG2);
+  k_joint_bwd_tc<KAP><<<g, kBwThreads, sm, st>>>(a, NS1, STG1, NS2, STG2);
   count_launch();
 }
 
