@@ -18,6 +18,7 @@ struct TcClass {
   int64_t ntiles = 0;
   int K2max = 0, Kmax = 0, kcw = 32, kb2 = 8;
   int cls = 0;                     // kernel variant (TcBlock::cls)
+  int ks = 0, nparts = 1;          // split-K block: K parts of the forward
 };
 
 struct FfList {                    // blocks on the FFT route of the joint stage + column-tile prefix
@@ -133,11 +134,13 @@ void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
                      int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);
 // the per-block launches go round-robin over the ns streams ss (forked from and joined to the caller's)
+// split-K blocks accumulate W in wbuf (per-signal stride wb_sb) and leave it there when keep_w (backward)
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, int shard, int n_shards, int B, const cudaStream_t* ss, int ns);
+                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, int shard, int n_shards, int B,
+                         const cudaStream_t* ss, int ns);
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                         int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
-                         int B, const cudaStream_t* ss, int ns);
+                         int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
+                         const float* thr, int shard, int n_shards, int B, const cudaStream_t* ss, int ns);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st);

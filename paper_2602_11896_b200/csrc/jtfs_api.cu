@@ -235,7 +235,9 @@ static cudaError_t upload(Plan& p) {
       std::vector<TcBlock> bl{tb};
       std::vector<int64_t> tt{0, (p.binfo[tb.bi].n_cols + 128 * CT - 1) / (128 * CT)};
       c.n_blocks = 1;
-      c.K2max = tb.K2;
+      c.K2max = (fwd && tb.ks) ? tb.kpw : tb.K2;
+      c.ks = tb.ks;
+      c.nparts = tb.nparts;
       c.Kmax = tb.K;
       c.kcw = tb.kcw;
       c.kb2 = tb.kb2;
@@ -371,9 +373,9 @@ static jtfs_status ensure_device(jtfs_plan_s* h) {
 // ------------------------------------------------------------------------------ workspace layout
 struct Layout {
   // per-signal sizes in bytes (each 256-aligned) of every buffer, in this order
-  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss, thr;
+  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss, thr, Wk;
   size_t per_signal() const {
-    return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss + thr;
+    return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss + thr + Wk;
   }
 };
 static size_t al(size_t b) { return (b + 255) / 256 * 256; }
@@ -396,14 +398,15 @@ static Layout layout(const Plan& p, int with_grad) {
   L.g = with_grad ? al(p.N * 4) : 0;
   L.loss = 256;
   L.thr = 256;
+  L.Wk = al(std::max<int64_t>(p.ks_w_floats, 1) * 4);   // split-K blocks: complex W of every cell
   return L;
 }
 
 struct Bufs {
   float2 *xp, *Xh, *A, *Z1, *U1h, *Y2, *cs, *ct, *W1;
-  float *S1t, *V2, *o, *S, *r, *gS1t, *g, *loss, *thr;
+  float *S1t, *V2, *o, *S, *r, *gS1t, *g, *loss, *thr, *Wk;
   // per-signal strides in elements
-  int64_t s_xp, s_A, s_L1, s_Y2, s_c, s_S1t, s_W1, s_V2, s_o, s_S, s_g;
+  int64_t s_xp, s_A, s_L1, s_Y2, s_c, s_S1t, s_W1, s_V2, s_o, s_S, s_g, s_Wk;
 };
 static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
   Bufs b{};
@@ -415,9 +418,11 @@ static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
   b.S = (float*)take(L.S); b.r = (float*)take(L.r); b.gS1t = (float*)take(L.gS1t); b.g = (float*)take(L.g);
   b.loss = (float*)take(L.loss);
   b.thr = (float*)take(L.thr);   // one float per signal (mb contiguous floats at the start)
+  b.Wk = (float*)take(L.Wk);
   // strides in complex64 units (complex128 views: half)
   b.s_xp = L.xp / 8; b.s_A = L.A / 8; b.s_L1 = L.Z1 / 8; b.s_Y2 = L.Y2 / 8; b.s_c = L.cs / 8;
   b.s_S1t = L.S1t / 4; b.s_W1 = L.W1 / 8; b.s_V2 = L.V2 / 4; b.s_o = L.o / 4; b.s_S = L.S / 4; b.s_g = L.g / 4;
+  b.s_Wk = L.Wk / 4;
   (void)p;
   return b;
 }
@@ -430,7 +435,8 @@ static cudaError_t fft_rows(const Plan& p, const float2* in, int64_t in_sb, floa
 
 // Forward of one micro-batch. stop: 0 = full; 1 = after U1 (in A); 2 = after S1t; 3 = after Y2.
 static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb, float* S, int64_t S_sb,
-                               const Bufs& w, int shard, int n_shards, cudaStream_t st, int stop = 0) {
+                               const Bufs& w, int shard, int n_shards, cudaStream_t st, int stop = 0,
+                               bool keep_w = false) {
   const DeviceTables& d = *p.dev;
   cudaError_t e;
 #define RET() if ((e = cudaGetLastError()) != cudaSuccess) return e
@@ -482,7 +488,8 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     Fanout* fo = fanout_get();
     fan_fork(fo, st);
     launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, shard, n_shards, mb, fo->s[0]);
-    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, fo->s + 1, kFanStreams - 1);
+    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.Wk, w.s_Wk, keep_w, shard, n_shards, mb, fo->s + 1,
+                        kFanStreams - 1);
     launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, fo->s[0]);
     fan_join(fo, st);
     prof_end(st, 0);
@@ -506,7 +513,7 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     Fanout* fo = fanout_get();
     fan_fork(fo, st);
     launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
-    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s + 1,
+    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.Wk, w.s_Wk, w.thr, shard, n_shards, mb, fo->s + 1,
                         kFanStreams - 1);
     launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
     fan_join(fo, st);
@@ -746,7 +753,7 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
   Bufs w = carve(p, L, (char*)ws, mb);
   for (int64_t b0 = 0; b0 < B; b0 += mb) {
     int n = (int)std::min<int64_t>(mb, B - b0);
-    CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, shard, n_shards, st));
+    CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, shard, n_shards, st, 0, true));
     float* lossp = mstate ? mstate->loss + b0 : loss + b0;
     launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, shard, n_shards, n, st);
     launch_absmax(y + b0 * p.N, p.N, kModTau, w.thr, n, st);

@@ -53,15 +53,16 @@ __device__ __forceinline__ int find_tc(const int64_t* __restrict__ tiles, int n,
   return lo;
 }
 
-// A tile: Y2[n][col0 + c] -> tf32 hi/lo, canonical K-major [128][K2], k' = 2n + (re, im)
+// A tile: Y2[n0 + n][col0 + c] -> tf32 hi/lo, canonical K-major [128][K2], k' = 2n + (re, im)
 __device__ __forceinline__ void build_a(float* a_hi, float* a_lo, const float2* __restrict__ ysrc,
-                                        const BlockInfo& bf, int64_t col0, int K, int K2, int tid, int nthr) {
+                                        const BlockInfo& bf, int64_t col0, int K, int K2, int tid, int nthr,
+                                        int n0 = 0) {
   for (int idx = tid; idx < 128 * (K2 / 2); idx += nthr) {
     const int c = idx & 127;
     const int n = idx >> 7;
     const int64_t col = col0 + c;
     float2 v = make_float2(0.f, 0.f);
-    if (n < K && col < bf.n_cols) v = ysrc[(int64_t)n * bf.T2 + (bf.c_lo + col) % bf.T2];
+    if (n0 + n < K && col < bf.n_cols) v = ysrc[(int64_t)(n0 + n) * bf.T2 + (bf.c_lo + col) % bf.T2];
     float h0, l0, h1, l1;
     tc::split_tf32(v.x, h0, l0);
     tc::split_tf32(v.y, h1, l1);
@@ -80,7 +81,10 @@ struct TcArgs {
   const float* wts;                 // phi_F weights [unit][rho][NT*64]
   const TcUnit* tcu;                // per unit image / weight offsets
   int nfr, shard, n_shards;
+  float* wbuf; int64_t wb_sb;       // split-K blocks: per-signal W buffer
+  int part, pmode;                  // K part of this launch; kPm* bits
 };
+constexpr int kPmLoad = 1, kPmStore = 2, kPmFinish = 4;
 
 // =====================================================================================
 // forward
@@ -96,7 +100,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   const BlockInfo bf = a.binfo[TB.bi];
   const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)(128 * CT);
   const int b = blockIdx.y;
-  const int K = TB.K, K2 = TB.K2, kcw = TB.kcw;
+  const int K = TB.K, kcw = TB.kcw;
+  const int kp_lo = TB.ks ? a.part * TB.kpw : 0;            // k' range of this launch (split-K blocks)
+  const int K2 = TB.ks ? min(TB.kpw, TB.K2 - kp_lo) : TB.K2;
+  const int pmode = TB.ks ? a.pmode : kPmFinish;
   float* a_hi = reinterpret_cast<float*>(sm);              // [CT][128][K2] canonical
   float* a_lo = a_hi + CT * 128 * K2;
   float* bst = a_lo + CT * 128 * K2;                        // NS stages x STG floats
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   if (warp == 1) tc::tmem_alloc(&tmem_base, CT == 1 ? 256 : 512);
   const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off;
   for (int m = 0; m < CT; ++m)
-    build_a(a_hi + m * 128 * K2, a_lo + m * 128 * K2, ysrc, bf, col0 + m * 128, K, K2, tid, kTcThreads);
+    build_a(a_hi + m * 128 * K2, a_lo + m * 128 * K2, ysrc, bf, col0 + m * 128, K, K2, tid, kTcThreads, kp_lo / 2);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -126,8 +133,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
       const int u = TB.bi * a.nfr + f;
       if (u % a.n_shards != a.shard) continue;
       const TcUnit tu = a.tcu[u];
-      const float* src = a.img + tu.img_off;
       for (int t = 0; t < tu.NT; ++t) {
+        // row tile t of the unit's image: chunks of the full K2, starting at this launch's k' range
+        const float* src = a.img + tu.img_off + (int64_t)t * (2 * kTcN * TB.K2) + 2 * kTcN * kp_lo;
         for (int ch = 0; ch < nchunks; ++ch) {
           const int kc = min(kcw, K2 - ch * kcw);
           const uint32_t bytes = (uint32_t)(2 * kTcN * kc * 4);
@@ -226,6 +234,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
           tc::tmem_ld16_nowait(ta + 32, v + 32);
           tc::tmem_ld16_nowait(ta + 48, v + 48);
           tc::tmem_wait_ld();
+          if (pmode != kPmFinish) {
+            // split-K: W of (tile t, column c, rows h*32 ..) accumulated across the K parts
+            float4* wp = reinterpret_cast<float4*>(
+                a.wbuf + b * a.wb_sb + TB.wp_off +
+                (((int64_t)(blockIdx.x - a.tiles[jb]) * TB.wp_tiles + tu.wp_tile0 + t) * 128 + c) * 128 + h * 64);
+            if (pmode & kPmLoad) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float4 w = wp[i];
+                v[4 * i] += w.x; v[4 * i + 1] += w.y; v[4 * i + 2] += w.z; v[4 * i + 3] += w.w;
+              }
+            }
+            if (pmode & kPmStore) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) wp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+            if (!(pmode & kPmFinish)) continue;
+          }
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float mod = tc::sqrt_approx(fmaf(v[2 * i], v[2 * i], v[2 * i + 1] * v[2 * i + 1]));
@@ -238,6 +264,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         if (++buf == 2) { buf = 0; bph ^= 1; }
       }
+      if (!(pmode & kPmFinish)) continue;
       // combine the two row halves in a fixed order, write o[rho][col]
       if (h == 1) {
 #pragma unroll
@@ -290,21 +317,32 @@ static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st)
 }
 
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, int shard, int n_shards, int B, const cudaStream_t* ss, int ns) {
+                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, int shard, int n_shards, int B,
+                         const cudaStream_t* ss, int ns) {
   int li = 0;
   for (const TcClass& C : d.tc) {
     const cudaStream_t st = ss[li++ % ns];
     if (C.n_blocks == 0) continue;
-    TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
-             (int)p.L_fr.size(), shard, n_shards};
-    // class = 3 * ct_kind + kap_kind; ct_kind 0: CT=2 (K2<=64), 1: CT=1 kcw 32, 2: CT=1 kcw 16
-    switch (C.cls) {
-      case 0: launch_tc<2, 2>(a, C, B, st); break;
-      case 1: launch_tc<2, 4>(a, C, B, st); break;
-      case 2: launch_tc<2, 8>(a, C, B, st); break;
-      case 3: case 6: launch_tc<1, 2>(a, C, B, st); break;
-      case 4: case 7: launch_tc<1, 4>(a, C, B, st); break;
-      case 5: case 8: launch_tc<1, 8>(a, C, B, st); break;
+    const int nparts = C.ks ? C.nparts : 1;
+    for (int part = 0; part < nparts; ++part) {   // split-K parts run in order on one stream
+      int pmode = kPmFinish;
+      if (C.ks) {
+        pmode = (part > 0 ? kPmLoad : 0) | (part < nparts - 1 || keep_w ? kPmStore : 0) |
+                (part == nparts - 1 ? kPmFinish : 0);
+      }
+      TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
+               (int)p.L_fr.size(), shard, n_shards, wbuf, wb_sb, part, pmode};
+      // class = 8 * ct_kind + kap_kind (CT = 2 for ct_kind 0)
+      switch (C.cls) {
+        case 0: launch_tc<2, 2>(a, C, B, st); break;
+        case 1: launch_tc<2, 4>(a, C, B, st); break;
+        case 2: launch_tc<2, 8>(a, C, B, st); break;
+        case 8: launch_tc<1, 2>(a, C, B, st); break;
+        case 9: launch_tc<1, 4>(a, C, B, st); break;
+        case 10: launch_tc<1, 8>(a, C, B, st); break;
+        case 11: launch_tc<1, 16>(a, C, B, st); break;
+        case 12: launch_tc<1, 32>(a, C, B, st); break;
+      }
     }
   }
 }
@@ -325,6 +363,7 @@ struct TcBwArgs {
   int nfr, shard, n_shards;
   const float* thr;
   int expt;                         // timing experiments only (JTFS_TC_EXPT); 0 in production
+  const float* wbuf; int64_t wb_sb; // split-K blocks: W left by the forward (GEMM1 skipped)
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
 };
 #ifdef JTFS_TC_TRACE
@@ -350,11 +389,13 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   const int b = blockIdx.y;
   const int K = TB.K, K2 = TB.K2, kcw = TB.kcw, kB2c = TB.kb2;
   const int N2 = ((2 * K + 15) / 16) * 16;
+  const bool ksm = TB.ks != 0;                         // split-K block: W from the forward, no GEMM1
   int nab, ta;                                         // A2 buffers; Y2 tile in TMEM (GEMM1 TS form)
-  tc_bwd_mode(K, K2, &nab, &ta);
+  if (ksm) { nab = N2 <= 256 ? 2 : 1; ta = 0; }
+  else tc_bwd_mode(K, K2, &nab, &ta);
   float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2] (SMEM mode only)
   float* a_lo = a_hi + 128 * K2;
-  float* bst1 = ta ? a_hi : a_lo + 128 * K2;            // ring 1 (GEMM1 B images): NS1 x STG1 floats
+  float* bst1 = (ta || ksm) ? a_hi : a_lo + 128 * K2;   // ring 1 (GEMM1 B images): NS1 x STG1 floats
   float* bst2 = bst1 + NS1 * STG1;                      // ring 2 (GEMM2 B2 images): NS2 x STG2 floats
 
   if (tid == 0) {
@@ -366,7 +407,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, 512);
-  if (!ta) build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kBwThreads);
+  if (!ta && !ksm) build_a(a_hi, a_lo, a.Y2 + b * a.y_sb + bf.y_off, bf, col0, K, K2, tid, kBwThreads);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -374,8 +415,8 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   // TMEM columns: D1 buffers [0,64) [64,128); A2 buffer j: hi [128+128j, +64), lo [192+128j, +64);
   // D2 [128+128 nab, +N2); TMEM mode: A hi [D2 end, +K2), A lo [+K2, +K2)
   const uint32_t tbase = tmem_base;
-  const uint32_t ta2 = tbase + 128;
-  const uint32_t d2 = tbase + 128 + 128 * (uint32_t)nab;
+  const uint32_t ta2 = tbase + (ksm ? 0u : 128u);       // split-K: no D1
+  const uint32_t d2 = ta2 + 128 * (uint32_t)nab;
   const uint32_t taa_hi = d2 + (uint32_t)N2, taa_lo = taa_hi + (uint32_t)K2;
   if (ta && warp >= 4 && warp < 8) {
     // Y2 tile -> tf32 hi/lo rows of TMEM (lane = time column, column = k' = 2n + re/im)
@@ -413,7 +454,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const bool p1 = warp == 0;
     int stage = 0;
     uint32_t ph = 0;
-    for (int f = 0; f < a.nfr; ++f) {
+    for (int f = 0; f < (p1 && ksm ? 0 : a.nfr); ++f) {   // no GEMM1 (ring 1) in split-K mode
       const int u = TB.bi * a.nfr + f;
       if (u % a.n_shards != a.shard) continue;
       const TcUnit tu = a.tcu[u];
@@ -462,7 +503,10 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     // Two issuing threads keep the tensor pipe fed: GEMM1 of later tiles queues while GEMM2 waits for
     // the epilogue's A2 or its B2 chunk (tcgen05.commit tracks each thread's own MMAs).
     const uint32_t idesc1 = tc::idesc_tf32(128, kBwN1);
-    const uint32_t idesc2 = tc::idesc_tf32(128, (uint32_t)N2);
+    // GEMM2 N = N2 (<= 384): UMMA N <= 256, so wider D2 is covered by two MMAs over row halves of B2
+    const int N2a = N2 > 256 ? ((N2 / 2 + 15) / 16) * 16 : N2;
+    const uint32_t idesc2 = tc::idesc_tf32(128, (uint32_t)N2a);
+    const uint32_t idesc2b = tc::idesc_tf32(128, (uint32_t)(N2 - N2a > 0 ? N2 - N2a : 16));
     const uint32_t sboA = (uint32_t)K2 * 32u;
     const uint64_t dA_hi = tc::sdesc(tc::smem_u32(a_hi), 128, sboA);
     const uint64_t dA_lo = tc::sdesc(tc::smem_u32(a_lo), 128, sboA);
@@ -529,6 +573,13 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
             tc::mma_tf32_ts(d2, ta2_hi + 8u * kg, dbh + 16u * ks, idesc2, (g2 > 0 || kg > 0) ? 1u : 0u);
             tc::mma_tf32_ts(d2, ta2_hi + 8u * kg, dbl + 16u * ks, idesc2, 1u);
             tc::mma_tf32_ts(d2, ta2_lo + 8u * kg, dbh + 16u * ks, idesc2, 1u);
+            if (N2a < N2) {   // rows N2a .. N2-1 of B2 start (N2a / 8) core-matrix groups further
+              const uint64_t o2 = (uint64_t)((N2a / 8) * kB2c * 32) >> 4;
+              const uint32_t d2b = d2 + (uint32_t)N2a;
+              tc::mma_tf32_ts(d2b, ta2_hi + 8u * kg, dbh + o2 + 16u * ks, idesc2b, (g2 > 0 || kg > 0) ? 1u : 0u);
+              tc::mma_tf32_ts(d2b, ta2_hi + 8u * kg, dbl + o2 + 16u * ks, idesc2b, 1u);
+              tc::mma_tf32_ts(d2b, ta2_lo + 8u * kg, dbh + o2 + 16u * ks, idesc2b, 1u);
+            }
           }
           tc::mma_commit(&empty2[stage2]);
           if (ch == 64 / kB2c - 1) tc::mma_commit(&a2empty[ab]);
@@ -548,7 +599,8 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       G += (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
     }
     if (warp == 1) {
-      for (int g = 0; g < G; ++g) gemm1();
+      if (!ksm)
+        for (int g = 0; g < G; ++g) gemm1();
     } else {
       for (int g = 0; g < G; ++g) gemm2();
       if (tc::elect_one()) tc::mma_commit(&d2full);
@@ -587,9 +639,24 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         gor[r] = (r < U.rows_out && colg < bf.n_cols) ? a.go[b * a.go_sb + U.o_off + (int64_t)r * bf.n_cols + colg]
                                                        : 0.f;
     };
+    // split-K mode: W of (tile, column, this warp's 8 rows) from the forward's buffer, one tile ahead
+    const float* wcol = ksm ? a.wbuf + b * a.wb_sb + TB.wp_off +
+                                  (((int64_t)(blockIdx.x - a.tiles[jb]) * TB.wp_tiles) * 128 + c) * 128 + h * 16
+                            : nullptr;
+    auto load_wv = [&](int u, int t32, float4* wv) {
+      const float4* q4 = reinterpret_cast<const float4*>(
+          wcol + ((int64_t)(a.tcu[u].wp_tile0 + (t32 >> 1)) * 128) * 128 + (t32 & 1) * 64);
+#pragma unroll
+      for (int i = 0; i < kBwRpw / 2; ++i) wv[i] = q4[i];
+    };
     int f = next_unit(0);
     float wl_n[KAP], gor_n[KAP];
-    if (f < a.nfr) { load_w(TB.bi * a.nfr + f, 0, wl_n); load_go(TB.bi * a.nfr + f, gor_n); }
+    float4 wv_n[kBwRpw / 2];
+    if (f < a.nfr) {
+      load_w(TB.bi * a.nfr + f, 0, wl_n);
+      load_go(TB.bi * a.nfr + f, gor_n);
+      if (ksm) load_wv(TB.bi * a.nfr + f, 0, wv_n);
+    }
     for (; f < a.nfr;) {
       const int u = TB.bi * a.nfr + f;
       const JointUnit U = a.units[u];
@@ -600,21 +667,35 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       const int fn = next_unit(f + 1);
       for (int t = 0; t < NT32; ++t, ++g) {
         float wl[KAP];
+        float v[2 * kBwRpw];
 #pragma unroll
         for (int r = 0; r < KAP; ++r) wl[r] = wl_n[r];
-        if (t + 1 < NT32) load_w(u, t + 1, wl_n);
-        else if (fn < a.nfr) { load_w(TB.bi * a.nfr + fn, 0, wl_n); load_go(TB.bi * a.nfr + fn, gor_n); }
-        tc::mbar_wait(&tfull[buf], bph);
-        tc::tc_fence_after();
-        if (warp == 4 && lane == 0) TC_TRACE(5, g);
-        float v[2 * kBwRpw];
-        const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 2 * kBwRpw);
-        tc::tmem_ld16_nowait(ta, v);
-        tc::tmem_wait_ld();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
-        if (++buf == 2) { buf = 0; bph ^= 1; }
+        if (ksm) {
+#pragma unroll
+          for (int i = 0; i < kBwRpw / 2; ++i) {
+            v[4 * i] = wv_n[i].x; v[4 * i + 1] = wv_n[i].y; v[4 * i + 2] = wv_n[i].z; v[4 * i + 3] = wv_n[i].w;
+          }
+        }
+        if (t + 1 < NT32) {
+          load_w(u, t + 1, wl_n);
+          if (ksm) load_wv(u, t + 1, wv_n);
+        } else if (fn < a.nfr) {
+          load_w(TB.bi * a.nfr + fn, 0, wl_n);
+          load_go(TB.bi * a.nfr + fn, gor_n);
+          if (ksm) load_wv(TB.bi * a.nfr + fn, 0, wv_n);
+        }
+        if (!ksm) {
+          tc::mbar_wait(&tfull[buf], bph);
+          tc::tc_fence_after();
+          if (warp == 4 && lane == 0) TC_TRACE(5, g);
+          const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 2 * kBwRpw);
+          tc::tmem_ld16_nowait(ta, v);
+          tc::tmem_wait_ld();
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+          if (++buf == 2) { buf = 0; bph ^= 1; }
+        }
         float ghi[2 * kBwRpw], glo[2 * kBwRpw];
         if (a.expt & 1) {
 #pragma unroll
@@ -684,6 +765,11 @@ void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2
   const int N2 = ((2 * K + 15) / 16) * 16;
   *STG1 = 2 * kBwN1 * kcw;
   *STG2 = 2 * N2 * kb2;
+  if (K2 == 0) {   // split-K block: no GEMM1 (W comes from the forward), ring 2 only
+    *NS1 = 0;
+    *NS2 = (int)std::min<long>(kTcMaxStages2, (224L * 1024 - 1024) / (*STG2 * 4));
+    return;
+  }
   int nab, ta;
   tc_bwd_mode(K, K2, &nab, &ta);
   const long avail = 224L * 1024 - 1024 - (ta ? 0L : (long)2 * 128 * K2 * 4);
@@ -703,9 +789,10 @@ static const int g_tc_expt = [] {
 template <int KAP>
 static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream_t st) {
   int NS1, NS2, STG1, STG2;
-  tc_bwd_rings(C.Kmax, C.K2max, C.kcw, C.kb2, &NS1, &STG1, &NS2, &STG2);
+  tc_bwd_rings(C.Kmax, C.ks ? 0 : C.K2max, C.kcw, C.kb2, &NS1, &STG1, &NS2, &STG2);
   int nab, ta;
   tc_bwd_mode(C.Kmax, C.K2max, &nab, &ta);
+  if (C.ks) ta = 1;   // no A tile in SMEM
   const size_t sm = (size_t)((ta ? 0 : 2 * 128 * C.K2max) + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)C.ntiles, (unsigned)B);
@@ -714,23 +801,26 @@ static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream
 }
 
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                         int64_t go_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards,
-                         int B, const cudaStream_t* ss, int ns) {
+                         int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
+                         const float* thr, int shard, int n_shards, int B, const cudaStream_t* ss, int ns) {
   int li = 0;
   for (const TcClass& C : d.tcb) {
     const cudaStream_t st = ss[li++ % ns];
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
-               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, nullptr};
+               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, wbuf, wb_sb,
+               nullptr};
 #ifdef JTFS_TC_TRACE
     static long long* trace = nullptr;
     if (!trace) cudaMalloc(&trace, 16 * 512 * 8);
     if (C.Kmax == 18) { cudaMemsetAsync(trace, 0, 16 * 512 * 8, st); a.trace = trace; }
 #endif
-    switch (C.cls % 3) {  // class = 3 * kcw_kind + kap_kind
+    switch (C.cls) {  // class = kap_kind (KAP = 2 << kap_kind)
       case 0: launch_tc_bwd<2>(a, C, B, st); break;
       case 1: launch_tc_bwd<4>(a, C, B, st); break;
       case 2: launch_tc_bwd<8>(a, C, B, st); break;
+      case 3: launch_tc_bwd<16>(a, C, B, st); break;
+      case 4: launch_tc_bwd<32>(a, C, B, st); break;
     }
 #ifdef JTFS_TC_TRACE
     if (a.trace) {

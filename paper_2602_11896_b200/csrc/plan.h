@@ -59,14 +59,22 @@ struct BlockInfo {
 struct TcUnit {
   int64_t img_off, wt_off;   // offsets (floats) of the unit's B images / phi_F weights
   int64_t img2_off;          // offset of the backward B2 images (32-row tiles)
-  int32_t NT, pad;           // row tiles of 64 (0 = unit not on the tensor-core path)
+  int32_t NT;                // row tiles of 64 (0 = unit not on the tensor-core path)
+  int32_t wp_tile0;          // split-K blocks: index of the unit's first 64-row tile in the block's W buffer
 };
 struct TcBlock {
   int32_t bi, K, K2, cls;    // block, n1_max, padded 2K, launch class
   int32_t kcw, kb2;          // B-image chunk widths: forward/GEMM1 (k' elements), backward B2 (kk elements)
+  int32_t ks, nparts;        // split-K block (A tile too large for SMEM): number of K parts
+  int32_t kpw, wp_tiles;     // part width (k' elements, multiple of kcw); 64-row tiles per column tile
+  int64_t wp_off;            // offset (floats, per signal) of the block's W buffer
 };
-// forward classes 3*ct_kind + kap_kind (ct_kind: 0 = 2 column tiles, 1 = 1 tile kcw 32,
-// 2 = 1 tile kcw 16; kap_kind: rows_out <= 2, 4, 8); backward classes 3*(kcw == 16) + kap_kind
+// forward class = 8 * ct_kind + kap_kind (ct_kind 0: 2 column tiles, 1: one; KAP = 2 << kap_kind,
+// rows_out <= 2, 4, 8, 16, 32); backward class = kap_kind
+// Split-K blocks (K too large for a resident A tile, SURVEY §8(a) A5 large n1_max): the forward runs
+// in nparts launches over k' ranges of width kpw, accumulating the complex W of every cell in a
+// per-signal buffer (first part stores, middle parts add, the last adds and finishes: modulus, phi_F)
+// and leaving the full W there; the backward reads W instead of recomputing GEMM1.
 // backward TMEM plan (kernels_tc.cu): A2 double-buffered (nab = 2) when D2 leaves room; the Y2 tile A in
 // TMEM (ta = 1, GEMM1 in the TS form) when D1 + A2 + D2 + A_hi + A_lo fit in 512 columns.
 inline
@@ -119,7 +127,8 @@ struct Plan {
   std::vector<TcBlock> tc_blocks;               // tensor-core eligible blocks
   std::vector<char> blk_tc;                     // [n_blocks] 1 = forward on the tensor-core path
   std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
-  std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class 0..2)
+  std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class)
+  int64_t ks_w_floats = 0;                      // per-signal W buffer of the split-K blocks
   std::vector<float> tc_img, tc_wts, tc_img2;
   // FFT route of the joint stage (kernels_frfft.cu)
   std::vector<float> fr_spec;                   // [n_fr_all][P] level-0 responses of L_fr on the P grid

@@ -162,43 +162,62 @@ static void build_tc_tables(Plan* p) {
   p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0, 0});
   p->blk_tc.assign(p->blocks.size(), 0);
   p->blk_tcb.assign(p->blocks.size(), 0);
+  p->ks_w_floats = 0;
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
     const int K = p->blocks[bi].n1_max;
     const int K2 = ((2 * K + 7) / 8) * 8;
+    const int N2 = ((2 * K + 15) / 16) * 16;
     int ro_max = 0;
     for (int f = 0; f < nfr; ++f) ro_max = std::max(ro_max, p->units[bi * nfr + f].rows_out);
-    if (K2 > 168 || ro_max > 8) continue;   // resident A tile (128 x K2 x 8 B) must fit in SMEM
-    const int CT = K2 <= 64 ? 2 : 1;
-    const int kap = ro_max <= 2 ? 0 : (ro_max <= 4 ? 1 : 2);
-    // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
-    int kcw = 16;
-    for (int w : {K2, 64, 32}) {
-      if (w > 64 || w > K2) continue;
-      if (tc_fwd_stages(CT, 2 << kap, K2, w) >= 3) { kcw = w; break; }
+    if (ro_max > 32 || N2 > 384) continue;                  // FFT route (kernels_frfft.cu)
+    int kap = 0;
+    while ((2 << kap) < ro_max) ++kap;
+    // resident A tile (128 x K2 x 8 B) when it fits with >= 3 B stages, else split-K parts
+    int ks = 0, nparts = 1, kpw = K2, kcw = 16;
+    const int CT = (K2 <= 64 && kap <= 2) ? 2 : 1;
+    if (K2 <= 168 && kap <= 2) {
+      // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
+      for (int w : {K2, 64, 32}) {
+        if (w > 64 || w > K2) continue;
+        if (tc_fwd_stages(CT, 2 << kap, K2, w) >= 3) { kcw = w; break; }
+      }
+    } else {
+      ks = 1;
+      for (nparts = 2;; ++nparts) {
+        kpw = ((K2 + nparts - 1) / nparts + kcw - 1) / kcw * kcw;
+        if (tc_fwd_stages(1, 2 << kap, kpw, kcw) >= 3) break;
+      }
     }
-    const int ctk = CT == 2 ? 0 : (kcw == 32 ? 1 : 2);
     p->blk_tc[bi] = 1;
-    const int N2 = ((2 * K + 15) / 16) * 16;
-    // widest B2 chunk whose rings fit (fewer chunk hand-offs per tile): ring 2 >= 2 stages, ring 1 >= 2
+    // widest B2 chunk whose rings fit (fewer chunk hand-offs per tile)
     int kb2 = 8;
     for (int w : {64, 32, 16, 8}) {
       int ns1, s1, ns2, s2;
-      tc_bwd_rings(K, K2, kcw, w, &ns1, &s1, &ns2, &s2);
-      if (ns1 >= 2 && ns2 * w >= 128 + w) { kb2 = w; break; }
+      tc_bwd_rings(K, ks ? 0 : K2, kcw, w, &ns1, &s1, &ns2, &s2);
+      if (ks ? ns2 >= 3 : (ns1 >= 2 && ns2 * w >= 128 + w)) { kb2 = w; break; }
     }
-    p->tc_blocks.push_back({(int32_t)bi, K, K2, 3 * ctk + kap, kcw, kb2});
+    int wp_tiles = 0;
+    for (int f = 0; f < nfr; ++f) wp_tiles += (int)((p->units[bi * nfr + f].n_rows + 63) / 64);
+    const int64_t n_ct = (p->binfo[bi].n_cols + 127) / 128;
+    const int64_t wp_off = ks ? p->ks_w_floats : 0;
+    if (ks) p->ks_w_floats += n_ct * wp_tiles * 128 * 128;
+    p->tc_blocks.push_back({(int32_t)bi, K, K2, 8 * (CT == 2 ? 0 : 1) + kap, kcw, kb2, ks, nparts, kpw, wp_tiles,
+                            wp_off});
     int ns1, s1, ns2, s2;
-    tc_bwd_rings(K, K2, kcw, kb2, &ns1, &s1, &ns2, &s2);
-    const bool bwd = N2 <= 256 && ns1 >= 2 && ns2 >= 2;
+    tc_bwd_rings(K, ks ? 0 : K2, kcw, kb2, &ns1, &s1, &ns2, &s2);
+    const bool bwd = ks ? ns2 >= 2 : (N2 <= 256 && ns1 >= 2 && ns2 >= 2);
     if (bwd) {
       p->blk_tcb[bi] = 1;
-      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcw, kb2});
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcw, kb2, ks, nparts, kpw, wp_tiles, wp_off});
     }
+    int tile0 = 0;
     for (int f = 0; f < nfr; ++f) {
       const int u = (int)bi * nfr + f;
       const JointUnit& U = p->units[u];
       TcUnit tu{};
       tu.NT = (int32_t)((U.n_rows + 63) / 64);
+      tu.wp_tile0 = tile0;
+      tile0 += tu.NT;
       tu.img_off = (int64_t)p->tc_img.size();
       tu.wt_off = (int64_t)p->tc_wts.size();
       const double* h = p->hfr_d.data() + (size_t)U.f * p->P * 2;
