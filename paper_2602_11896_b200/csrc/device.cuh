@@ -19,6 +19,10 @@ struct TcClass {
   int K2max = 0, Kmax = 0, kcw = 32, kb2 = 8;
   int cls = 0;                     // kernel variant (TcBlock::cls)
   int ks = 0, nparts = 1;          // split-K block: K parts of the forward
+  int ngmax = 1;                   // filter groups the launch may use (TcBlock::ngmax)
+  int64_t n_cols = 0;              // columns of the block
+  int bi = 0;                      // block index
+  int64_t gp_off = 0;              // backward g_Y2 partials offset (TcBlock::gp_off)
 };
 
 struct FfList {                    // blocks on the FFT route of the joint stage + column-tile prefix
@@ -140,7 +144,8 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
                          const cudaStream_t* ss, int ns);
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
-                         const float* thr, int shard, int n_shards, int B, const cudaStream_t* ss, int ns);
+                         float2* gp, int64_t gp_sb, const float* thr, int shard, int n_shards, int B,
+                         const cudaStream_t* ss, int ns);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                       int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
                       cudaStream_t st);

@@ -238,6 +238,10 @@ static cudaError_t upload(Plan& p) {
       c.K2max = (fwd && tb.ks) ? tb.kpw : tb.K2;
       c.ks = tb.ks;
       c.nparts = tb.nparts;
+      c.ngmax = tb.ngmax;
+      c.n_cols = p.binfo[tb.bi].n_cols;
+      c.bi = tb.bi;
+      c.gp_off = tb.gp_off;
       c.Kmax = tb.K;
       c.kcw = tb.kcw;
       c.kb2 = tb.kb2;
@@ -373,9 +377,9 @@ static jtfs_status ensure_device(jtfs_plan_s* h) {
 // ------------------------------------------------------------------------------ workspace layout
 struct Layout {
   // per-signal sizes in bytes (each 256-aligned) of every buffer, in this order
-  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss, thr, Wk;
+  size_t xp, Xh, A, Z1, U1h, Y2, cs, ct, S1t, W1, V2, o, S, r, gS1t, g, loss, thr, Wk, gp;
   size_t per_signal() const {
-    return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss + thr + Wk;
+    return xp + Xh + A + Z1 + U1h + Y2 + cs + ct + S1t + W1 + V2 + o + S + r + gS1t + g + loss + thr + Wk + gp;
   }
 };
 static size_t al(size_t b) { return (b + 255) / 256 * 256; }
@@ -399,14 +403,16 @@ static Layout layout(const Plan& p, int with_grad) {
   L.loss = 256;
   L.thr = 256;
   L.Wk = al(std::max<int64_t>(p.ks_w_floats, 1) * 4);   // split-K blocks: complex W of every cell
+  L.gp = with_grad ? al(std::max<int64_t>(p.gp_complex, 1) * 8) : 0;   // g_Y2 partials of filter groups
   return L;
 }
 
 struct Bufs {
   float2 *xp, *Xh, *A, *Z1, *U1h, *Y2, *cs, *ct, *W1;
   float *S1t, *V2, *o, *S, *r, *gS1t, *g, *loss, *thr, *Wk;
+  float2* gp;
   // per-signal strides in elements
-  int64_t s_xp, s_A, s_L1, s_Y2, s_c, s_S1t, s_W1, s_V2, s_o, s_S, s_g, s_Wk;
+  int64_t s_xp, s_A, s_L1, s_Y2, s_c, s_S1t, s_W1, s_V2, s_o, s_S, s_g, s_Wk, s_gp;
 };
 static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
   Bufs b{};
@@ -419,10 +425,12 @@ static Bufs carve(const Plan& p, const Layout& L, char* base, int mb) {
   b.loss = (float*)take(L.loss);
   b.thr = (float*)take(L.thr);   // one float per signal (mb contiguous floats at the start)
   b.Wk = (float*)take(L.Wk);
+  b.gp = (float2*)take(L.gp);
   // strides in complex64 units (complex128 views: half)
   b.s_xp = L.xp / 8; b.s_A = L.A / 8; b.s_L1 = L.Z1 / 8; b.s_Y2 = L.Y2 / 8; b.s_c = L.cs / 8;
   b.s_S1t = L.S1t / 4; b.s_W1 = L.W1 / 8; b.s_V2 = L.V2 / 4; b.s_o = L.o / 4; b.s_S = L.S / 4; b.s_g = L.g / 4;
   b.s_Wk = L.Wk / 4;
+  b.s_gp = L.gp / 8;
   (void)p;
   return b;
 }
@@ -513,7 +521,8 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     Fanout* fo = fanout_get();
     fan_fork(fo, st);
     launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
-    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.Wk, w.s_Wk, w.thr, shard, n_shards, mb, fo->s + 1,
+    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.Wk, w.s_Wk, w.gp, w.s_gp, w.thr, shard,
+                        n_shards, mb, fo->s + 1,
                         kFanStreams - 1);
     launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
     fan_join(fo, st);

@@ -83,6 +83,7 @@ struct TcArgs {
   int nfr, shard, n_shards;
   float* wbuf; int64_t wb_sb;       // split-K blocks: per-signal W buffer
   int part, pmode;                  // K part of this launch; kPm* bits
+  int ng;                           // filter groups: CTA x handles column tile x % ntiles, filters f = x / ntiles mod ng
 };
 constexpr int kPmLoad = 1, kPmStore = 2, kPmFinish = 4;
 
@@ -95,10 +96,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   __shared__ uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int jb = find_tc(a.tiles, a.n_tc_blocks, blockIdx.x);
+  const int jb = 0;                                         // one block per launch
+  const int ntl = (int)(a.tiles[1] - a.tiles[0]);
+  const int ct = (int)blockIdx.x % ntl, grp = (int)blockIdx.x / ntl;
   const TcBlock TB = a.blocks[jb];
   const BlockInfo bf = a.binfo[TB.bi];
-  const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)(128 * CT);
+  const int64_t col0 = (int64_t)ct * (128 * CT);
   const int b = blockIdx.y;
   const int K = TB.K, kcw = TB.kcw;
   const int kp_lo = TB.ks ? a.part * TB.kpw : 0;            // k' range of this launch (split-K blocks)
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     uint32_t ph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard) continue;
+      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       for (int t = 0; t < tu.NT; ++t) {
         // row tile t of the unit's image: chunks of the full K2, starting at this launch's k' range
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     uint32_t ph = 0, bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard) continue;
+      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       for (int t = 0; t < tu.NT; ++t) {
         tc::mbar_wait(&tempty[buf], bph ^ 1);
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     uint32_t bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard) continue;
+      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       const JointUnit U = a.units[u];
       const TcUnit tu = a.tcu[u];
       const int ro = U.rows_out;
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
             // split-K: W of (tile t, column c, rows h*32 ..) accumulated across the K parts
             float4* wp = reinterpret_cast<float4*>(
                 a.wbuf + b * a.wb_sb + TB.wp_off +
-                (((int64_t)(blockIdx.x - a.tiles[jb]) * TB.wp_tiles + tu.wp_tile0 + t) * 128 + c) * 128 + h * 64);
+                (((int64_t)ct * TB.wp_tiles + tu.wp_tile0 + t) * 128 + c) * 128 + h * 64);
             if (pmode & kPmLoad) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
@@ -305,13 +308,20 @@ int tc_fwd_stages(int CT, int KAP, int K2, int kcw) {
   return NS;
 }
 
+// filter groups of a launch: fixed per block by the planner (about two waves of 148 SMs per signal),
+// independent of the batch so that micro-batching leaves every summation order, hence the bits, unchanged
+static int tc_groups(const TcClass& C, int B) {
+  (void)B;
+  return C.ngmax;
+}
+
 template <int CT, int KAP>
 static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st) {
   const int STG = 2 * kTcN * C.kcw;
   const int NS = tc_fwd_stages(CT, KAP, C.K2max, C.kcw);
   const size_t sm = tc_fwd_smem(CT, KAP, NS, C.K2max, STG);
   cudaFuncSetAttribute(k_joint_fwd_tc<CT, KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 g((unsigned)C.ntiles, (unsigned)B);
+  dim3 g((unsigned)(C.ntiles * a.ng), (unsigned)B);
   k_joint_fwd_tc<CT, KAP><<<g, kTcThreads, sm, st>>>(a, NS, STG);
   count_launch();
 }
@@ -331,7 +341,7 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
                 (part == nparts - 1 ? kPmFinish : 0);
       }
       TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
-               (int)p.L_fr.size(), shard, n_shards, wbuf, wb_sb, part, pmode};
+               (int)p.L_fr.size(), shard, n_shards, wbuf, wb_sb, part, pmode, tc_groups(C, B)};
       // class = 8 * ct_kind + kap_kind (CT = 2 for ct_kind 0)
       switch (C.cls) {
         case 0: launch_tc<2, 2>(a, C, B, st); break;
@@ -364,6 +374,8 @@ struct TcBwArgs {
   const float* thr;
   int expt;                         // timing experiments only (JTFS_TC_EXPT); 0 in production
   const float* wbuf; int64_t wb_sb; // split-K blocks: W left by the forward (GEMM1 skipped)
+  int ng;                           // filter groups (see TcArgs); ng > 1: D2 partials to gp, reduced after
+  float2* gp; int64_t gp_sb;
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
 };
 #ifdef JTFS_TC_TRACE
@@ -382,10 +394,12 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   __shared__ uint64_t tfull[2], tempty[2], a2full[2], a2empty[2], d2full;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int jb = find_tc(a.tiles, a.n_tc_blocks, blockIdx.x);
+  const int jb = 0;                                     // one block per launch
+  const int ntl = (int)(a.tiles[1] - a.tiles[0]);
+  const int ct = (int)blockIdx.x % ntl, grp = (int)blockIdx.x / ntl;
   const TcBlock TB = a.blocks[jb];
   const BlockInfo bf = a.binfo[TB.bi];
-  const int64_t col0 = (blockIdx.x - a.tiles[jb]) * (int64_t)128;
+  const int64_t col0 = (int64_t)ct * 128;
   const int b = blockIdx.y;
   const int K = TB.K, K2 = TB.K2, kcw = TB.kcw, kB2c = TB.kb2;
   const int N2 = ((2 * K + 15) / 16) * 16;
@@ -456,7 +470,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     uint32_t ph = 0;
     for (int f = 0; f < (p1 && ksm ? 0 : a.nfr); ++f) {   // no GEMM1 (ring 1) in split-K mode
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard) continue;
+      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       const int NT32 = (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
       for (int t32 = 0; t32 < NT32; ++t32) {
@@ -595,7 +609,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     int G = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard) continue;
+      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       G += (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
     }
     if (warp == 1) {
@@ -620,7 +634,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     // phi_F weights and g_o are prefetched one tile ahead (their L2 latency would otherwise sit on the
     // epilogue's critical path every tile)
     auto next_unit = [&](int f) {
-      while (f < a.nfr && (TB.bi * a.nfr + f) % a.n_shards != a.shard) ++f;
+      while (f < a.nfr && ((TB.bi * a.nfr + f) % a.n_shards != a.shard || f % a.ng != grp)) ++f;
       return f;
     };
     auto load_w = [&](int u, int t, float* wl) {
@@ -641,7 +655,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     };
     // split-K mode: W of (tile, column, this warp's 8 rows) from the forward's buffer, one tile ahead
     const float* wcol = ksm ? a.wbuf + b * a.wb_sb + TB.wp_off +
-                                  (((int64_t)(blockIdx.x - a.tiles[jb]) * TB.wp_tiles) * 128 + c) * 128 + h * 16
+                                  (((int64_t)ct * TB.wp_tiles) * 128 + c) * 128 + h * 16
                             : nullptr;
     auto load_wv = [&](int u, int t32, float4* wv) {
       const float4* q4 = reinterpret_cast<const float4*>(
@@ -736,7 +750,10 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       tc::tc_fence_after();
     }
     if (h == 0) {
-      float2* dst = a.gY + b * a.gy_sb + bf.y_off + (bf.c_lo + (colg < bf.n_cols ? colg : 0)) % bf.T2;
+      // ng == 1: g_Y2[n][col]; ng > 1: this group's partial gp[grp][n][col] (reduced by k_gy_reduce)
+      const int64_t dstride = a.ng > 1 ? bf.n_cols : bf.T2;
+      float2* dst = a.ng > 1 ? a.gp + b * a.gp_sb + TB.gp_off + (int64_t)grp * K * bf.n_cols + (colg < bf.n_cols ? colg : 0)
+                             : a.gY + b * a.gy_sb + bf.y_off + (bf.c_lo + (colg < bf.n_cols ? colg : 0)) % bf.T2;
       for (int c0 = 0; c0 < N2; c0 += 16) {
         float v[16];
         if (g > 0) {
@@ -749,7 +766,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int n = c0 / 2 + i;
-            if (n < K) dst[(int64_t)n * bf.T2] = make_float2(v[2 * i], v[2 * i + 1]);
+            if (n < K) dst[(int64_t)n * dstride] = make_float2(v[2 * i], v[2 * i + 1]);
           }
         }
       }
@@ -795,21 +812,39 @@ static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream
   if (C.ks) ta = 1;   // no A tile in SMEM
   const size_t sm = (size_t)((ta ? 0 : 2 * 128 * C.K2max) + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 g((unsigned)C.ntiles, (unsigned)B);
+  dim3 g((unsigned)(C.ntiles * a.ng), (unsigned)B);
   k_joint_bwd_tc<KAP><<<g, kBwThreads, sm, st>>>(a, NS1, STG1, NS2, STG2);
   count_launch();
 }
 
+// g_Y2[n][col] = sum over filter groups of the partials (fixed order: deterministic)
+__global__ void k_gy_reduce(const float2* __restrict__ gp, int64_t gp_sb, int64_t gp_off, float2* __restrict__ gY,
+                            int64_t gy_sb, BlockInfo bf, int K, int ng) {
+  const int b = blockIdx.y;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (int64_t)K * bf.n_cols) return;
+  const int64_t n = q / bf.n_cols, col = q % bf.n_cols;
+  const float2* src = gp + b * gp_sb + gp_off + q;
+  float2 acc = src[0];
+  for (int g = 1; g < ng; ++g) {
+    const float2 v = src[(int64_t)g * K * bf.n_cols];
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  gY[b * gy_sb + bf.y_off + n * bf.T2 + (bf.c_lo + col) % bf.T2] = acc;
+}
+
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
-                         const float* thr, int shard, int n_shards, int B, const cudaStream_t* ss, int ns) {
+                         float2* gp, int64_t gp_sb, const float* thr, int shard, int n_shards, int B,
+                         const cudaStream_t* ss, int ns) {
   int li = 0;
   for (const TcClass& C : d.tcb) {
     const cudaStream_t st = ss[li++ % ns];
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
                d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, wbuf, wb_sb,
-               nullptr};
+               tc_groups(C, B), gp, gp_sb, nullptr};
 #ifdef JTFS_TC_TRACE
     static long long* trace = nullptr;
     if (!trace) cudaMalloc(&trace, 16 * 512 * 8);
@@ -821,6 +856,12 @@ void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
       case 2: launch_tc_bwd<8>(a, C, B, st); break;
       case 3: launch_tc_bwd<16>(a, C, B, st); break;
       case 4: launch_tc_bwd<32>(a, C, B, st); break;
+    }
+    if (a.ng > 1) {
+      const BlockInfo& bf = p.binfo[C.bi];
+      dim3 gr((unsigned)((C.Kmax * bf.n_cols + 255) / 256), (unsigned)B);
+      k_gy_reduce<<<gr, 256, 0, st>>>(gp, gp_sb, C.gp_off, gY, gy_sb, bf, C.Kmax, a.ng);
+      count_launch();
     }
 #ifdef JTFS_TC_TRACE
     if (a.trace) {

@@ -68,6 +68,8 @@ struct TcBlock {
   int32_t ks, nparts;        // split-K block (A tile too large for SMEM): number of K parts
   int32_t kpw, wp_tiles;     // part width (k' elements, multiple of kcw); 64-row tiles per column tile
   int64_t wp_off;            // offset (floats, per signal) of the block's W buffer
+  int32_t ngmax, pad2;       // filter groups a launch may split into (few column tiles -> more CTAs)
+  int64_t gp_off;            // backward: offset (complex, per signal) of the block's g_Y2 partials
 };
 // forward class = 8 * ct_kind + kap_kind (ct_kind 0: 2 column tiles, 1: one; KAP = 2 << kap_kind,
 // rows_out <= 2, 4, 8, 16, 32); backward class = kap_kind
@@ -129,6 +131,7 @@ struct Plan {
   std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
   std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class)
   int64_t ks_w_floats = 0;                      // per-signal W buffer of the split-K blocks
+  int64_t gp_complex = 0;                       // per-signal g_Y2 partials of the filter-group split
   std::vector<float> tc_img, tc_wts, tc_img2;
   // FFT route of the joint stage (kernels_frfft.cu)
   std::vector<float> fr_spec;                   // [n_fr_all][P] level-0 responses of L_fr on the P grid

@@ -163,6 +163,7 @@ static void build_tc_tables(Plan* p) {
   p->blk_tc.assign(p->blocks.size(), 0);
   p->blk_tcb.assign(p->blocks.size(), 0);
   p->ks_w_floats = 0;
+  p->gp_complex = 0;
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
     const int K = p->blocks[bi].n1_max;
     const int K2 = ((2 * K + 7) / 8) * 8;
@@ -201,14 +202,25 @@ static void build_tc_tables(Plan* p) {
     const int64_t n_ct = (p->binfo[bi].n_cols + 127) / 128;
     const int64_t wp_off = ks ? p->ks_w_floats : 0;
     if (ks) p->ks_w_floats += n_ct * wp_tiles * 128 * 128;
+    // launches with few column tiles split the filters over CTA groups: about two waves of 148 SMs for a
+    // batch of kRefBatch signals. Fixed per plan (not per call), so every summation order and hence every
+    // bit of a signal's result is independent of the batch / micro-batch it is computed in.
+    constexpr int64_t kRefBatch = 8;
+    const int64_t n_tiles = (p->binfo[bi].n_cols + 128 * CT - 1) / (128 * CT);
+    const int ngmax =
+        (int)std::min<int64_t>(nfr, std::max<int64_t>(1, (296 + n_tiles * kRefBatch - 1) / (n_tiles * kRefBatch)));
     p->tc_blocks.push_back({(int32_t)bi, K, K2, 8 * (CT == 2 ? 0 : 1) + kap, kcw, kb2, ks, nparts, kpw, wp_tiles,
-                            wp_off});
+                            wp_off, ngmax, 0, 0});
     int ns1, s1, ns2, s2;
     tc_bwd_rings(K, ks ? 0 : K2, kcw, kb2, &ns1, &s1, &ns2, &s2);
     const bool bwd = ks ? ns2 >= 2 : (N2 <= 256 && ns1 >= 2 && ns2 >= 2);
     if (bwd) {
       p->blk_tcb[bi] = 1;
-      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcw, kb2, ks, nparts, kpw, wp_tiles, wp_off});
+      const int ngb =
+          (int)std::min<int64_t>(nfr, std::max<int64_t>(1, (296 + n_ct * kRefBatch - 1) / (n_ct * kRefBatch)));
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcw, kb2, ks, nparts, kpw, wp_tiles, wp_off, ngb, 0,
+                               ngb > 1 ? p->gp_complex : 0});
+      if (ngb > 1) p->gp_complex += (int64_t)ngb * K * p->binfo[bi].n_cols;
     }
     int tile0 = 0;
     for (int f = 0; f < nfr; ++f) {
