@@ -162,7 +162,8 @@ int64_t jtfs_launch_count(void);
  *  out[0] forward dense-contraction flops on the tensor-core blocks (8 K per cell)
  *  out[1] forward FP32 flops on the FFT-route blocks (per column: 5 P log2 P for FFT_P of y; per filter
  *         4 P fold + 5 L_f log2 L_f inverse FFT + 4 n_rows modulus + 2 rows_out n_rows phi_F)
- *  out[2] backward contraction flops on the tensor-core blocks (16 K per cell)
+ *  out[2] backward contraction flops on the tensor-core blocks (16 K per cell: recompute + adjoint;
+ *         8 K on split-K blocks, whose backward reuses the W kept by the forward)
  *  out[3] backward FP32 flops on the FFT-route blocks (recompute, phi_F adjoint, phase, DFT, spectrum
  *         accumulation, final inverse FFT_P)
  *  out[4] cells, out[5] HBM bytes of the joint stage (Y2 r fwd + r bwd, g_Y2 w, o w + g_o r). cap >= 8. */

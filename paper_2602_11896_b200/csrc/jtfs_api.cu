@@ -604,7 +604,8 @@ jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap) {
     // tensor-core route: the complex contraction (8K flops per modulus value forward, 16K backward)
     if (rf == kRouteTc) c[0] += cells * 8.0 * u.n1_max;
     else if (rf == kRouteSimt) c[1] += cells * (8.0 * u.n1_max + 3.0 + 2.0 * u.rows_out);
-    if (rb == kRouteTc) c[2] += cells * 16.0 * u.n1_max;
+    // split-K blocks: the backward reads W kept by the forward (GEMM2 only, 8K per cell)
+    if (rb == kRouteTc) c[2] += cells * (p.blk_ks[u.bi] ? 8.0 : 16.0) * u.n1_max;
     else if (rb == kRouteSimt) c[3] += cells * (16.0 * u.n1_max + 6.0 + 2.0 * u.rows_out);
     c[4] += cells;
     c[5] += 2.0 * 4.0 * u.rows_out * ncols;   // o written (fwd) and g_o read (bwd)

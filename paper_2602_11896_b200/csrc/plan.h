@@ -129,6 +129,7 @@ struct Plan {
   std::vector<TcBlock> tc_blocks;               // tensor-core eligible blocks
   std::vector<char> blk_tc;                     // [n_blocks] 1 = forward on the tensor-core path
   std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
+  std::vector<char> blk_ks;                     // [n_blocks] 1 = split-K tensor-core block
   std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class)
   int64_t ks_w_floats = 0;                      // per-signal W buffer of the split-K blocks
   int64_t gp_complex = 0;                       // per-signal g_Y2 partials of the filter-group split

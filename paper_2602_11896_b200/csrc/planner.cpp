@@ -162,6 +162,7 @@ static void build_tc_tables(Plan* p) {
   p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0, 0});
   p->blk_tc.assign(p->blocks.size(), 0);
   p->blk_tcb.assign(p->blocks.size(), 0);
+  p->blk_ks.assign(p->blocks.size(), 0);
   p->ks_w_floats = 0;
   p->gp_complex = 0;
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
@@ -190,6 +191,7 @@ static void build_tc_tables(Plan* p) {
       }
     }
     p->blk_tc[bi] = 1;
+    p->blk_ks[bi] = (char)ks;
     // widest B2 chunk whose rings fit (fewer chunk hand-offs per tile)
     int kb2 = 8;
     for (int w : {64, 32, 16, 8}) {
