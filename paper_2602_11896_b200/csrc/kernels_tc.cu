@@ -107,9 +107,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   const int kp_lo = TB.ks ? a.part * TB.kpw : 0;            // k' range of this launch (split-K blocks)
   const int K2 = TB.ks ? min(TB.kpw, TB.K2 - kp_lo) : TB.K2;
   const int pmode = TB.ks ? a.pmode : kPmFinish;
-  float* a_hi = reinterpret_cast<float*>(sm);              // [CT][128][K2] canonical
+  const bool tsa = tc_fwd_tsa(CT, K2);                     // A in TMEM (TS-form MMAs)
+  float* a_hi = reinterpret_cast<float*>(sm);              // [CT][128][K2] canonical (SS form)
   float* a_lo = a_hi + CT * 128 * K2;
-  float* bst = a_lo + CT * 128 * K2;                        // NS stages x STG floats
+  float* bst = tsa ? a_hi : a_lo + CT * 128 * K2;           // NS stages x STG floats
   float* red = bst + NS * STG;                              // [CT][KAP][128]
 
   if (tid == 0) {
@@ -117,15 +118,49 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, CT == 1 ? 256 : 512);
+  const int tcols = (CT == 1 && !tsa) ? 256 : 512;
+  if (warp == 1) tc::tmem_alloc(&tmem_base, tcols);
   const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off;
-  for (int m = 0; m < CT; ++m)
-    build_a(a_hi + m * 128 * K2, a_lo + m * 128 * K2, ysrc, bf, col0 + m * 128, K, K2, tid, kTcThreads, kp_lo / 2);
+  if (!tsa)
+    for (int m = 0; m < CT; ++m)
+      build_a(a_hi + m * 128 * K2, a_lo + m * 128 * K2, ysrc, bf, col0 + m * 128, K, K2, tid, kTcThreads, kp_lo / 2);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = tmem_base;
+  // TS form: A hi at TMEM columns [256, 256 + K2), lo at [256 + K2, 256 + 2 K2)
+  const uint32_t taa_hi = tbase + 256, taa_lo = taa_hi + (uint32_t)K2;
+  if (tsa) {
+    if (warp >= 4 && warp < 8) {
+      const uint32_t lq = (uint32_t)((warp & 3) * 32) << 16;
+      const int64_t col = col0 + (warp & 3) * 32 + lane;
+      const float2* ycol = ysrc + (bf.c_lo + (col < bf.n_cols ? col : 0)) % bf.T2;
+      const int n0 = kp_lo / 2;
+      for (int k0 = 0; k0 < K2; k0 += 16) {
+        float hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n = n0 + k0 / 2 + j;
+          float2 v = make_float2(0.f, 0.f);
+          if (n < K && k0 / 2 + j < K2 / 2 && col < bf.n_cols) v = ycol[(int64_t)n * bf.T2];
+          tc::split_tf32(v.x, hi[2 * j], lo[2 * j]);
+          tc::split_tf32(v.y, hi[2 * j + 1], lo[2 * j + 1]);
+        }
+        if (K2 - k0 >= 16) {
+          tc::tmem_st16(taa_hi + lq + (uint32_t)k0, hi);
+          tc::tmem_st16(taa_lo + lq + (uint32_t)k0, lo);
+        } else {
+          tc::tmem_st8(taa_hi + lq + (uint32_t)k0, hi);
+          tc::tmem_st8(taa_lo + lq + (uint32_t)k0, lo);
+        }
+      }
+      tc::tmem_wait_st();
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+  }
   const int nchunks = (K2 + kcw - 1) / kcw;
 
   if (warp == 0) {
@@ -182,13 +217,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
           if (tc::elect_one()) {
             for (int ks = 0; ks < kc / 8; ++ks) {
               const uint32_t kg = (uint32_t)(ch * (kcw / 8) + ks);
+              if (tsa) {
+                tc::mma_tf32_ts(dbase, taa_hi + 8u * kg, dB_hi + 16u * ks, idesc, (ch > 0 || ks > 0) ? 1u : 0u);
+                tc::mma_tf32_ts(dbase, taa_hi + 8u * kg, dB_lo + 16u * ks, idesc, 1u);
+                tc::mma_tf32_ts(dbase, taa_lo + 8u * kg, dB_hi + 16u * ks, idesc, 1u);
+              } else {
 #pragma unroll
-              for (int m = 0; m < CT; ++m) {
-                const uint32_t d = dbase + (uint32_t)(m * kTcN);
-                const uint64_t ao = (uint64_t)(m * aStepM + 16u * kg);
-                tc::mma_tf32(d, dA_hi + ao, dB_hi + 16u * ks, idesc, (ch > 0 || ks > 0) ? 1u : 0u);
-                tc::mma_tf32(d, dA_hi + ao, dB_lo + 16u * ks, idesc, 1u);
-                tc::mma_tf32(d, dA_lo + ao, dB_hi + 16u * ks, idesc, 1u);
+                for (int m = 0; m < CT; ++m) {
+                  const uint32_t d = dbase + (uint32_t)(m * kTcN);
+                  const uint64_t ao = (uint64_t)(m * aStepM + 16u * kg);
+                  tc::mma_tf32(d, dA_hi + ao, dB_hi + 16u * ks, idesc, (ch > 0 || ks > 0) ? 1u : 0u);
+                  tc::mma_tf32(d, dA_hi + ao, dB_lo + 16u * ks, idesc, 1u);
+                  tc::mma_tf32(d, dA_lo + ao, dB_hi + 16u * ks, idesc, 1u);
+                }
               }
             }
             tc::mma_commit(&empty[stage]);
@@ -293,11 +334,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, CT == 1 ? 256 : 512);
+  if (warp == 1) tc::tmem_dealloc(tbase, tcols);
 }
 
 static size_t tc_fwd_smem(int CT, int KAP, int NS, int K2, int STG) {
-  return (size_t)(2 * CT * 128 * K2 + NS * STG + CT * KAP * 128) * 4 + 1024;
+  return (size_t)((tc_fwd_tsa(CT, K2) ? 0 : 2 * CT * 128 * K2) + NS * STG + CT * KAP * 128) * 4 + 1024;
 }
 
 // forward B ring stages that fit (the planner rejects chunk widths that leave fewer than 3)

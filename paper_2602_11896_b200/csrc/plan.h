@@ -92,6 +92,14 @@ void tc_bwd_mode(int K, int K2, int* nab, int* ta) {
 // backward B ring sizing shared by the planner (chooses kb2) and the launcher (kernels_tc.cu)
 void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2, int* STG2);
 int tc_fwd_stages(int CT, int KAP, int K2, int kcw);
+// forward TMEM plan: the Y2 tile (hi + lo, 2 K2 columns) goes to TMEM and the MMAs take the TS form when
+// it fits beside the double-buffered accumulators (CT = 1: 2 x 128 columns); the SS form reads A and B
+// from SMEM at 8 KB per N = 128 MMA, which saturates SMEM bandwidth together with the B stream
+inline
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+bool tc_fwd_tsa(int CT, int K2) { return CT == 1 && 256 + 2 * K2 <= 512; }
 
 struct DeviceTables;  // device pointers (jtfs_api.cu)
 

@@ -185,10 +185,16 @@ static void build_tc_tables(Plan* p) {
       }
     } else {
       ks = 1;
-      for (nparts = 2;; ++nparts) {
+      // fewest K parts whose A tile fits TMEM (TS-form MMAs); else the fewest with >= 3 SMEM stages
+      int np_ss = 0;
+      for (nparts = 2; nparts <= 8; ++nparts) {
         kpw = ((K2 + nparts - 1) / nparts + kcw - 1) / kcw * kcw;
-        if (tc_fwd_stages(1, 2 << kap, kpw, kcw) >= 3) break;
+        if (tc_fwd_stages(1, 2 << kap, kpw, kcw) < 3) continue;
+        if (!np_ss) np_ss = nparts;
+        if (tc_fwd_tsa(1, kpw)) break;
       }
+      if (nparts > 8) nparts = np_ss;
+      kpw = ((K2 + nparts - 1) / nparts + kcw - 1) / kcw * kcw;
     }
     p->blk_tc[bi] = 1;
     p->blk_ks[bi] = (char)ks;
