@@ -84,8 +84,17 @@ struct TcArgs {
   float* wbuf; int64_t wb_sb;       // split-K blocks: per-signal W buffer
   int part, pmode;                  // K part of this launch; kPm* bits
   int ng;                           // filter groups: CTA x handles column tile x % ntiles, filters f = x / ntiles mod ng
+  long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
 };
 constexpr int kPmLoad = 1, kPmStore = 2, kPmFinish = 4;
+#ifdef JTFS_TC_TRACE
+#define TC_TRACE(ev, g)                                                                  \
+  do {                                                                                   \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (g) < 512) a.trace[(ev) * 512 + (g)] = clock64(); \
+  } while (0)
+#else
+#define TC_TRACE(ev, g) do {} while (0)
+#endif
 
 // =====================================================================================
 // forward
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     const uint64_t dA_lo = tc::sdesc(tc::smem_u32(a_lo), 128, sboA);
     const uint32_t aStepM = (uint32_t)(128 * K2 * 4) >> 4;
     const uint32_t bst_s = tc::smem_u32(bst);
-    int stage = 0, buf = 0;
+    int stage = 0, buf = 0, gt = 0;
     uint32_t ph = 0, bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
@@ -206,11 +215,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
       for (int t = 0; t < tu.NT; ++t) {
         tc::mbar_wait(&tempty[buf], bph ^ 1);
         tc::tc_fence_after();
+        if (lane == 0) TC_TRACE(0, gt);
         const uint32_t dbase = tbase + (uint32_t)(buf * CT * kTcN);
         for (int ch = 0; ch < nchunks; ++ch) {
           const int kc = min(kcw, K2 - ch * kcw);
           tc::mbar_wait(&full[stage], ph);
           tc::tc_fence_after();
+          if (lane == 0 && ch == 0) TC_TRACE(1, gt);
           const uint32_t bh = bst_s + (uint32_t)(stage * STG * 4);
           const uint64_t dB_hi = tc::sdesc(bh, 128, (uint32_t)kc * 32u);
           const uint64_t dB_lo = tc::sdesc(bh + (uint32_t)(kTcN * kc * 4), 128, (uint32_t)kc * 32u);
@@ -239,6 +250,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         }
         if (tc::elect_one()) tc::mma_commit(&tfull[buf]);
         __syncwarp();
+        if (lane == 0) TC_TRACE(2, gt);
+        ++gt;
         if (++buf == 2) { buf = 0; bph ^= 1; }
       }
     }
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     const int e = warp - 4;
     const int q = e & 3, h = e >> 2;        // lane quadrant, column half (32 complex rows)
     const int c = q * 32 + lane;            // time column within the tile
-    int buf = 0;
+    int buf = 0, ge = 0;
     uint32_t bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
@@ -269,6 +282,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         for (int r = 0; r < KAP; ++r) wl[r] = (r < ro) ? __ldg(wt + r * ldw + t * kTcRows + h * 32 + lane) : 0.f;
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
+        if (warp == 4 && lane == 0) TC_TRACE(5, ge);
 #pragma unroll
         for (int m = 0; m < CT; ++m) {
           float v[64];
@@ -306,6 +320,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        if (warp == 4 && lane == 0) TC_TRACE(6, ge);
+        ++ge;
         if (++buf == 2) { buf = 0; bph ^= 1; }
       }
       if (!(pmode & kPmFinish)) continue;
@@ -349,6 +365,13 @@ int tc_fwd_stages(int CT, int KAP, int K2, int kcw) {
   return NS;
 }
 
+#ifdef JTFS_TC_TRACE
+static const int g_trace_fwd_k = [] {
+  const char* e = std::getenv("JTFS_TRACE_K");
+  return e ? std::atoi(e) : 34;
+}();
+#endif
+
 // filter groups of a launch: fixed per block by the planner (about two waves of 148 SMs per signal),
 // independent of the batch so that micro-batching leaves every summation order, hence the bits, unchanged
 static int tc_groups(const TcClass& C, int B) {
@@ -382,7 +405,12 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
                 (part == nparts - 1 ? kPmFinish : 0);
       }
       TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
-               (int)p.L_fr.size(), shard, n_shards, wbuf, wb_sb, part, pmode, tc_groups(C, B)};
+               (int)p.L_fr.size(), shard, n_shards, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr};
+#ifdef JTFS_TC_TRACE
+      static long long* ftrace = nullptr;
+      if (!ftrace) cudaMalloc(&ftrace, 16 * 512 * 8);
+      if (C.Kmax == g_trace_fwd_k && part == 0) { cudaMemsetAsync(ftrace, 0, 16 * 512 * 8, st); a.trace = ftrace; }
+#endif
       // class = 8 * ct_kind + kap_kind (CT = 2 for ct_kind 0)
       switch (C.cls) {
         case 0: launch_tc<2, 2>(a, C, B, st); break;
@@ -394,6 +422,14 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
         case 11: launch_tc<1, 16>(a, C, B, st); break;
         case 12: launch_tc<1, 32>(a, C, B, st); break;
       }
+#ifdef JTFS_TC_TRACE
+      if (a.trace) {
+        static long long h[16 * 512];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
+        if (FILE* fo = fopen("gpurun_out/tc_trace_fwd.bin", "wb")) { fwrite(h, 1, sizeof(h), fo); fclose(fo); }
+      }
+#endif
     }
   }
 }
@@ -419,14 +455,7 @@ struct TcBwArgs {
   float2* gp; int64_t gp_sb;
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
 };
-#ifdef JTFS_TC_TRACE
-#define TC_TRACE(ev, g)                                                                  \
-  do {                                                                                   \
-    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (g) < 512) a.trace[(ev) * 512 + (g)] = clock64(); \
-  } while (0)
-#else
-#define TC_TRACE(ev, g) do {} while (0)
-#endif
+
 
 template <int KAP>
 __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS1, int STG1, int NS2, int STG2) {
