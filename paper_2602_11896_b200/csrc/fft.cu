@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 1) k_fft_colA(C* __r
 
 // ---------------------------------------------------------------- four-step B: rows, transposed out
 // For rows k1 in [k1_0, k1_0 + M): X[k1 + L1 k2] = sum_n2 y[k1][n2] W_L2^{n2 k2}.
-template <class C, class TO, int NPT>
-__global__ void __launch_bounds__(512) k_fft_rowB(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
+template <class C, class TO, int NPT, int NT>
+__global__ void __launch_bounds__(NT) k_fft_rowB(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
                                                   int L1, int lgM, int inv, double scale, const C* __restrict__ tw) {
   extern __shared__ __align__(16) uint8_t smraw[];
   constexpr int lgL2 = 12, L2 = 4096;
@@ -138,13 +138,13 @@ __global__ void __launch_bounds__(512) k_fft_rowB(const C* __restrict__ in, TO* 
   const int k10 = blockIdx.x * M;
   const C* src = in + b * ri.stride_b + ri.off + r * L + (int64_t)k10 * L2;
   TO* dst = out + b * ro.stride_b + ro.off + r * L;
-  load_twiddles<C, 512>(tws, tw, lgL2);
+  load_twiddles<C, NT>(tws, tw, lgL2);
   __syncthreads();
   const LdRows<C, C> ld{src, lgL2, M};
   const SeqCol<C> buf{s, L2};
-  seq_fft<C, 512, NPT>(lgM, lgL2, inv != 0, tws, lgL2, ld, buf, buf);
+  seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, lgL2, ld, buf, buf);
   const typename Cx<C>::R sc = (typename Cx<C>::R)scale;
-  for (int i = threadIdx.x; i < (L2 << lgM); i += 512) {
+  for (int i = threadIdx.x; i < (L2 << lgM); i += NT) {
     const int m = i & (M - 1), k2 = i >> lgM;
     const C v = buf(m, k2);
     dst[(int64_t)k2 * L1 + k10 + m] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
@@ -194,11 +194,13 @@ static int ilog2_exact(int64_t v) {
 template <class TI, class TO, class C>
 static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,
                                 cudaStream_t st) {
-  constexpr int kRowNPT = 16;                                  // rowB: 2 rows per CTA (2 CTAs per SM)
+  // rowB: 2 rows per CTA, 512 threads x 16 points (256 threads x 32 points measured slower)
+  constexpr int kRowNT = 512;
+  constexpr int kRowNPT = (2 * 4096) / kRowNT;
   constexpr int kRowLgM = 1;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fft_rowB<C, TO, kRowNPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fft_rowB<C, TO, kRowNPT, kRowNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(((4096 << kRowLgM) + 4096) * sizeof(C)));
     cudaFuncSetAttribute(k_fft_colA<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * sizeof(C)));
     cudaFuncSetAttribute(k_fft_small<TI, TO, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -231,7 +233,7 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
   {
     const int lgM = std::min(kRowLgM, lgL1);
     dim3 grid((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
-    k_fft_rowB<C, TO, kRowNPT><<<grid, 512, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
+    k_fft_rowB<C, TO, kRowNPT, kRowNT><<<grid, kRowNT, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
         reinterpret_cast<const C*>(in), out, ri, ro, L1, lgM, inverse ? 1 : 0, scale, tw);
   }
   count_launch(2);

@@ -50,7 +50,7 @@ __global__ void k_o1_W(const float* __restrict__ S1t, int64_t S1t_sb, float2* __
   if (i >= nrows[f]) return;
   const int kf = kf_of[f];
   const int64_t Lf = P >> kf;
-  const int64_t r = (rlo[f] + i) % Lf;
+  const int64_t r = (rlo[f] + i) & (Lf - 1);
   const int hb = (int)((r << kf) & (P - 1));
   const float* x = S1t + b * S1t_sb + t;
   const float2* h = hfr + (int64_t)f * P;
@@ -109,11 +109,11 @@ __global__ void k_o1_out(const float2* __restrict__ W1, int64_t W1_sb, const flo
     const float* g = phiF_k + phiF_off[kf];
     const float* v = V2 + b * V2_sb + (int64_t)f * P * frames + tp;
     double acc = 0;
-    for (int64_t i = 0; i < nrows[f]; ++i) {
-      int64_t r = (rlo[f] + i) % Lf;
-      int64_t e = ((rho << d) - r) % Lf;
-      if (e < 0) e += Lf;
-      acc += (double)__ldg(g + e) * (double)v[i * frames];
+    const int nr = (int)nrows[f], r0 = (int)rlo[f], Lm = (int)Lf - 1;   // L_f: power of two
+    for (int i = 0; i < nr; ++i) {
+      const int r = (r0 + i) & Lm;
+      const int e = (((int)rho << d) - r) & Lm;
+      acc += (double)__ldg(g + e) * (double)v[(int64_t)i * frames];
     }
     out = (float)acc;
   }
@@ -132,13 +132,12 @@ __global__ void k_o1_bwd_rows(const float* __restrict__ rres, int64_t r_sb, floa
   if (i >= nrows[f]) return;
   const int kf = kf_of[f], d = log2F - kf;
   const int64_t Lf = P >> kf;
-  const int64_t r = (rlo[f] + i) % Lf;
+  const int64_t r = (rlo[f] + i) & (Lf - 1);
   const float* g = phiF_k + phiF_off[kf];
   const float* rr = rres + b * r_sb + frames + (int64_t)f * rows1 * frames + tp;
   double acc = 0;
   for (int rho = 0; rho < rows1; ++rho) {
-    int64_t e = (((int64_t)rho << d) - r) % Lf;
-    if (e < 0) e += Lf;
+    const int64_t e = (((int64_t)rho << d) - r) & (Lf - 1);
     acc += (double)__ldg(g + e) * (double)rr[(int64_t)rho * frames];
   }
   V2[b * V2_sb + ((int64_t)f * P + i) * frames + tp] = (float)acc;

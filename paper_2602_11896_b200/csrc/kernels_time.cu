@@ -60,13 +60,12 @@ __global__ void __launch_bounds__(kGatherTile) k_gather(const TI* __restrict__ i
   const int64_t m = (tile - tiles[j]) * kGatherTile + threadIdx.x;
   if (m >= J.L_out) return;
   const TI* src = in + b * in_sb + J.in_off;
-  int64_t s = m - floor_div(m - J.lo, J.L_out) * J.L_out;  // smallest s >= lo with s = m mod L_out
+  // L_in, L_out: powers of two (grid lengths N_pad >> k)
+  int64_t s = J.lo + ((m - J.lo) & (J.L_out - 1));          // smallest s >= lo with s = m mod L_out
   R ax = 0, ay = 0;
   for (; s < J.lo + J.len; s += J.L_out) {
     const R h = (R)__ldg(vals + J.val_off + (s - J.lo));
-    int64_t si = s % J.L_in;
-    if (si < 0) si += J.L_in;
-    const TI v = src[si];
+    const TI v = src[s & (J.L_in - 1)];
     ax += h * (R)v.x;
     ay += h * (R)v.y;
   }
@@ -158,23 +157,21 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
   float2 acc = make_float2(0.f, 0.f);
   {
     const Support sp = phiT_sup[k1];
-    int64_t t = m - sp.lo;
-    t %= L1; if (t < 0) t += L1;
+    const int64_t t = (m - sp.lo) & (L1 - 1);                 // L1, Ft, T2: powers of two
     if (t < sp.len) {
       float h = __ldg(vals + sp.off + t);
-      float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m % Ft)];
+      float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m & (Ft - 1))];
       acc = make_float2(h * v.x, h * v.y);
     }
   }
   for (int bi = 0; bi < n_blocks; ++bi) {
     if (n1 >= nmax[bi]) continue;
     const Support sp = psi2_sup[bi * (log2T + 1) + k1];
-    int64_t t = m - sp.lo;
-    t %= L1; if (t < 0) t += L1;
+    const int64_t t = (m - sp.lo) & (L1 - 1);
     if (t < sp.len) {
       float h = __ldg(vals + sp.off + t);
       const BlockInfo bf = binfo[bi];
-      float2 v = GY[b * GY_sb + bf.y_off + (int64_t)n1 * bf.T2 + (m % bf.T2)];
+      float2 v = GY[b * GY_sb + bf.y_off + (int64_t)n1 * bf.T2 + (m & (bf.T2 - 1))];
       acc.x = fmaf(h, v.x, acc.x);
       acc.y = fmaf(h, v.y, acc.y);
     }
