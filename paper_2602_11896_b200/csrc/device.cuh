@@ -76,6 +76,7 @@ struct DeviceTables {
   TcUnit* tc_units = nullptr;
   std::vector<TcClass> tc;         // one launch per tensor-core block (forward)
   float* tc_img2 = nullptr;
+  float* tc_img1b = nullptr;
   std::vector<TcClass> tcb;        // one launch per tensor-core block (backward)
   // FFT route (kernels_frfft.cu)
   float* fr_spec = nullptr;

@@ -158,6 +158,7 @@ static void free_tables(DeviceTables* d) {
   }
   if (d->tc_img) cudaFree(d->tc_img);
   if (d->tc_img2) cudaFree(d->tc_img2);
+  if (d->tc_img1b) cudaFree(d->tc_img1b);
   for (auto& c : d->tcb) {
     if (c.blocks) cudaFree(c.blocks);
     if (c.tiles) cudaFree(c.tiles);
@@ -225,7 +226,7 @@ static cudaError_t upload(Plan& p) {
     }
   }
   // tensor-core classes (forward and backward)
-  UP(p.tc_img, tc_img); UP(p.tc_wts, tc_wts); UP(p.tc_units, tc_units); UP(p.tc_img2, tc_img2);
+  UP(p.tc_img, tc_img); UP(p.tc_wts, tc_wts); UP(p.tc_units, tc_units); UP(p.tc_img2, tc_img2); UP(p.tc_img1b, tc_img1b);
   // one launch per tensor-core block: each sizes its pipeline for its own K
   auto build_classes = [&](const std::vector<TcBlock>& src, std::vector<TcClass>* out, bool fwd) -> cudaError_t {
     for (auto& tb : src) {

@@ -104,7 +104,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // logical warp roles: 0 producer, 1 MMA issuer, 4.. epilogue. The epilogue occupies the LOW physical
+  // warps so the producer and the MMA issuer get the higher warp ids, which the scheduler favours
+  // (highest-id-first arbitration): otherwise the busy epilogue warps starve the issuing warp.
+  const int tid = threadIdx.x, lane = tid & 31, pw = tid >> 5;
+  const int warp = pw >= 8 ? pw - 8 : pw + 4;
   const int jb = 0;                                         // one block per launch
   const int ntl = (int)(a.tiles[1] - a.tiles[0]);
   const int ct = (int)blockIdx.x % ntl, grp = (int)blockIdx.x / ntl;
@@ -444,7 +448,8 @@ struct TcBwArgs {
   const JointUnit* units; const BlockInfo* binfo;
   const TcBlock* blocks; const int64_t* tiles; int n_tc_blocks;
   const float* img;                 // forward B images (64-row tiles, kcw-wide chunks)
-  const float* img2;                // backward B2 images [unit][tile32][chunk][hi|lo][N2 x 16]
+  const float* img2;                // backward B2 images [unit][tile32][chunk][hi|lo][N2 x kb2]
+  const float* img1b;               // backward GEMM1 images [unit][tile32][chunk][hi|lo][64 x kc]
   const float* wts;
   const TcUnit* tcu;
   int nfr, shard, n_shards;
@@ -463,7 +468,10 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   __shared__ uint64_t full1[kTcMaxStages], empty1[kTcMaxStages], full2[kTcMaxStages2], empty2[kTcMaxStages2];
   __shared__ uint64_t tfull[2], tempty[2], a2full[2], a2empty[2], d2full;
   __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // logical warp roles: 0/2 producers, 1/3 MMA issuers, 4.. epilogue (epilogue on the low physical warps so
+  // the producers and issuers get the higher, favoured warp ids; see the forward kernel)
+  const int tid = threadIdx.x, lane = tid & 31, pw = tid >> 5;
+  const int warp = pw >= kBwEpiWarps ? pw - kBwEpiWarps : pw + 4;
   const int jb = 0;                                     // one block per launch
   const int ntl = (int)(a.tiles[1] - a.tiles[0]);
   const int ct = (int)blockIdx.x % ntl, grp = (int)blockIdx.x / ntl;
@@ -545,23 +553,21 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       const int NT32 = (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
       for (int t32 = 0; t32 < NT32; ++t32) {
         if (p1) {
-          // half (rows 32*(t32&1) ..) of the forward 64-row image, every chunk: [hi half | lo half]
-          const float* src = a.img + tu.img_off + (int64_t)(t32 >> 1) * (2 * kTcN * K2);
-          const int half = t32 & 1;
+          // 32-row tile t32 of the backward GEMM1 images, every chunk [hi 64 x kc | lo 64 x kc]: one bulk
+          // copy per chunk (each copy costs the SM's copy engine ~400 cycles whatever its size)
+          const float* src = a.img1b + tu.img1b_off + (int64_t)t32 * (2 * kBwN1 * K2);
           for (int ch = 0; ch < nchunks; ++ch) {
             const int kc = min(kcw, K2 - ch * kcw);
-            const uint32_t hb = (uint32_t)(kBwN1 * kc * 4);
+            const uint32_t bytes = (uint32_t)(2 * kBwN1 * kc * 4);
             tc::mbar_wait(&empty1[stage], ph ^ 1);
             if ((a.expt & 2) && t32 > 0) {
               if (tc::elect_one()) tc::mbar_arrive(&full1[stage]);
             } else if (tc::elect_one()) {
-              tc::mbar_expect_tx(&full1[stage], 2 * hb);
-              float* dst = bst1 + stage * STG1;
-              tc::bulk_g2s(dst, src + half * kBwN1 * kc, hb, &full1[stage]);
-              tc::bulk_g2s(dst + kBwN1 * kc, src + kTcN * kc + half * kBwN1 * kc, hb, &full1[stage]);
+              tc::mbar_expect_tx(&full1[stage], bytes);
+              tc::bulk_g2s(bst1 + stage * STG1, src, bytes, &full1[stage]);
             }
             __syncwarp();
-            src += 2 * kTcN * kc;
+            src += 2 * kBwN1 * kc;
             if (++stage == NS1) { stage = 0; ph ^= 1; }
           }
         } else {
@@ -913,7 +919,7 @@ void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
     const cudaStream_t st = ss[li++ % ns];
     if (C.n_blocks == 0) continue;
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
-               d.tc_img2, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, wbuf, wb_sb,
+               d.tc_img2, d.tc_img1b, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, wbuf, wb_sb,
                tc_groups(C, B), gp, gp_sb, nullptr};
 #ifdef JTFS_TC_TRACE
     static long long* trace = nullptr;

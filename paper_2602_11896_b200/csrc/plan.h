@@ -59,6 +59,7 @@ struct BlockInfo {
 struct TcUnit {
   int64_t img_off, wt_off;   // offsets (floats) of the unit's B images / phi_F weights
   int64_t img2_off;          // offset of the backward B2 images (32-row tiles)
+  int64_t img1b_off;         // offset of the backward GEMM1 images (32-row tiles, [hi 64 x kc | lo 64 x kc])
   int32_t NT;                // row tiles of 64 (0 = unit not on the tensor-core path)
   int32_t wp_tile0;          // split-K blocks: index of the unit's first 64-row tile in the block's W buffer
 };
@@ -141,7 +142,7 @@ struct Plan {
   std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class)
   int64_t ks_w_floats = 0;                      // per-signal W buffer of the split-K blocks
   int64_t gp_complex = 0;                       // per-signal g_Y2 partials of the filter-group split
-  std::vector<float> tc_img, tc_wts, tc_img2;
+  std::vector<float> tc_img, tc_wts, tc_img2, tc_img1b;
   // FFT route of the joint stage (kernels_frfft.cu)
   std::vector<float> fr_spec;                   // [n_fr_all][P] level-0 responses of L_fr on the P grid
   std::vector<float> u_wts;                     // per unit [rows_out][n_rows] phi_F weights

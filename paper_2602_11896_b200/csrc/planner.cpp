@@ -159,7 +159,7 @@ static uint32_t core_off_host(uint32_t r, uint32_t k, uint32_t Kc) {
 // hi/lo, in K-chunks of 32 in the canonical K-major layout; plus the phi_F weights per row.
 static void build_tc_tables(Plan* p) {
   const int nfr = (int)p->L_fr.size();
-  p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0, 0});
+  p->tc_units.assign(p->units.size(), TcUnit{0, 0, 0, 0, 0, 0});
   p->blk_tc.assign(p->blocks.size(), 0);
   p->blk_tcb.assign(p->blocks.size(), 0);
   p->blk_ks.assign(p->blocks.size(), 0);
@@ -271,6 +271,32 @@ static void build_tc_tables(Plan* p) {
               // Re W = Re M Re Y - Im M Im Y ; Im W = Im M Re Y + Re M Im Y
               const double v = (po == 0) ? ((pi == 0) ? mr : -mi) : ((pi == 0) ? mi : mr);
               put(p->tc_img, base, base + 128 * kc, core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kc) / 4, v);
+            }
+          }
+        }
+      }
+      // backward GEMM1 images: per 32-row tile, per kcw-wide chunk: [hi 64 x kc | lo 64 x kc] (the forward
+      // image rows of that half tile, contiguous so one bulk copy moves a chunk)
+      if (bwd && !ks) {
+        tu.img1b_off = (int64_t)p->tc_img1b.size();
+        const int NT32 = (int)((U.n_rows + 31) / 32);
+        for (int t = 0; t < NT32; ++t) {
+          for (int ch = 0; ch * kcw < K2; ++ch) {
+            const int kc = std::min(kcw, K2 - ch * kcw);
+            const size_t base = p->tc_img1b.size();
+            p->tc_img1b.resize(base + 2 * 64 * kc, 0.f);
+            for (int nn = 0; nn < 64; ++nn) {
+              const int i = nn / 2, po = nn % 2;
+              const int64_t lr = (int64_t)t * 32 + i;
+              if (lr >= U.n_rows) continue;
+              for (int kl = 0; kl < kc; ++kl) {
+                const int kk = ch * kcw + kl, n = kk / 2, pi = kk % 2;
+                if (n >= K) continue;
+                double mr, mi;
+                Mval(lr, n, &mr, &mi);
+                const double v = (po == 0) ? ((pi == 0) ? mr : -mi) : ((pi == 0) ? mi : mr);
+                put(p->tc_img1b, base, base + 64 * kc, core_off_host((uint32_t)nn, (uint32_t)kl, (uint32_t)kc) / 4, v);
+              }
             }
           }
         }

@@ -51,6 +51,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// polling variant (mbarrier.test_wait never suspends the thread): for the MMA issuers, whose waits sit
+// on the tensor pipe's critical path
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_SPIN:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra LAB_SPIN;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- bulk async copy global -> smem
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
