@@ -179,8 +179,9 @@ static void build_tc_tables(Plan* p) {
     const int CT = (K2 <= 64 && kap <= 2) ? 2 : 1;
     if (K2 <= 168 && kap <= 2) {
       // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
+      // (each bulk copy costs the copy engine ~400 cycles whatever its size: one copy per tile if possible)
       for (int w : {K2, 64, 32}) {
-        if (w > 64 || w > K2) continue;
+        if (w > 128 || w > K2) continue;
         if (tc_fwd_stages(CT, 2 << kap, K2, w) >= 3) { kcw = w; break; }
       }
     } else {
