@@ -199,12 +199,22 @@ static void build_tc_tables(Plan* p) {
     }
     p->blk_tc[bi] = 1;
     p->blk_ks[bi] = (char)ks;
-    // widest B2 chunk whose rings fit (fewer chunk hand-offs per tile)
-    int kb2 = 8;
-    for (int w : {64, 32, 16, 8}) {
-      int ns1, s1, ns2, s2;
-      tc_bwd_rings(K, ks ? 0 : K2, kcw, w, &ns1, &s1, &ns2, &s2);
-      if (ks ? ns2 >= 3 : (ns1 >= 2 && ns2 * w >= 128 + w)) { kb2 = w; break; }
+    // backward chunk widths: GEMM1 images (kcwb, own layout) and B2 images (kb2), chosen for the fewest bulk
+    // copies per 32-row tile (each costs the copy engine ~400 cycles) with ring 1 >= 2 stages and ring 2
+    // holding >= 2 tiles; split-K blocks have no GEMM1
+    int kb2 = 8, kcwb = kcw, best = 1 << 30, best_depth = 0;
+    for (int wb : {K2, 64, 32, 16}) {
+      if (wb > 128 || wb > K2 || wb % 8) continue;
+      for (int w : {64, 32, 16, 8}) {
+        int ns1, s1, ns2, s2;
+        tc_bwd_rings(K, ks ? 0 : K2, wb, w, &ns1, &s1, &ns2, &s2);
+        const bool ok = ks ? ns2 >= 3 : (ns1 >= 2 && ns2 >= 2);
+        if (!ok) continue;
+        // copies per tile, plus a penalty when ring 2 holds less than two tiles of lookahead
+        const int cost = (ks ? 0 : (K2 + wb - 1) / wb) + 64 / w + (ns2 * w < 128 ? 2 : 0);
+        if (cost < best || (cost == best && ns2 * w > best_depth)) { best = cost; best_depth = ns2 * w; kb2 = w; kcwb = wb; }
+      }
+      if (ks) break;
     }
     int wp_tiles = 0;
     for (int f = 0; f < nfr; ++f) wp_tiles += (int)((p->units[bi * nfr + f].n_rows + 63) / 64);
@@ -221,13 +231,13 @@ static void build_tc_tables(Plan* p) {
     p->tc_blocks.push_back({(int32_t)bi, K, K2, 8 * (CT == 2 ? 0 : 1) + kap, kcw, kb2, ks, nparts, kpw, wp_tiles,
                             wp_off, ngmax, 0, 0});
     int ns1, s1, ns2, s2;
-    tc_bwd_rings(K, ks ? 0 : K2, kcw, kb2, &ns1, &s1, &ns2, &s2);
-    const bool bwd = ks ? ns2 >= 2 : (N2 <= 256 && ns1 >= 2 && ns2 >= 2);
+    tc_bwd_rings(K, ks ? 0 : K2, kcwb, kb2, &ns1, &s1, &ns2, &s2);
+    const bool bwd = best < (1 << 30) && (ks ? ns2 >= 2 : (N2 <= 256 && ns1 >= 2 && ns2 >= 2));
     if (bwd) {
       p->blk_tcb[bi] = 1;
       const int ngb =
           (int)std::min<int64_t>(nfr, std::max<int64_t>(1, (296 + n_ct * kRefBatch - 1) / (n_ct * kRefBatch)));
-      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcw, kb2, ks, nparts, kpw, wp_tiles, wp_off, ngb, 0,
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcwb, kb2, ks, nparts, kpw, wp_tiles, wp_off, ngb, 0,
                                ngb > 1 ? p->gp_complex : 0});
       if (ngb > 1) p->gp_complex += (int64_t)ngb * K * p->binfo[bi].n_cols;
     }
@@ -282,8 +292,8 @@ static void build_tc_tables(Plan* p) {
         tu.img1b_off = (int64_t)p->tc_img1b.size();
         const int NT32 = (int)((U.n_rows + 31) / 32);
         for (int t = 0; t < NT32; ++t) {
-          for (int ch = 0; ch * kcw < K2; ++ch) {
-            const int kc = std::min(kcw, K2 - ch * kcw);
+          for (int ch = 0; ch * kcwb < K2; ++ch) {
+            const int kc = std::min(kcwb, K2 - ch * kcwb);
             const size_t base = p->tc_img1b.size();
             p->tc_img1b.resize(base + 2 * 64 * kc, 0.f);
             for (int nn = 0; nn < 64; ++nn) {
@@ -291,7 +301,7 @@ static void build_tc_tables(Plan* p) {
               const int64_t lr = (int64_t)t * 32 + i;
               if (lr >= U.n_rows) continue;
               for (int kl = 0; kl < kc; ++kl) {
-                const int kk = ch * kcw + kl, n = kk / 2, pi = kk % 2;
+                const int kk = ch * kcwb + kl, n = kk / 2, pi = kk % 2;
                 if (n >= K) continue;
                 double mr, mi;
                 Mval(lr, n, &mr, &mi);
