@@ -177,7 +177,12 @@ static void build_tc_tables(Plan* p) {
     // resident A tile (128 x K2 x 8 B) when it fits with >= 3 B stages, else split-K parts
     int ks = 0, nparts = 1, kpw = K2, kcw = 16;
     const int CT = (K2 <= 64 && kap <= 2) ? 2 : 1;
-    if (K2 <= 168 && kap <= 2) {
+    // resident Y2 tile when it fits the TMEM (TS form) or two column tiles share the B stream (K2 <= 64);
+    // else the tile in SMEM (SS form) while it fits (K2 <= 168); larger K goes split-K: the forward's parts
+    // stay in the TS form and the backward reads the forward's W instead of recomputing GEMM1. (Measured
+    // at c2: converting the K2 = 136 / 168 blocks to split-K costs more in W traffic, 24 B per cell over
+    // two parts, than it saves.)
+    if (kap <= 2 && (CT == 2 || tc_fwd_tsa(1, K2) || K2 <= 168)) {
       // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
       // (each bulk copy costs the copy engine ~400 cycles whatever its size: one copy per tile if possible)
       for (int w : {K2, 64, 32}) {
@@ -186,15 +191,23 @@ static void build_tc_tables(Plan* p) {
       }
     } else {
       ks = 1;
-      // fewest K parts whose A tile fits TMEM (TS-form MMAs); else the fewest with >= 3 SMEM stages
-      int np_ss = 0;
-      for (nparts = 2; nparts <= 8; ++nparts) {
-        kpw = ((K2 + nparts - 1) / nparts + kcw - 1) / kcw * kcw;
-        if (tc_fwd_stages(1, 2 << kap, kpw, kcw) < 3) continue;
-        if (!np_ss) np_ss = nparts;
-        if (tc_fwd_tsa(1, kpw)) break;
+      // fewest balanced K parts whose A tile fits TMEM (TS-form MMAs), each part m whole chunks with the
+      // fewest chunks (m) that leave >= 3 stages
+      int best_np = 0, best_w = 16;
+      for (int np = 2; np <= 8 && !best_np; ++np) {
+        const int kp0 = ((K2 + np - 1) / np + 7) / 8 * 8;
+        for (int m = 1; m <= 4; ++m) {
+          const int w = ((kp0 + m - 1) / m + 7) / 8 * 8;
+          if (tc_fwd_tsa(1, m * w) && tc_fwd_stages(1, 2 << kap, m * w, w) >= 3 && (np - 1) * m * w < K2) {
+            best_np = np;
+            best_w = w;
+            break;
+          }
+        }
       }
-      if (nparts > 8) nparts = np_ss;
+      if (!best_np) { best_np = (K2 + 127) / 128; best_w = 16; }
+      nparts = best_np;
+      kcw = best_w;
       kpw = ((K2 + nparts - 1) / nparts + kcw - 1) / kcw * kcw;
     }
     p->blk_tc[bi] = 1;
@@ -208,7 +221,7 @@ static void build_tc_tables(Plan* p) {
       for (int w : {64, 32, 16, 8}) {
         int ns1, s1, ns2, s2;
         tc_bwd_rings(K, ks ? 0 : K2, wb, w, &ns1, &s1, &ns2, &s2);
-        const bool ok = ks ? ns2 >= 3 : (ns1 >= 2 && ns2 >= 2);
+        const bool ok = ks ? ns2 >= 2 : (ns1 >= 2 && ns2 >= 2);
         if (!ok) continue;
         // copies per tile, plus a penalty when ring 2 holds less than two tiles of lookahead
         const int cost = (ks ? 0 : (K2 + wb - 1) / wb) + 64 / w + (ns2 * w < 128 ? 2 : 0);
