@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   const int K2 = TB.ks ? min(TB.kpw, TB.K2 - kp_lo) : TB.K2;
   const int pmode = TB.ks ? a.pmode : kPmFinish;
   const bool tsa = tc_fwd_tsa(CT, K2);                     // A in TMEM (TS-form MMAs)
+  const int nbuf = tc_fwd_nbuf(CT, K2);                    // TMEM accumulator buffers
   float* a_hi = reinterpret_cast<float*>(sm);              // [CT][128][K2] canonical (SS form)
   float* a_lo = a_hi + CT * 128 * K2;
   float* bst = tsa ? a_hi : a_lo + CT * 128 * K2;           // NS stages x STG floats
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   tc::tc_fence_after();
   const uint32_t tbase = tmem_base;
   // TS form: A hi at TMEM columns [256, 256 + K2), lo at [256 + K2, 256 + 2 K2)
-  const uint32_t taa_hi = tbase + 256, taa_lo = taa_hi + (uint32_t)K2;
+  const uint32_t taa_hi = tbase + 128 * (uint32_t)nbuf, taa_lo = taa_hi + (uint32_t)K2;
   if (tsa) {
     if (warp >= 4 && warp < 8) {
       const uint32_t lq = (uint32_t)((warp & 3) * 32) << 16;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         __syncwarp();
         if (lane == 0) TC_TRACE(2, gt);
         ++gt;
-        if (++buf == 2) { buf = 0; bph ^= 1; }
+        if (++buf == nbuf) { buf = 0; bph ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         if (warp == 4 && lane == 0) TC_TRACE(6, ge);
         ++ge;
-        if (++buf == 2) { buf = 0; bph ^= 1; }
+        if (++buf == nbuf) { buf = 0; bph ^= 1; }
       }
       if (!(pmode & kPmFinish)) continue;
       // combine the two row halves in a fixed order, write o[rho][col]

@@ -100,7 +100,14 @@ inline
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-bool tc_fwd_tsa(int CT, int K2) { return CT == 1 && 256 + 2 * K2 <= 512; }
+bool tc_fwd_tsa(int CT, int K2) { return CT == 1 && 128 + 2 * K2 <= 512; }
+// accumulator buffers of the forward: 2 (epilogue of tile t overlaps the MMAs of tile t + 1) unless the TS
+// form only fits beside a single one (K2 > 128)
+inline
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+int tc_fwd_nbuf(int CT, int K2) { return (tc_fwd_tsa(CT, K2) && 256 + 2 * K2 > 512) ? 1 : 2; }
 
 struct DeviceTables;  // device pointers (jtfs_api.cu)
 

@@ -198,7 +198,8 @@ static void build_tc_tables(Plan* p) {
         const int kp0 = ((K2 + np - 1) / np + 7) / 8 * 8;
         for (int m = 1; m <= 4; ++m) {
           const int w = ((kp0 + m - 1) / m + 7) / 8 * 8;
-          if (tc_fwd_tsa(1, m * w) && tc_fwd_stages(1, 2 << kap, m * w, w) >= 3 && (np - 1) * m * w < K2) {
+          if (tc_fwd_tsa(1, m * w) && tc_fwd_nbuf(1, m * w) == 2 && tc_fwd_stages(1, 2 << kap, m * w, w) >= 3 &&
+              (np - 1) * m * w < K2) {
             best_np = np;
             best_w = w;
             break;
