@@ -291,9 +291,21 @@ def main() -> None:
                    "ideal_ms_per_step": 1000.0 * ideal / args.steps}
     dom = max(kern, key=lambda k: kern[k]["ms_per_step"]) if kern else None
     roof = dict(kern[dom]) if dom else {}
+    # DRAM traffic of the dominant group per step, from the committed ncu --set full capture of the same
+    # command (tools/gpu_session.sh traffic -> profiles/traffic_<config>.json), when one exists
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if dom and os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            traffic = {"bytes_per_step": tj[dom]["dram_bytes_per_step"],
+                       "bytes_per_step_per_signal": tj[dom]["dram_bytes_per_step"] / B,
+                       "source": os.path.relpath(tpath, ROOT)}
+        except Exception:
+            traffic = None
     roof.update({"kernel": {"joint_bwd": "k_joint_bwd_tc + k_joint_bwd_fft (concurrent)",
                             "joint_fwd": "k_joint_fwd_tc + k_joint_fwd_fft (concurrent)"}.get(dom, dom),
-                 "traffic": None, "share_of_step": roof.get("ms_per_step", 0) / (ms / args.steps) if ms else None,
+                 "traffic": traffic, "share_of_step": roof.get("ms_per_step", 0) / (ms / args.steps) if ms else None,
                  "peak_note": ("TF32 dense = measured bf16 %.0f TF x 1.1/2.25 (guide nominal ratio); 3xTF32 "
                                "counts 3 MMAs; FFT route against FP32 = 148 SM x 128 lanes x 2 x %.0f MHz, "
                                "folded into TF32-equivalent time" % (float(pk.get("bf16_tflops", 1590.0)), clock_mhz)),
