@@ -20,7 +20,8 @@ def main(rep, config, nf, nb, out):
                       h.index("gpu__time_duration.sum"))
     units = rows[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
-    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6,
+              "ms": 1e-3, "s": 1.0}
     g = {"joint_fwd": [0.0, 0.0, 0], "joint_bwd": [0.0, 0.0, 0]}
     for r in rows[2:]:
         name = r[ki]
