@@ -140,6 +140,34 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_metamer(plan, args, dev) -> dict:
+    """Metamer synthesis: y0 = white noise at the target's RMS, then
+    --metamer bold-driver momentum steps (m = 0.9, mu0 = 0.1), all on the device. Reports steps/s (CUDA
+    events around the loop) and the mean loss every 10 steps."""
+    import torch
+    cfg = CONFIGS[args.config]
+    B = args.batch or cfg["B"]
+    x = torch.from_numpy(batch(args.config, B)).to(dev)
+    y0 = torch.from_numpy(batch(args.config, B, which="y")).to(dev)
+    St = plan.forward(x)
+    st = plan.metamer_state(y0)
+    ws = plan.workspace(B, True, dev)
+    curve = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for it in range(args.metamer):
+        plan.metamer_step(st, St, ws=ws)
+        if it % 10 == 0 or it == args.metamer - 1:
+            curve.append([it, float(st["loss"].mean())])   # host read: outside the timed work's critical path
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"steps": args.metamer, "steps_per_s": args.metamer / (ms / 1000.0), "ms_per_step": ms / args.metamer,
+            "batch": B, "loss_curve_mean": curve, "final_over_initial": curve[-1][1] / max(curve[0][1], 1e-30),
+            "accepted_last": int(st["accepted"].sum())}
+
+
 def _describe(c: str) -> str:
     d = CONFIGS[c]
     return (f"B={d['B']} N={d['N']} J={d['J']} Q={d['Q']} J_fr={d['J_fr']} Q_fr={d['Q_fr']} "
@@ -156,6 +184,9 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--metamer", type=int, default=0,
+                    help="also run this many metamer_step iterations (BASELINE configs[2]: c3, 100) from white-noise "
+                         "init and report steps/s and the loss curve under the 'metamer' key")
     ap.add_argument("--path-shards", type=int, default=1,
                     help="ranks per path group (order-2 units split, dE/dx all-reduced over NVLink)")
     args = ap.parse_args()
@@ -322,6 +353,8 @@ def main() -> None:
     }
     if e2e:
         line["e2e"] = e2e
+    if args.metamer > 0:
+        line["metamer"] = run_metamer(plan, args, dev)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)
