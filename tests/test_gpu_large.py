@@ -61,3 +61,24 @@ def test_large_forward_and_gradient(name):
     Eo, go = o.loss_grad_subset(y, So[None], blocks)
     assert rel(loss.cpu().numpy(), Eo.numpy()) <= 1e-4
     assert rel(g.cpu().numpy(), go.numpy()) <= 1e-3
+
+
+def test_split_k_shards_and_microbatch():
+    """c2 exercises the split-K tensor-core blocks (W kept by the forward, GEMM2-only backward) and the
+    filter-group split with g_Y2 partials: per-signal results are bitwise independent of the micro-batch,
+    and path shards sum to the whole (only fp32 summation order differs)."""
+    from paper_2602_11896_b200 import Plan
+    p = Plan(*plan_args(CONFIGS["c2"]))
+    x = torch.from_numpy(batch("c2", 2)).cuda()
+    y = torch.from_numpy(batch("c2", 2, which="y")).cuda()
+    S = p.forward(x)
+    loss, g = p.loss_grad(y, S)
+    ws = torch.empty(p.workspace_size(1, True), dtype=torch.uint8, device="cuda")
+    l1, g1 = p.loss_grad(y, S, ws=ws)
+    assert torch.equal(g1, g) and torch.equal(l1, loss)
+    ls, gs = 0, 0
+    for sh in range(2):
+        l_, g_ = p.loss_grad(y, S, shard=sh, n_shards=2)
+        ls, gs = ls + l_, gs + g_
+    assert rel(gs.cpu().numpy(), g.cpu().numpy()) <= 1e-5
+    assert rel(ls.cpu().numpy(), loss.cpu().numpy()) <= 1e-5
