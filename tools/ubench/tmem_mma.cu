@@ -171,6 +171,43 @@ __global__ void __launch_bounds__(160, 1) k_contend(long long* out, int iters, i
   if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
+// per-instruction timing of the MMA-issue path: n MMAs (N=128, TS) then commit, then a try_wait on an
+// already-completed mbarrier, then the wait for the commit
+__global__ void __launch_bounds__(128, 1) k_issue(long long* out, int n) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t bar, done_bar;
+  const int warp = threadIdx.x >> 5;
+  float* B = reinterpret_cast<float*>(sm);
+  for (int i = threadIdx.x; i < 128 * 64 * 2; i += 128) B[i] = 0.f;
+  if (threadIdx.x == 0) { tc::mbar_init(&bar, 1); tc::mbar_init(&done_bar, 1); tc::fence_mbar_init(); }
+  if (warp == 0) tc::tmem_alloc(&tbase, 512);
+  tc::fence_async_smem();
+  tc::tc_fence_before(); __syncthreads(); tc::tc_fence_after();
+  if (threadIdx.x == 0) tc::mbar_arrive(&done_bar);   // completes phase 0
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t dB = tc::sdesc(tc::smem_u32(B), 128, 64 * 32);
+    const uint32_t idesc = tc::idesc_tf32(128, 128);
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    if (tc::elect_one()) {
+      t0 = clock64();
+      for (int i = 0; i < n; ++i) tc::mma_tf32_ts(tbase, tbase + 256 + 8u * (i & 7), dB + 16u * (i & 7), idesc, 1u);
+      t1 = clock64();
+      tc::mma_commit(&bar);
+      t2 = clock64();
+    }
+    __syncwarp();
+    tc::mbar_wait(&done_bar, 0);   // already complete
+    t3 = clock64();
+    tc::mbar_wait(&bar, 0);
+    t4 = clock64();
+    if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = t4 - t3; }
+  }
+  tc::tc_fence_before(); __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
 int main() {
   long long* d; cudaMalloc(&d, 2000 * 8);
   long long h[148];
@@ -206,6 +243,16 @@ int main() {
     cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
     printf("pingpong (%d MMA N=64 + commit -> ld 32 / st 64 cols -> arrive): %.1f cycles/round (err %s)\n", nm,
            (double)h[0] / it, cudaGetErrorString(cudaGetLastError()));
+  }
+  cudaFuncSetAttribute(k_issue, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int n : {1, 4, 8, 16, 30, 60}) {
+    k_issue<<<1, 128, 200 * 1024>>>(d, n);
+    cudaDeviceSynchronize();
+    k_issue<<<1, 128, 200 * 1024>>>(d, n);
+    long long hh[4];
+    cudaMemcpy(hh, d, 4 * 8, cudaMemcpyDeviceToHost);
+    printf("issue %2d TS N=128 MMAs: issue %lld cyc, commit %lld, wait(complete bar) %lld, wait(commit) %lld (%s)\n", n,
+           hh[0], hh[1], hh[2], hh[3], cudaGetErrorString(cudaGetLastError()));
   }
   cudaFuncSetAttribute(k_contend, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int epi = 0; epi < 2; ++epi) {
