@@ -202,8 +202,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer (warp-uniform loop, one elected lane issues)
+  } else if (warp == 1 || (warp == 3 && nbuf == 2)) {
+    // ===================== MMA issuers (warp-uniform loops, one elected lane issues). The tensor pipe's
+    // issue queue holds only ~3 MMAs (~200 cycles of N=128 work) while a commit plus a barrier wait costs
+    // ~200 cycles even when the phase has completed (tools/ubench/tmem_mma.cu k_issue), so one issuer
+    // drains the pipe at every chunk and tile boundary. With two accumulator buffers, warp 1 issues the
+    // even tiles (buffer 0) and warp 3 the odd ones (buffer 1): one's waits overlap the other's MMAs.
+    const int nis = nbuf == 2 ? 2 : 1, q = warp == 3 ? 1 : 0;
     const uint32_t idesc = tc::idesc_tf32(128, kTcN);
     const uint32_t sboA = (uint32_t)K2 * 32u;
     // descriptors differ only in the start-address field: add (byte offset >> 4) to the low word
@@ -211,13 +216,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     const uint64_t dA_lo = tc::sdesc(tc::smem_u32(a_lo), 128, sboA);
     const uint32_t aStepM = (uint32_t)(128 * K2 * 4) >> 4;
     const uint32_t bst_s = tc::smem_u32(bst);
-    int stage = 0, buf = 0, gt = 0;
+    int stage = 0, gt = 0;
+    const int buf = q;
     uint32_t ph = 0, bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
       if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       for (int t = 0; t < tu.NT; ++t) {
+        if (gt % nis != q) {   // the other issuer's tile: skip its chunks in the ring
+          for (int ch = 0; ch < nchunks; ++ch)
+            if (++stage == NS) { stage = 0; ph ^= 1; }
+          ++gt;
+          continue;
+        }
         tc::mbar_wait(&tempty[buf], bph ^ 1);
         tc::tc_fence_after();
         if (lane == 0) TC_TRACE(0, gt);
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         __syncwarp();
         if (lane == 0) TC_TRACE(2, gt);
         ++gt;
-        if (++buf == nbuf) { buf = 0; bph ^= 1; }
+        bph ^= 1;
       }
     }
   } else if (warp >= 4) {
