@@ -26,20 +26,20 @@ namespace jtfs {
 
 template <class C> struct FftTw;
 template <> struct FftTw<float2> {
-  static const float2* base(const FftTables& t) { return t.tw; }
+  static const float2* base(const FftTables& t) { return t.twp; }
   static const float2* lo(const FftTables& t, int lg) { return t.lo_f[lg]; }
   static const float2* hi(const FftTables& t, int lg) { return t.hi_f[lg]; }
 };
 template <> struct FftTw<double2> {
-  static const double2* base(const FftTables& t) { return t.twd; }
+  static const double2* base(const FftTables& t) { return t.twpd; }
   static const double2* lo(const FftTables& t, int lg) { return t.lo_d[lg]; }
   static const double2* hi(const FftTables& t, int lg) { return t.hi_d[lg]; }
 };
 
-// SMEM twiddle table W_L^e, e < L = 2^lgL, from the global 4096-entry table
+// SMEM copy of the per-pass twiddle table of length L = 2^lgL (fft_pass_tables; cf_pass with lgT = -1)
 template <class C, int NT>
 __device__ __forceinline__ void load_twiddles(C* tws, const C* __restrict__ tw, int lgL) {
-  for (int e = threadIdx.x; e < (1 << lgL); e += NT) tws[e] = tw[e << (12 - lgL)];
+  for (int e = threadIdx.x; e < (1 << lgL); e += NT) tws[e] = tw[(1 << lgL) + e];
 }
 
 // ---------------------------------------------------------------- L <= 4096: 4096 / L rows per CTA
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) k_fft_small(const TI* __restrict__ in, TO
   const LdRows<TI, C> ld{in + b * ri.stride_b + ri.off + (r0 << lgL), lgL, rows};
   const StRows<TO, C> st{out + b * ro.stride_b + ro.off + (r0 << lgL), lgL, rows, (typename Cx<C>::R)scale};
   const SeqCol<C> buf{s, 1 << lgL};
-  seq_fft<C, 256, 16>(lgM, lgL, inv != 0, tws, lgL, ld, st, buf);
+  seq_fft<C, 256, 16>(lgM, lgL, inv != 0, tws, -1, ld, st, buf);
 }
 
 // ---------------------------------------------------------------- four-step A: columns
@@ -103,7 +103,7 @@ struct StColsTw {
 };
 
 template <class C>
-__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 1) k_fft_colA(C* __restrict__ data, Rows ri, int lgL1, int L2, int lgCW, int inv,
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) k_fft_colA(C* __restrict__ data, Rows ri, int lgL1, int L2, int lgCW, int inv,
                                                   const C* __restrict__ tw, const C* __restrict__ lo,
                                                   const C* __restrict__ hi) {
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 1) k_fft_colA(C* __r
   const LdCols<C> ld{base, L2};
   const StColsTw<C> st{base, L2, c0, inv, lo, hi};
   const SeqInter<C> buf{s, 1 << lgCW};
-  seq_fft<C, 256, 16>(lgCW, lgL1, inv != 0, tws, lgL1, ld, st, buf);
+  seq_fft<C, 256, 16>(lgCW, lgL1, inv != 0, tws, -1, ld, st, buf);
 }
 
 // ---------------------------------------------------------------- four-step B: rows, transposed out
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(NT) k_fft_rowB(const C* __restrict__ in, TO* _
   __syncthreads();
   const LdRows<C, C> ld{src, lgL2, M};
   const SeqCol<C> buf{s, L2};
-  seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, lgL2, ld, buf, buf);
+  seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, -1, ld, buf, buf);
   const typename Cx<C>::R sc = (typename Cx<C>::R)scale;
   for (int i = threadIdx.x; i < (L2 << lgM); i += NT) {
     const int m = i & (M - 1), k2 = i >> lgM;
@@ -163,6 +163,29 @@ static std::vector<T> twiddles() {
   return t;
 }
 std::vector<float2> fft_twiddle_table() { return twiddles<float2>(); }
+
+template <class T>
+static std::vector<T> pass_tables() {
+  std::vector<T> t(2 * kTw);
+  for (int lg = 1; lg <= 12; ++lg) {
+    T* tab = t.data() + (1 << lg);
+    const int n16 = lg / 4, rem = lg - 4 * n16;
+    int Ns = 1;
+    for (int p = 0; p < n16 + (rem ? 1 : 0); ++p) {
+      const int R = p < n16 ? 16 : (1 << rem);
+      for (int r = 1; r < R; ++r)
+        for (int k = 0; k < Ns; ++k) {
+          const double a = -2.0 * 3.14159265358979323846 * (double)(r * k) / (double)(Ns * R);
+          tab[(Ns - 1) + (r - 1) * Ns + k].x = (decltype(tab[0].x))std::cos(a);
+          tab[(Ns - 1) + (r - 1) * Ns + k].y = (decltype(tab[0].x))std::sin(a);
+        }
+      Ns *= R;
+    }
+  }
+  return t;
+}
+std::vector<float2> fft_pass_tables() { return pass_tables<float2>(); }
+std::vector<double2> fft_pass_tables_d() { return pass_tables<double2>(); }
 std::vector<double2> fft_twiddle_table_d() { return twiddles<double2>(); }
 
 // four-step twiddles W_L^e = lo[e & 4095] * hi[e >> 12] for L = 2^lgL > 4096 (float64 evaluation)

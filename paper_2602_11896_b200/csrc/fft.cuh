@@ -12,6 +12,8 @@ namespace jtfs {
 struct FftTables {
   const float2* tw = nullptr;
   const double2* twd = nullptr;
+  const float2* twp = nullptr;     // per-pass tables (fft_pass_tables), lengths 2 .. 4096
+  const double2* twpd = nullptr;
   const float2* lo_f[23] = {};
   const float2* hi_f[23] = {};
   const double2* lo_d[23] = {};
@@ -28,6 +30,12 @@ cudaError_t fft_launch_dd(const double2* in, double2* out, Rows ri, Rows ro, int
 cudaError_t fft_launch_df(const double2* in, float2* out, Rows ri, Rows ro, int B, bool inverse,
                           const FftTables& T, cudaStream_t st);
 std::vector<float2> fft_twiddle_table();
+// Per-pass twiddles for the in-SMEM transforms of length L = 2^lg <= 4096, table of L at [L, 2L): pass p of
+// seq_fft (radix R_p, sub-transform size Ns_p) holds W_{Ns_p R_p}^{r k} at (Ns_p - 1) + (r - 1) Ns_p + k,
+// r < R_p, k < Ns_p (sum over passes of (R_p - 1) Ns_p = L - 1 entries), so lanes with consecutive k read
+// consecutive words (the strided W_4096 table puts lanes of one pass in the same bank).
+std::vector<float2> fft_pass_tables();
+std::vector<double2> fft_pass_tables_d();
 std::vector<double2> fft_twiddle_table_d();
 void fft_fourstep_tables_f(int lgL, std::vector<float2>* lo, std::vector<float2>* hi);
 void fft_fourstep_tables_d(int lgL, std::vector<double2>* lo, std::vector<double2>* hi);

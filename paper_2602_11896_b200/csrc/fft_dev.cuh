@@ -190,7 +190,7 @@ using CfSmem = SeqCol<float2>;
 
 // One Stockham pass of radix R (16, 8, 4, 2) over nseq = 2^lgC sequences of length L = 2^lgL (sub-transform
 // size Ns = 2^lgNs before the pass). tws = SMEM table W_{2^lgT}^e = exp(-2 pi i e / 2^lgT), e < 2^lgT,
-// 2^lgT >= L. All loads happen before the barrier and all stores after it (in place when ld and st address
+// 2^lgT >= L; lgT = -1: the per-pass table of length L (fft.cuh fft_pass_tables). All loads happen before the barrier and all stores after it (in place when ld and st address
 // the same buffer). CFAST: consecutive threads take consecutive sequences.
 template <class Cp, int R, int NT, int NPT, bool CFAST, class LD, class ST>
 __device__ __noinline__ void cf_pass(int lgC, int lgL, int lgNs, bool inv, const Cp* tws, int lgT, LD ld, ST st) {
@@ -215,7 +215,7 @@ __device__ __noinline__ void cf_pass(int lgC, int lgL, int lgNs, bool inv, const
       if (k > 0) {
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          Cp w = tws[(r * k) << tsh];
+          Cp w = lgT < 0 ? tws[(Ns - 1) + (r - 1) * Ns + k] : tws[(r * k) << tsh];
           w.y *= sg;
           v[i][r] = cmul_f(v[i][r], w);
         }

@@ -329,6 +329,20 @@ static cudaError_t upload(Plan& p) {
   UP(twd, twd);
   d->fftt.tw = d->tw;
   d->fftt.twd = d->twd;
+  {
+    std::vector<float2> pf = fft_pass_tables();
+    std::vector<double2> pd = fft_pass_tables_d();
+    float2* a = nullptr;
+    double2* c = nullptr;
+    if ((e = up(pf, &a)) != cudaSuccess || (e = up(pd, &c)) != cudaSuccess) {
+      if (a) cudaFree(a);
+      free_tables(d);
+      return e;
+    }
+    d->fs_bufs.insert(d->fs_bufs.end(), {(void*)a, (void*)c});
+    d->fftt.twp = a;
+    d->fftt.twpd = c;
+  }
   for (int lg = 13; lg <= 22 && (int64_t(1) << lg) <= p.N_pad; ++lg) {
     std::vector<float2> lf, hf;
     std::vector<double2> ld, hd;
