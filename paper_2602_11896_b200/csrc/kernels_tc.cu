@@ -726,14 +726,13 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       while (f < a.nfr && ((TB.bi * a.nfr + f) % a.n_shards != a.shard || f % a.ng != grp)) ++f;
       return f;
     };
-    auto load_w = [&](int u, int t, float* wl) {
-      const JointUnit U = a.units[u];
-      const TcUnit tu = a.tcu[u];
-      const float* wt = a.wts + tu.wt_off;
-      const int ldw = tu.NT * kTcRows;
-#pragma unroll
-      for (int r = 0; r < KAP; ++r)
-        wl[r] = (r < U.rows_out && lane < kBwRpw) ? __ldg(wt + r * ldw + t * kBwRows + h * kBwRpw + lane) : 0.f;
+    // phi_F weights of this warp's 8 rows of tile t (row block of output r at + r * ldw): read as two
+    // warp-uniform float4 loads per r (broadcast) and folded into g_W's row factors before the tile's W is
+    // waited for; the next tile's lines are prefetched into L1 one tile ahead
+    auto wrow = [&](int u, int t) { return a.wts + a.tcu[u].wt_off + t * kBwRows + h * kBwRpw; };
+    auto pf_w = [&](int u, int t) {
+      if (lane < min(KAP, a.units[u].rows_out))
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(wrow(u, t) + (int64_t)lane * a.tcu[u].NT * kTcRows));
     };
     auto load_go = [&](int u, float* gor) {
       const JointUnit U = a.units[u];
@@ -753,10 +752,10 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       for (int i = 0; i < kBwRpw / 2; ++i) wv[i] = q4[i];
     };
     int f = next_unit(0);
-    float wl_n[KAP], gor_n[KAP];
+    float gor_n[KAP];
     float4 wv_n[kBwRpw / 2];
     if (f < a.nfr) {
-      load_w(TB.bi * a.nfr + f, 0, wl_n);
+      pf_w(TB.bi * a.nfr + f, 0);
       load_go(TB.bi * a.nfr + f, gor_n);
       if (ksm) load_wv(TB.bi * a.nfr + f, 0, wv_n);
     }
@@ -768,11 +767,27 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       for (int r = 0; r < KAP; ++r) gor[r] = gor_n[r];
       const int NT32 = (int)((U.n_rows + kBwRows - 1) / kBwRows);
       const int fn = next_unit(f + 1);
+      const int ldw = a.tcu[u].NT * kTcRows;
       for (int t = 0; t < NT32; ++t, ++g) {
-        float wl[KAP];
-        float v[2 * kBwRpw];
+        // gv[i] = (Phi_F^T g_o)[row i] for this column (Eq. 4 adjoint)
+        float gv[kBwRpw];
+        {
+          const float* wr = wrow(u, t);
 #pragma unroll
-        for (int r = 0; r < KAP; ++r) wl[r] = wl_n[r];
+          for (int i = 0; i < kBwRpw; ++i) gv[i] = 0.f;
+#pragma unroll
+          for (int r = 0; r < KAP; ++r) {
+            if (r < U.rows_out) {
+              const float4 w0 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)r * ldw));
+              const float4 w1 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)r * ldw) + 1);
+              gv[0] = fmaf(w0.x, gor[r], gv[0]); gv[1] = fmaf(w0.y, gor[r], gv[1]);
+              gv[2] = fmaf(w0.z, gor[r], gv[2]); gv[3] = fmaf(w0.w, gor[r], gv[3]);
+              gv[4] = fmaf(w1.x, gor[r], gv[4]); gv[5] = fmaf(w1.y, gor[r], gv[5]);
+              gv[6] = fmaf(w1.z, gor[r], gv[6]); gv[7] = fmaf(w1.w, gor[r], gv[7]);
+            }
+          }
+        }
+        float v[2 * kBwRpw];
         if (ksm) {
 #pragma unroll
           for (int i = 0; i < kBwRpw / 2; ++i) {
@@ -780,10 +795,10 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           }
         }
         if (t + 1 < NT32) {
-          load_w(u, t + 1, wl_n);
+          pf_w(u, t + 1);
           if (ksm) load_wv(u, t + 1, wv_n);
         } else if (fn < a.nfr) {
-          load_w(TB.bi * a.nfr + fn, 0, wl_n);
+          pf_w(TB.bi * a.nfr + fn, 0);
           load_go(TB.bi * a.nfr + fn, gor_n);
           if (ksm) load_wv(TB.bi * a.nfr + fn, 0, wv_n);
         }
@@ -807,12 +822,9 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
 #pragma unroll
         for (int i = 0; i < kBwRpw; ++i) {
           // g_W = (W/|W|) Phi_F^T g_o (Eq.4 adjoint, modulus adjoint with the R22 dead zone)
-          float gv = 0.f;
-#pragma unroll
-          for (int r = 0; r < KAP; ++r) gv = fmaf(__shfl_sync(0xffffffffu, wl[r], i), gor[r], gv);
           const float re = v[2 * i], im = v[2 * i + 1];
           const float m2 = fmaf(re, re, im * im);
-          const float s = m2 > th2 ? gv * tc::rsqrt_approx(m2) : 0.f;
+          const float s = m2 > th2 ? gv[i] * tc::rsqrt_approx(m2) : 0.f;
           tc::split_tf32_fast(re * s, ghi[2 * i], glo[2 * i]);
           tc::split_tf32_fast(im * s, ghi[2 * i + 1], glo[2 * i + 1]);
         }

@@ -198,11 +198,12 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return r;
 }
 
-// tf32 split for 3xTF32: x = hi + lo (+ O(2^-22 x)), hi/lo rounded to tf32 (cvt.rna)
+// tf32 split for 3xTF32: x = hi + lo (+ O(2^-22 x)), hi/lo rounded to tf32. Round to nearest, ties
+// away from zero (the cvt.rna.tf32.f32 rounding, bit for bit on finite values) done on the integer pipe:
+// add half of the 13 dropped mantissa bits, then clear them (a carry into the exponent is the correct
+// rounding). The CVT runs on the quarter-rate conversion pipe and showed up in the epilogues.
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
