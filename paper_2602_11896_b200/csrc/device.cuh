@@ -52,7 +52,7 @@ struct DeviceTables {
   int32_t* kf_of = nullptr;         // [n_fr] k_f per frequential filter
   int32_t* hfr_H = nullptr;         // [n_fr] support half-width of h_f
   // phi_T kernels: (unit, rho) rows in unit order and the prefix of their 256-column tiles
-  int32_t* phT_rows_u = nullptr;    int64_t* phT_tiles = nullptr;  int phT_nrows = 0;  int64_t phT_ntiles = 0;
+  int32_t* phT_rows_u = nullptr;    int32_t* phT_tiles = nullptr;   /* per adjoint tile: u, rho, c0 */  int phT_nrows = 0;  int64_t phT_ntiles = 0;
   int32_t* blk_nmax = nullptr;      // [n_blocks]
   int64_t* ucoef = nullptr;         // [n_units] coefficient offset of the unit's path - o2_start
   int64_t* uo = nullptr;            // [n_units] o_off

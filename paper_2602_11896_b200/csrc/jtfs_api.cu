@@ -271,20 +271,18 @@ static cudaError_t upload(Plan& p) {
   UP(kf, kf_of);
   UP(p.hfr_H, hfr_H);
   {
-    std::vector<int32_t> ru;
-    std::vector<int64_t> cnt;
+    std::vector<int32_t> ru, ti;   // rows (u, rho); adjoint tiles (u, rho, first column)
     for (size_t u = 0; u < p.units.size(); ++u)
       for (int rho = 0; rho < p.units[u].rows_out; ++rho) {
         ru.push_back((int32_t)u);
         ru.push_back(rho);
-        cnt.push_back((p.binfo[p.units[u].bi].n_cols + 255) / 256);
+        for (int64_t c0 = 0; c0 < p.binfo[p.units[u].bi].n_cols; c0 += 256)
+          ti.insert(ti.end(), {(int32_t)u, (int32_t)rho, (int32_t)c0});
       }
-    d->phT_nrows = (int)cnt.size();
-    t = prefix(cnt);
-    d->phT_ntiles = t.back();
-    t.pop_back();
+    d->phT_nrows = (int)(ru.size() / 2);
+    d->phT_ntiles = (int64_t)(ti.size() / 3);
     UP(ru, phT_rows_u);
-    UP(t, phT_tiles);
+    UP(ti, phT_tiles);
   }
   std::vector<int32_t> nm;
   std::vector<int64_t> bt;

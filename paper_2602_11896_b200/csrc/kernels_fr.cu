@@ -712,39 +712,20 @@ __global__ void k_phiT_adj(const float* __restrict__ rres, int64_t r_sb, float* 
   go[b * go_sb + q] = (float)acc;
 }
 
-// ---- phi_T over time, row-tiled (one CTA per (unit, rho) row and 256-column tile): the tile is located
-// once per CTA from the prefix table rt (rows of all units, in unit order), float accumulation.
-struct PhiTRow {
-  int u, rho;
-  int64_t c0;   // first column of the tile
-};
-__device__ __forceinline__ PhiTRow phiT_row(const int64_t* __restrict__ rt, const int32_t* __restrict__ rt_u,
-                                            int nrows, int64_t tile, int tiles_per_row_shift_unused) {
-  (void)tiles_per_row_shift_unused;
-  int lo = 0, hi = nrows - 1;                       // rt[r] = first tile of row r (prefix)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(rt + mid) <= tile) lo = mid; else hi = mid - 1;
-  }
-  PhiTRow R;
-  R.u = rt_u[2 * lo];
-  R.rho = rt_u[2 * lo + 1];
-  R.c0 = (tile - rt[lo]) * 256;
-  return R;
-}
-
+// ---- phi_T over time, row-tiled: one CTA per (unit, rho) row and 256-column tile, the tile's (u, rho,
+// first column) read from a per-tile table (broadcast loads), float accumulation.
 // g_o[u][rho][i] = sum_{t'} tT_s2[dist((m0+t')D - c_i)] r[path][rho][t']  (adjoint of Eq.4's phi_T + stride)
 __global__ void __launch_bounds__(256) k_phiT_adj2(
     const float* __restrict__ rres, int64_t r_sb, float* __restrict__ go, int64_t go_sb,
     const JointUnit* __restrict__ units, const BlockInfo* __restrict__ binfo, const float* __restrict__ phiT_half,
     const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H, const int64_t* __restrict__ ucoef,
-    const int64_t* __restrict__ rt, const int32_t* __restrict__ rt_u, int nrows, int64_t o2_start, int frames,
-    int64_t m0, int shard, int n_shards) {
-  __shared__ PhiTRow R;
+    const int32_t* __restrict__ tinfo, int64_t o2_start, int frames, int64_t m0, int shard, int n_shards) {
+  struct { int u, rho; int64_t c0; } R;
+  R.u = __ldg(tinfo + 3 * blockIdx.x);
+  R.rho = __ldg(tinfo + 3 * blockIdx.x + 1);
+  R.c0 = __ldg(tinfo + 3 * blockIdx.x + 2);
   __shared__ float rr[256];
   const int b = blockIdx.y;
-  if (threadIdx.x == 0) R = phiT_row(rt, rt_u, nrows, blockIdx.x, 0);
-  __syncthreads();
   if (R.u % n_shards != shard) return;
   const JointUnit U = units[R.u];
   const BlockInfo bf = binfo[U.bi];
@@ -946,7 +927,7 @@ void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64
   if (p.o_size == 0 || d.phT_ntiles == 0) return;
   dim3 g((unsigned)d.phT_ntiles, (unsigned)B);
   k_phiT_adj2<<<g, 256, 0, st>>>(r, r_sb, go, go_sb, d.units, d.binfo, d.phiT_half, d.phiT_off, d.phiT_H, d.ucoef,
-                                 d.phT_tiles, d.phT_rows_u, d.phT_nrows, d.o2_start, (int)p.frames,
+                                 d.phT_tiles, d.o2_start, (int)p.frames,
                                  p.pad_left / p.T, shard, n_shards);
   count_launch();
 }

@@ -176,11 +176,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     tc::tc_fence_after();
   }
   const int nchunks = (K2 + kcw - 1) / kcw;
+  // Two MMA issuers (see below) when there are two accumulator buffers: tiles alternate between them and
+  // so do the B stages, split into two rings of NS / 2 stages (one ring per issuer: a stage is then only
+  // ever waited on by one thread, which keeps the parity waits unambiguous). A ring needs >= 2 stages
+  // when a tile spans several chunks (load of chunk c + 1 under the MMAs of chunk c).
+  const int nis = (nbuf == 2 && NS >= 2 && (nchunks == 1 || NS >= 4)) ? 2 : 1;
+  const int NSr = NS / nis;
 
   if (warp == 0) {
     // ===================== producer: B chunks via the bulk-copy engine (one elected lane issues)
-    int stage = 0;
-    uint32_t ph = 0;
+    int stage_r[2] = {0, 0}, gt = 0;
+    uint32_t ph_r[2] = {0, 0};
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
       if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
@@ -188,27 +194,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
       for (int t = 0; t < tu.NT; ++t) {
         // row tile t of the unit's image: chunks of the full K2, starting at this launch's k' range
         const float* src = a.img + tu.img_off + (int64_t)t * (2 * kTcN * TB.K2) + 2 * kTcN * kp_lo;
+        const int r = gt % nis;
+        int& stage = stage_r[r];
+        uint32_t& ph = ph_r[r];
         for (int ch = 0; ch < nchunks; ++ch) {
           const int kc = min(kcw, K2 - ch * kcw);
           const uint32_t bytes = (uint32_t)(2 * kTcN * kc * 4);
-          tc::mbar_wait(&empty[stage], ph ^ 1);
+          const int sg = r * NSr + stage;
+          tc::mbar_wait(&empty[sg], ph ^ 1);
           if (tc::elect_one()) {
-            tc::mbar_expect_tx(&full[stage], bytes);
-            tc::bulk_g2s(bst + stage * STG, src, bytes, &full[stage]);
+            tc::mbar_expect_tx(&full[sg], bytes);
+            tc::bulk_g2s(bst + sg * STG, src, bytes, &full[sg]);
           }
           __syncwarp();
           src += 2 * kTcN * kc;
-          if (++stage == NS) { stage = 0; ph ^= 1; }
+          if (++stage == NSr) { stage = 0; ph ^= 1; }
         }
+        ++gt;
       }
     }
-  } else if (warp == 1 || (warp == 3 && nbuf == 2)) {
+  } else if (warp == 1 || (warp == 3 && nis == 2)) {
     // ===================== MMA issuers (warp-uniform loops, one elected lane issues). The tensor pipe's
     // issue queue holds only ~3 MMAs (~200 cycles of N=128 work) while a commit plus a barrier wait costs
     // ~200 cycles even when the phase has completed (tools/ubench/tmem_mma.cu k_issue), so one issuer
     // drains the pipe at every chunk and tile boundary. With two accumulator buffers, warp 1 issues the
-    // even tiles (buffer 0) and warp 3 the odd ones (buffer 1): one's waits overlap the other's MMAs.
-    const int nis = nbuf == 2 ? 2 : 1, q = warp == 3 ? 1 : 0;
+    // even tiles (buffer 0, stage ring 0) and warp 3 the odd ones (buffer 1, ring 1): one's waits overlap
+    // the other's MMAs.
+    const int q = warp == 3 ? 1 : 0;
     const uint32_t idesc = tc::idesc_tf32(128, kTcN);
     const uint32_t sboA = (uint32_t)K2 * 32u;
     // descriptors differ only in the start-address field: add (byte offset >> 4) to the low word
@@ -217,16 +229,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     const uint32_t aStepM = (uint32_t)(128 * K2 * 4) >> 4;
     const uint32_t bst_s = tc::smem_u32(bst);
     int stage = 0, gt = 0;
-    const int buf = q;
+    int buf = q;
     uint32_t ph = 0, bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
       if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       for (int t = 0; t < tu.NT; ++t) {
-        if (gt % nis != q) {   // the other issuer's tile: skip its chunks in the ring
-          for (int ch = 0; ch < nchunks; ++ch)
-            if (++stage == NS) { stage = 0; ph ^= 1; }
+        if (gt % nis != q) {   // the other issuer's tile (other ring)
           ++gt;
           continue;
         }
@@ -236,10 +246,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         const uint32_t dbase = tbase + (uint32_t)(buf * CT * kTcN);
         for (int ch = 0; ch < nchunks; ++ch) {
           const int kc = min(kcw, K2 - ch * kcw);
-          tc::mbar_wait(&full[stage], ph);
+          tc::mbar_wait(&full[q * NSr + stage], ph);
           tc::tc_fence_after();
           if (lane == 0 && ch == 0) TC_TRACE(1, gt);
-          const uint32_t bh = bst_s + (uint32_t)(stage * STG * 4);
+          const uint32_t bh = bst_s + (uint32_t)((q * NSr + stage) * STG * 4);
           const uint64_t dB_hi = tc::sdesc(bh, 128, (uint32_t)kc * 32u);
           const uint64_t dB_lo = tc::sdesc(bh + (uint32_t)(kTcN * kc * 4), 128, (uint32_t)kc * 32u);
           if (tc::elect_one()) {
@@ -260,16 +270,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
                 }
               }
             }
-            tc::mma_commit(&empty[stage]);
+            tc::mma_commit(&empty[q * NSr + stage]);
           }
           __syncwarp();
-          if (++stage == NS) { stage = 0; ph ^= 1; }
+          if (++stage == NSr) { stage = 0; ph ^= 1; }
         }
         if (tc::elect_one()) tc::mma_commit(&tfull[buf]);
         __syncwarp();
         if (lane == 0) TC_TRACE(2, gt);
         ++gt;
-        bph ^= 1;
+        if (nis == 2) bph ^= 1;                          // own buffer q, every own tile
+        else if (++buf == nbuf) { buf = 0; bph ^= 1; }
       }
     }
   } else if (warp >= 4) {

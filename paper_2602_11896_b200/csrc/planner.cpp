@@ -185,10 +185,18 @@ static void build_tc_tables(Plan* p) {
     if (kap <= 2 && (CT == 2 || tc_fwd_tsa(1, K2) || K2 <= 168)) {
       // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
       // (each bulk copy costs the copy engine ~400 cycles whatever its size: one copy per tile if possible)
-      for (int w : {K2, 64, 32}) {
-        if (w > 128 || w > K2) continue;
-        if (tc_fwd_stages(CT, 2 << kap, K2, w) >= 3) { kcw = w; break; }
-      }
+      // Preferred: a width that also allows the forward's two MMA issuers (two accumulator buffers and two
+      // stage rings, each >= 2 stages when a tile spans several chunks; kernels_tc.cu) -- measured at c2:
+      // the second issuer hides the per-chunk barrier waits and outweighs the extra copies.
+      kcw = 0;
+      for (int pass = 0; pass < 2 && !kcw; ++pass)
+        for (int w : {K2, 64, 32}) {
+          if (w > 128 || w > K2) continue;
+          const int ns = tc_fwd_stages(CT, 2 << kap, K2, w), nch = (K2 + w - 1) / w;
+          const bool two = tc_fwd_nbuf(CT, K2) == 2 && (nch == 1 ? ns >= 2 : ns >= 4);
+          if (ns >= 3 && (pass == 1 || two)) { kcw = w; break; }
+        }
+      if (!kcw) kcw = 16;
     } else {
       ks = 1;
       // fewest balanced K parts whose A tile fits TMEM (TS-form MMAs), each part m whole chunks with the
@@ -198,7 +206,8 @@ static void build_tc_tables(Plan* p) {
         const int kp0 = ((K2 + np - 1) / np + 7) / 8 * 8;
         for (int m = 1; m <= 4; ++m) {
           const int w = ((kp0 + m - 1) / m + 7) / 8 * 8;
-          if (tc_fwd_tsa(1, m * w) && tc_fwd_nbuf(1, m * w) == 2 && tc_fwd_stages(1, 2 << kap, m * w, w) >= 3 &&
+          const int ns = tc_fwd_stages(1, 2 << kap, m * w, w);
+          if (tc_fwd_tsa(1, m * w) && tc_fwd_nbuf(1, m * w) == 2 && ns >= 3 &&
               (np - 1) * m * w < K2) {
             best_np = np;
             best_w = w;
