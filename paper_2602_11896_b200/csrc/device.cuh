@@ -134,7 +134,7 @@ void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, in
 void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,
                      int64_t S_sb, int shard, int n_shards, int B, cudaStream_t st);
 void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S_sb, const float* St,
-                 int64_t St_sb, float* r, int64_t r_sb, float* loss, int shard, int n_shards, int B,
+                 int64_t St_sb, float* r, int64_t r_sb, float* loss, double* part, int shard, int n_shards, int B,
                  cudaStream_t st);
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
                      int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);

@@ -276,7 +276,7 @@ static cudaError_t upload(Plan& p) {
       for (int rho = 0; rho < p.units[u].rows_out; ++rho) {
         ru.push_back((int32_t)u);
         ru.push_back(rho);
-        for (int64_t c0 = 0; c0 < p.binfo[p.units[u].bi].n_cols; c0 += 256)
+        for (int64_t c0 = 0; c0 < p.binfo[p.units[u].bi].n_cols; c0 += 1024)   // kernels_fr.cu kPhiTCols
           ti.insert(ti.end(), {(int32_t)u, (int32_t)rho, (int32_t)c0});
       }
     d->phT_nrows = (int)(ru.size() / 2);
@@ -422,7 +422,7 @@ static Layout layout(const Plan& p, int with_grad) {
   L.S = al(p.n_coef * 4); L.r = al(p.n_coef * 4);
   L.gS1t = al(N1 * p.Ft * 4);
   L.g = with_grad ? al(p.N * 4) : 0;
-  L.loss = 256;
+  L.loss = 256;   // k_loss partials (32 float64 per signal)
   L.thr = 256;
   L.Wk = al(std::max<int64_t>(p.ks_w_floats, 1) * 4);   // split-K blocks: complex W of every cell
   L.gp = with_grad ? al(std::max<int64_t>(p.gp_complex, 1) * 8) : 0;   // g_Y2 partials of filter groups
@@ -814,7 +814,8 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
     int n = (int)std::min<int64_t>(mbl, B - b0);
     CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, shard, n_shards, ls, 0, true, l));
     float* lossp = mstate ? mstate->loss + b0 : loss + b0;
-    launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, shard, n_shards, n, ls);
+    launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, (double*)w.loss, shard,
+                n_shards, n, ls);
     launch_absmax(y + b0 * p.N, p.N, kModTau, w.thr, n, ls);
     float* gp = mstate ? w.g : grad + b0 * p.N;
     int64_t sg = mstate ? w.s_g : p.N;

@@ -712,7 +712,8 @@ __global__ void k_phiT_adj(const float* __restrict__ rres, int64_t r_sb, float* 
   go[b * go_sb + q] = (float)acc;
 }
 
-// ---- phi_T over time, row-tiled: one CTA per (unit, rho) row and 256-column tile, the tile's (u, rho,
+constexpr int kPhiTCols = 1024;   // adjoint columns per CTA (jtfs_api.cu builds the tile table with this step)
+// ---- phi_T over time, row-tiled: one CTA per (unit, rho) row and kPhiTCols-column tile, the tile's (u, rho,
 // first column) read from a per-tile table (broadcast loads), float accumulation.
 // g_o[u][rho][i] = sum_{t'} tT_s2[dist((m0+t')D - c_i)] r[path][rho][t']  (adjoint of Eq.4's phi_T + stride)
 __global__ void __launch_bounds__(256) k_phiT_adj2(
@@ -732,30 +733,32 @@ __global__ void __launch_bounds__(256) k_phiT_adj2(
   const float* rsrc = rres + b * r_sb + o2_start + ucoef[R.u] + (int64_t)R.rho * frames;
   for (int t = threadIdx.x; t < frames; t += 256) rr[t] = rsrc[t];
   __syncthreads();
-  const int64_t i = R.c0 + threadIdx.x;
-  if (i >= bf.n_cols) return;
   const int H = (int)phiT_H[bf.s2];
   const float* tT = phiT_half + phiT_off[bf.s2];
   const int D = bf.D;
-  float acc = 0.f;
-  if (bf.n_cols < bf.T2) {
-    // unwrapped coordinates: column i sits at x = m0 D - H + i; frame m at m D; |m D - x| <= H
-    const int64_t x = m0 * D - H + i;
-    const int64_t lo = x - H, hi = x + H;
-    int64_t mlo = lo <= 0 ? -((-lo) / D) : (lo + D - 1) / D;
-    int64_t mhi = hi >= 0 ? hi / D : -((-hi + D - 1) / D);
-    if (mlo < m0) mlo = m0;
-    if (mhi > m0 + frames - 1) mhi = m0 + frames - 1;
-    int dd = (int)(mlo * D - x);
-    for (int64_t m = mlo; m <= mhi; ++m, dd += D) acc = fmaf(__ldg(tT + (dd < 0 ? -dd : dd)), rr[m - m0], acc);
-  } else {
-    const int64_t c = (bf.c_lo + i) % bf.T2;
-    for (int tp = 0; tp < frames; ++tp) {
-      const int64_t dd = cdist((m0 + tp) * D - c, bf.T2);
-      if (dd <= H) acc = fmaf(__ldg(tT + dd), rr[tp], acc);
+  float* gdst = go + b * go_sb + U.o_off + (int64_t)R.rho * bf.n_cols;
+  // kPhiTCols columns per CTA, 256 apart per thread (coalesced stores), one table lookup per CTA
+  for (int64_t i = R.c0 + threadIdx.x; i < R.c0 + kPhiTCols && i < bf.n_cols; i += 256) {
+    float acc = 0.f;
+    if (bf.n_cols < bf.T2) {
+      // unwrapped coordinates: column i sits at x = m0 D - H + i; frame m at m D; |m D - x| <= H
+      const int64_t x = m0 * D - H + i;
+      const int64_t lo = x - H, hi = x + H;
+      int64_t mlo = lo <= 0 ? -((-lo) / D) : (lo + D - 1) / D;
+      int64_t mhi = hi >= 0 ? hi / D : -((-hi + D - 1) / D);
+      if (mlo < m0) mlo = m0;
+      if (mhi > m0 + frames - 1) mhi = m0 + frames - 1;
+      int dd = (int)(mlo * D - x);
+      for (int64_t m = mlo; m <= mhi; ++m, dd += D) acc = fmaf(__ldg(tT + (dd < 0 ? -dd : dd)), rr[m - m0], acc);
+    } else {
+      const int64_t c = (bf.c_lo + i) % bf.T2;
+      for (int tp = 0; tp < frames; ++tp) {
+        const int64_t dd = cdist((m0 + tp) * D - c, bf.T2);
+        if (dd <= H) acc = fmaf(__ldg(tT + dd), rr[tp], acc);
+      }
     }
+    gdst[i] = acc;
   }
-  go[b * go_sb + U.o_off + (int64_t)R.rho * bf.n_cols + i] = acc;
 }
 
 // S[coef(u, rho, t')] = sum_j tT_s2[|j|] o[u][rho][col(t' D + j)]: one CTA per (unit, rho) row (tile 0 of
@@ -802,16 +805,21 @@ __global__ void __launch_bounds__(256) k_phiT_fwd2(
   }
 }
 
-// loss (R19): r = S - St on owned order-1/2 coefficients (0 elsewhere), E_b = 1/2 sum r^2
+// loss (R19): r = S - St on owned order-1/2 coefficients (0 elsewhere), E_b = 1/2 sum r^2. Two passes
+// for a deterministic sum spread over the SMs: kLossParts CTAs per signal write float64 partials (fixed
+// coefficient ranges), one warp per signal adds them in a fixed order.
+constexpr int kLossParts = 32;
 __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ S, int64_t S_sb, const float* __restrict__ St,
                                               int64_t St_sb, float* __restrict__ r, int64_t r_sb,
-                                              float* __restrict__ loss, const int32_t* __restrict__ coef_path,
+                                              double* __restrict__ part_out, const int32_t* __restrict__ coef_path,
                                               const int32_t* __restrict__ path_unit, int64_t n_coef, int shard,
                                               int n_shards) {
-  const int b = blockIdx.x;
+  const int b = blockIdx.y;
+  const int64_t per = (n_coef + kLossParts - 1) / kLossParts;
+  const int64_t lo = blockIdx.x * per, hi = lo + per < n_coef ? lo + per : n_coef;
   __shared__ double part[256];
   double acc = 0;
-  for (int64_t i = threadIdx.x; i < n_coef; i += 256) {
+  for (int64_t i = lo + threadIdx.x; i < hi; i += 256) {
     int pu = path_unit[coef_path[i]];
     bool own = (pu == -1) ? (shard == 0) : (pu >= 0 && pu % n_shards == shard);
     float d = own ? S[b * S_sb + i] - St[b * St_sb + i] : 0.f;
@@ -824,7 +832,14 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ S, int64
     if (threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
     __syncthreads();
   }
-  if (threadIdx.x == 0) loss[b] = (float)(0.5 * part[0]);
+  if (threadIdx.x == 0) part_out[b * kLossParts + blockIdx.x] = part[0];
+}
+__global__ void k_loss_final(const double* __restrict__ part, float* __restrict__ loss, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double acc = 0;
+  for (int k = 0; k < kLossParts; ++k) acc += part[b * kLossParts + k];
+  loss[b] = (float)(0.5 * acc);
 }
 
 }  // namespace jtfs
@@ -915,11 +930,12 @@ void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64
 }
 
 void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S_sb, const float* St,
-                 int64_t St_sb, float* r, int64_t r_sb, float* loss, int shard, int n_shards, int B,
+                 int64_t St_sb, float* r, int64_t r_sb, float* loss, double* part, int shard, int n_shards, int B,
                  cudaStream_t st) {
-  k_loss<<<B, 256, 0, st>>>(S, S_sb, St, St_sb, r, r_sb, loss, d.coef_path, d.path_owner_unit, p.n_coef, shard,
-                            n_shards);
-  count_launch();
+  k_loss<<<dim3(kLossParts, B), 256, 0, st>>>(S, S_sb, St, St_sb, r, r_sb, part, d.coef_path, d.path_owner_unit,
+                                              p.n_coef, shard, n_shards);
+  k_loss_final<<<(B + 127) / 128, 128, 0, st>>>(part, loss, B);
+  count_launch(2);
 }
 
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
