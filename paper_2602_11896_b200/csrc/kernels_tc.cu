@@ -320,6 +320,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
           tc::tmem_ld16_nowait(ta + 32, v + 32);
           tc::tmem_ld16_nowait(ta + 48, v + 48);
           tc::tmem_wait_ld();
+          if (m == CT - 1) {
+            // the accumulator buffer is free once its last column block sits in registers: release it
+            // before the math so the next tile's MMAs overlap it (essential with one buffer, K2 > 128)
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+          }
           if (pmode != kPmFinish) {
             // split-K: W of (tile t, column c, rows h*32 ..) accumulated across the K parts
             float4* wp = reinterpret_cast<float4*>(
@@ -345,9 +352,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
             for (int r = 0; r < KAP; ++r) oacc[m][r] = fmaf(__shfl_sync(0xffffffffu, wl[r], i), mod, oacc[m][r]);
           }
         }
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         if (warp == 4 && lane == 0) TC_TRACE(6, ge);
         ++ge;
         if (++buf == nbuf) { buf = 0; bph ^= 1; }

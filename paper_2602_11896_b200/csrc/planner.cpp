@@ -256,6 +256,21 @@ static void build_tc_tables(Plan* p) {
     int ns1, s1, ns2, s2;
     tc_bwd_rings(K, ks ? 0 : K2, kcwb, kb2, &ns1, &s1, &ns2, &s2);
     const bool bwd = best < (1 << 30) && (ks ? ns2 >= 2 : (N2 <= 256 && ns1 >= 2 && ns2 >= 2));
+    if (std::getenv("JTFS_PLAN_DUMP")) {   // tuning aid: one line per tensor-core block
+      int64_t rows = 0, prow = 0, prow32 = 0;
+      for (int f = 0; f < nfr; ++f) {
+        rows += p->units[bi * nfr + f].n_rows;
+        prow += (p->units[bi * nfr + f].n_rows + 63) / 64 * 64;
+        prow32 += (p->units[bi * nfr + f].n_rows + 31) / 32 * 32;
+      }
+      const int kw = ks ? kpw : K2;
+      std::fprintf(stderr,
+                   "tc block %zu: K=%d K2=%d CT=%d KAP=%d ks=%d parts=%d kpw=%d kcw=%d fwdNS=%d nch=%d | bwd=%d kcwb=%d "
+                   "kb2=%d ns1=%d ns2=%d | cols=%lld rows=%lld pad64=%lld pad32=%lld units=%d ng=%d\n",
+                   (size_t)bi, K, K2, CT, 2 << kap, ks, nparts, kpw, kcw, tc_fwd_stages(CT, 2 << kap, kw, kcw),
+                   (kw + kcw - 1) / kcw, (int)bwd, kcwb, kb2, ns1, ns2, (long long)p->binfo[bi].n_cols,
+                   (long long)rows, (long long)prow, (long long)prow32, nfr, ngmax);
+    }
     if (bwd) {
       p->blk_tcb[bi] = 1;
       const int ngb =
