@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     // even tiles (buffer 0, stage ring 0) and warp 3 the odd ones (buffer 1, ring 1): one's waits overlap
     // the other's MMAs.
     const int q = warp == 3 ? 1 : 0;
-    const uint32_t idesc = tc::idesc_tf32(128, kTcN);
+    // a unit's last row tile with <= 32 rows runs N = 64 MMAs (rows 32..63 are padding)
+    const uint32_t idesc_full = tc::idesc_tf32(128, kTcN), idesc_half = tc::idesc_tf32(128, kTcN / 2);
     const uint32_t sboA = (uint32_t)K2 * 32u;
     // descriptors differ only in the start-address field: add (byte offset >> 4) to the low word
     const uint64_t dA_hi = tc::sdesc(tc::smem_u32(a_hi), 128, sboA);
@@ -244,6 +245,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         tc::tc_fence_after();
         if (lane == 0) TC_TRACE(0, gt);
         const uint32_t dbase = tbase + (uint32_t)(buf * CT * kTcN);
+        const uint32_t idesc = (t == tu.NT - 1 && a.units[u].n_rows - t * kTcRows <= kTcRows / 2) ? idesc_half
+                                                                                                  : idesc_full;
         for (int ch = 0; ch < nchunks; ++ch) {
           const int kc = min(kcw, K2 - ch * kcw);
           tc::mbar_wait(&full[q * NSr + stage], ph);
@@ -311,10 +314,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
         if (warp == 4 && lane == 0) TC_TRACE(5, ge);
+        // rows h*32 .. of a half tile (see the issuer) are padding and their TMEM columns were not written
+        const bool skip = h == 1 && t == tu.NT - 1 && U.n_rows - t * kTcRows <= kTcRows / 2;
 #pragma unroll
         for (int m = 0; m < CT; ++m) {
           float v[64];
           const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * CT * kTcN + m * kTcN + h * 64);
+          if (skip) {
+            if (m == CT - 1) {
+              tc::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+            }
+            continue;
+          }
           tc::tmem_ld16_nowait(ta, v);
           tc::tmem_ld16_nowait(ta + 16, v + 16);
           tc::tmem_ld16_nowait(ta + 32, v + 32);
