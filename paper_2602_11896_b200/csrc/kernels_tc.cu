@@ -760,7 +760,12 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     auto wrow = [&](int u, int t) { return a.wts + a.tcu[u].wt_off + t * kBwRows + h * kBwRpw; };
     auto pf_w = [&](int u, int t) {
       if (lane < min(KAP, a.units[u].rows_out))
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(wrow(u, t) + (int64_t)lane * a.tcu[u].NT * kTcRows));
+      {
+        // a load whose register is never read: brings the sector into L1 without stalling the warp
+        // (prefetch.global.L1 did not hide the L2 latency of the row-factor loads)
+        float dead;
+        asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(dead) : "l"(wrow(u, t) + (int64_t)lane * a.tcu[u].NT * kTcRows));
+      }
     };
     auto load_go = [&](int u, float* gor) {
       const JointUnit U = a.units[u];
@@ -977,7 +982,7 @@ void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
 #ifdef JTFS_TC_TRACE
     static long long* trace = nullptr;
     if (!trace) cudaMalloc(&trace, 16 * 512 * 8);
-    if (C.Kmax == 18) { cudaMemsetAsync(trace, 0, 16 * 512 * 8, st); a.trace = trace; }
+    if (C.Kmax == g_trace_fwd_k) { cudaMemsetAsync(trace, 0, 16 * 512 * 8, st); a.trace = trace; }
 #endif
     switch (C.cls) {  // class = kap_kind (KAP = 2 << kap_kind)
       case 0: launch_tc_bwd<2>(a, C, B, st); break;
