@@ -315,7 +315,7 @@ static cudaError_t upload(Plan& p) {
   std::vector<int64_t> ut;
   for (size_t n = 0; n < p.psi1.size(); ++n) {
     k1.push_back(std::min(p.psi1[n].j, p.log2T));
-    ut.push_back((p.L1[n] + 255) / 256);
+    ut.push_back((p.L1[n] + 1023) / 1024);   // kernels_time.cu kU1AdjTile
   }
   UP(k1, n1_k1);
   t = prefix(ut); UP(t, u1adj_tiles); d->u1adj_ntiles = t.back();

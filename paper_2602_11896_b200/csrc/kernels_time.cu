@@ -141,6 +141,7 @@ void launch_s0_out(const float2* s0c, int64_t s0_sb, float* S, int64_t S_sb, con
 // Adjoint of layer 2 and of the S1 time average, in Fourier (R21: responses are real, so the
 // adjoint of "multiply + fold-mean + IFFT" is "FFT + periodic extension + multiply"):
 //   g_hat_U1[n1][m] = phiT_k1[m] GS[n1][m mod Ft] + sum_{blocks with n1 < n1_max} psi2_k1[m] GY[n1][m mod T2]
+constexpr int kU1AdjTile = 1024;   // elements per CTA (jtfs_api.cu builds u1adj_tiles with this size)
 __global__ void __launch_bounds__(256) k_adj_gather_u1(
     const float2* __restrict__ GS, int64_t GS_sb, const float2* __restrict__ GY, int64_t GY_sb,
     float2* __restrict__ out, int64_t out_sb, const int64_t* __restrict__ tiles, int N1,
@@ -152,31 +153,50 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
   const int n1 = find_job(tiles, N1, tile);
   const int k1 = n1_k1[n1];
   const int64_t L1 = N_pad >> k1;
-  const int64_t m = (tile - tiles[n1]) * 256 + threadIdx.x;
-  if (m >= L1) return;
-  float2 acc = make_float2(0.f, 0.f);
-  {
-    const Support sp = phiT_sup[k1];
-    const int64_t t = (m - sp.lo) & (L1 - 1);                 // L1, Ft, T2: powers of two
-    if (t < sp.len) {
-      float h = __ldg(vals + sp.off + t);
-      float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m & (Ft - 1))];
-      acc = make_float2(h * v.x, h * v.y);
-    }
-  }
-  for (int bi = 0; bi < n_blocks; ++bi) {
-    if (n1 >= nmax[bi]) continue;
-    const Support sp = psi2_sup[bi * (log2T + 1) + k1];
-    const int64_t t = (m - sp.lo) & (L1 - 1);
-    if (t < sp.len) {
-      float h = __ldg(vals + sp.off + t);
+  // the CTA's filter n1 is fixed: the blocks that reach it, with their psi2 support and Y2 layout, are
+  // gathered once into SMEM (the per-element loop then reads broadcast SMEM instead of chains of
+  // dependent global loads)
+  constexpr int kMaxB = 32;
+  __shared__ int64_t s_lo[kMaxB], s_len[kMaxB], s_off[kMaxB], s_y[kMaxB], s_T2[kMaxB];
+  __shared__ int s_nb;
+  if (threadIdx.x == 0) {
+    int nb = 0;
+    for (int bi = 0; bi < n_blocks && nb < kMaxB; ++bi) {
+      if (n1 >= nmax[bi]) continue;
+      const Support sp = psi2_sup[bi * (log2T + 1) + k1];
       const BlockInfo bf = binfo[bi];
-      float2 v = GY[b * GY_sb + bf.y_off + (int64_t)n1 * bf.T2 + (m & (bf.T2 - 1))];
-      acc.x = fmaf(h, v.x, acc.x);
-      acc.y = fmaf(h, v.y, acc.y);
+      s_lo[nb] = sp.lo; s_len[nb] = sp.len; s_off[nb] = sp.off;
+      s_y[nb] = bf.y_off + (int64_t)n1 * bf.T2; s_T2[nb] = bf.T2;
+      ++nb;
     }
+    s_nb = nb;
   }
-  out[b * out_sb + l1_off[n1] + m] = acc;
+  __syncthreads();
+  const Support spT = phiT_sup[k1];
+  const int nb = s_nb;
+  // kU1AdjTile elements per CTA, 256 apart per thread (coalesced), one setup per CTA
+  for (int64_t m = (tile - tiles[n1]) * kU1AdjTile + threadIdx.x; m < L1 && m < (tile - tiles[n1] + 1) * kU1AdjTile;
+       m += 256) {
+    float2 acc = make_float2(0.f, 0.f);
+    {
+      const int64_t t = (m - spT.lo) & (L1 - 1);                 // L1, Ft, T2: powers of two
+      if (t < spT.len) {
+        float h = __ldg(vals + spT.off + t);
+        float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m & (Ft - 1))];
+        acc = make_float2(h * v.x, h * v.y);
+      }
+    }
+    for (int i = 0; i < nb; ++i) {
+      const int64_t t = (m - s_lo[i]) & (L1 - 1);
+      if (t < s_len[i]) {
+        float h = __ldg(vals + s_off[i] + t);
+        float2 v = GY[b * GY_sb + s_y[i] + (m & (s_T2[i] - 1))];
+        acc.x = fmaf(h, v.x, acc.x);
+        acc.y = fmaf(h, v.y, acc.y);
+      }
+    }
+    out[b * out_sb + l1_off[n1] + m] = acc;
+  }
 }
 
 void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS, int64_t GS_sb,

@@ -519,6 +519,9 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     p->binfo.push_back(bf);
   }
   p->sumY2 = yoff;
+  // k_adj_gather_u1 stages the per-block supports of one filter in SMEM (kMaxB = 32); J <= 24 keeps the
+  // block count at most 25
+  if (p->binfo.size() > 32) { *err = "more than 32 second-order blocks"; return 1; }
 
   // ---- frequential row kernels h_f on the P grid (closed form, complex) for all of L_fr
   const int nfr = (int)p->L_fr.size();
