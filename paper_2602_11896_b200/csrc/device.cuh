@@ -85,7 +85,8 @@ struct DeviceTables {
   FfList ffw, ffb;
 };
 
-constexpr int kGatherTile = 256;   // outputs per CTA of the gather kernels
+constexpr int kGatherThreads = 256;                 // threads per CTA of the gather kernels
+constexpr int kGatherTile = 4 * kGatherThreads;     // outputs per CTA (4 per thread, 256 apart)
 constexpr int kPhiTSmem = 12288;   // phi_T half kernel staged in SMEM up to this many taps
 constexpr int kJC = 64;            // joint stage: columns per CTA
 constexpr int kJR = 64;            // joint stage: rows per chunk

@@ -47,29 +47,30 @@ __device__ __forceinline__ void st_c(float2* p, double re, double im) { *p = mak
 __device__ __forceinline__ void st_c(double2* p, double re, double im) { *p = make_double2(re, im); }
 
 template <class TI, class TO>
-__global__ void __launch_bounds__(kGatherTile) k_gather(const TI* __restrict__ in, int64_t in_sb,
-                                                         TO* __restrict__ out, int64_t out_sb,
-                                                         const GatherJob* __restrict__ jobs,
-                                                         const int64_t* __restrict__ tiles, int njobs,
-                                                         const float* __restrict__ vals) {
+__global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict__ in, int64_t in_sb,
+                                                            TO* __restrict__ out, int64_t out_sb,
+                                                            const GatherJob* __restrict__ jobs,
+                                                            const int64_t* __restrict__ tiles, int njobs,
+                                                            const float* __restrict__ vals) {
   using R = typename GAcc<TI>::R;
   const int64_t tile = blockIdx.x;
   const int b = blockIdx.y;
   const int j = find_job(tiles, njobs, tile);
   const GatherJob J = jobs[j];
-  const int64_t m = (tile - tiles[j]) * kGatherTile + threadIdx.x;
-  if (m >= J.L_out) return;
   const TI* src = in + b * in_sb + J.in_off;
-  // L_in, L_out: powers of two (grid lengths N_pad >> k)
-  int64_t s = J.lo + ((m - J.lo) & (J.L_out - 1));          // smallest s >= lo with s = m mod L_out
-  R ax = 0, ay = 0;
-  for (; s < J.lo + J.len; s += J.L_out) {
-    const R h = (R)__ldg(vals + J.val_off + (s - J.lo));
-    const TI v = src[s & (J.L_in - 1)];
-    ax += h * (R)v.x;
-    ay += h * (R)v.y;
+  const int64_t m0 = (tile - tiles[j]) * kGatherTile;
+  for (int64_t m = m0 + threadIdx.x; m < J.L_out && m < m0 + kGatherTile; m += kGatherThreads) {
+    // L_in, L_out: powers of two (grid lengths N_pad >> k)
+    int64_t s = J.lo + ((m - J.lo) & (J.L_out - 1));          // smallest s >= lo with s = m mod L_out
+    R ax = 0, ay = 0;
+    for (; s < J.lo + J.len; s += J.L_out) {
+      const R h = (R)__ldg(vals + J.val_off + (s - J.lo));
+      const TI v = src[s & (J.L_in - 1)];
+      ax += h * (R)v.x;
+      ay += h * (R)v.y;
+    }
+    st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
   }
-  st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
 }
 
 template <class TI, class TO>
@@ -77,7 +78,7 @@ static void gather_t(const TI* in, int64_t in_sb, TO* out, int64_t out_sb, const
                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   dim3 g((unsigned)ntiles, (unsigned)B);
-  k_gather<TI, TO><<<g, kGatherTile, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
+  k_gather<TI, TO><<<g, kGatherThreads, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
   count_launch();
 }
 void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
