@@ -737,15 +737,17 @@ __global__ void __launch_bounds__(256) k_phiT_adj2(
   const float* tT = phiT_half + phiT_off[bf.s2];
   const int D = bf.D;
   float* gdst = go + b * go_sb + U.o_off + (int64_t)R.rho * bf.n_cols;
+  const int lgD = __ffs(D) - 1;
   // kPhiTCols columns per CTA, 256 apart per thread (coalesced stores), one table lookup per CTA
   for (int64_t i = R.c0 + threadIdx.x; i < R.c0 + kPhiTCols && i < bf.n_cols; i += 256) {
     float acc = 0.f;
     if (bf.n_cols < bf.T2) {
       // unwrapped coordinates: column i sits at x = m0 D - H + i; frame m at m D; |m D - x| <= H
+      // D is a power of two: ceil / floor division by arithmetic shifts (no 64-bit divides per column)
       const int64_t x = m0 * D - H + i;
       const int64_t lo = x - H, hi = x + H;
-      int64_t mlo = lo <= 0 ? -((-lo) / D) : (lo + D - 1) / D;
-      int64_t mhi = hi >= 0 ? hi / D : -((-hi + D - 1) / D);
+      int64_t mlo = -((-lo) >> lgD);
+      int64_t mhi = hi >> lgD;
       if (mlo < m0) mlo = m0;
       if (mhi > m0 + frames - 1) mhi = m0 + frames - 1;
       int dd = (int)(mlo * D - x);
