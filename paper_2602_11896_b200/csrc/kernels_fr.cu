@@ -162,9 +162,13 @@ __global__ void k_o1_bwd_time(const float* __restrict__ rres, int64_t r_sb, floa
   }
   const float* gv2 = V2 + b * V2_sb + ((int64_t)f * P + i) * frames;
   double acc = 0;
+  // a = (m0 + tp - tau) mod Ft advanced by one per frame (one 64-bit modulo per output)
+  const int Fti = (int)Ft;
+  int ad = (int)(((m0 - tau) % Ft + Ft) % Ft);
   for (int64_t tp = 0; tp < frames; ++tp) {
-    int64_t dd = cdist(m0 + tp - tau, Ft);
+    const int dd = ad > Fti - ad ? Fti - ad : ad;
     if (dd <= H) acc += (double)__ldg(tT + dd) * (double)gv2[tp];
+    if (++ad == Fti) ad = 0;
   }
   float2 v = *w;
   float m2 = v.x * v.x + v.y * v.y;
