@@ -15,7 +15,9 @@ from synth import CONFIGS, plan_args, batch
 
 pytestmark = pytest.mark.gpu
 
-CASES = {"c2": [0, 9], "c3": [10], "c4": [11], "c5": [11]}
+# (config, sampled blocks): at c2 block 0 = CT = 2 SS form, 2 = two forward MMA issuers over 4-chunk tiles
+# (one B ring each), 5 = split-K (2 parts, W kept for the backward), 9 = split-K with filter groups
+CASES = [("c2", [0, 9]), ("c2", [2, 5]), ("c3", [10]), ("c4", [11]), ("c5", [11])]
 
 
 def rel(a, b):
@@ -32,12 +34,11 @@ def subset_mask(plan, blocks):
     return m
 
 
-@pytest.mark.parametrize("name", list(CASES))
-def test_large_forward_and_gradient(name):
+@pytest.mark.parametrize("name,blocks", CASES, ids=[f"{c}-b{'-'.join(map(str, b))}" for c, b in CASES])
+def test_large_forward_and_gradient(name, blocks):
     from paper_2602_11896_b200 import Plan
     cfg = CONFIGS[name]
     args = plan_args(cfg)
-    blocks = CASES[name]
     p = Plan(*args)
     o = Oracle(args)
     x = batch(name, 1)
@@ -72,6 +73,8 @@ def test_split_k_shards_and_microbatch():
     x = torch.from_numpy(batch("c2", 2)).cuda()
     y = torch.from_numpy(batch("c2", 2, which="y")).cuda()
     S = p.forward(x)
+    for _ in range(3):   # repeated launches are bitwise identical (no races in the pipelined kernels)
+        assert torch.equal(p.forward(x), S)
     loss, g = p.loss_grad(y, S)
     ws = torch.empty(p.workspace_size(1, True), dtype=torch.uint8, device="cuda")
     l1, g1 = p.loss_grad(y, S, ws=ws)
