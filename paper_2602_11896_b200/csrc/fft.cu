@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "fft.cuh"
 #include "fft_dev.cuh"
+#include "plan.h"
 
 namespace jtfs {
 
@@ -75,6 +76,40 @@ __global__ void __launch_bounds__(256) k_fft_small(const TI* __restrict__ in, TO
   __syncthreads();
   const LdRows<TI, C> ld{in + b * ri.stride_b + ri.off + (r0 << lgL), lgL, rows};
   const StRows<TO, C> st{out + b * ro.stride_b + ro.off + (r0 << lgL), lgL, rows, (typename Cx<C>::R)scale};
+  const SeqCol<C> buf{s, 1 << lgL};
+  seq_fft<C, 256, 16>(lgM, lgL, inv != 0, tws, -1, ld, st, buf);
+}
+
+// Several row groups of (possibly different) lengths <= 4096 in one launch: CTA x belongs to the group
+// whose CTA range holds it (the job list travels in the kernel parameters).
+struct FftJob {
+  int64_t off, count;   // first row element (same offset in and out), rows
+  int lgL, cta0;        // log2 length, first CTA
+};
+constexpr int kMaxFftJobs = 24;
+struct FftJobs {
+  FftJob j[kMaxFftJobs];
+  int n;
+};
+template <class TI, class TO, class C>
+__global__ void __launch_bounds__(256) k_fft_small_multi(const TI* __restrict__ in, TO* __restrict__ out,
+                                                         int64_t in_sb, int64_t out_sb, FftJobs J, int inv,
+                                                         const C* __restrict__ tw) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  int jx = 0;
+  while (jx + 1 < J.n && (int)blockIdx.x >= J.j[jx + 1].cta0) ++jx;
+  const int64_t off = J.j[jx].off, count = J.j[jx].count;
+  const int lgL = J.j[jx].lgL, lgM = 12 - lgL;
+  C* s = reinterpret_cast<C*>(smraw);          // [M][L] (swizzled sequences), M L = 4096
+  C* tws = s + 4096;                           // [L]
+  const int b = blockIdx.y;
+  const int64_t r0 = (int64_t)((int)blockIdx.x - J.j[jx].cta0) << lgM;
+  const int rows = (int)((count - r0) < (1 << lgM) ? (count - r0) : (1 << lgM));
+  load_twiddles<C, 256>(tws, tw, lgL);
+  __syncthreads();
+  const typename Cx<C>::R sc = inv ? (typename Cx<C>::R)1 / (typename Cx<C>::R)(1 << lgL) : (typename Cx<C>::R)1;
+  const LdRows<TI, C> ld{in + b * in_sb + off + (r0 << lgL), lgL, rows};
+  const StRows<TO, C> st{out + b * out_sb + off + (r0 << lgL), lgL, rows, sc};
   const SeqCol<C> buf{s, 1 << lgL};
   seq_fft<C, 256, 16>(lgM, lgL, inv != 0, tws, -1, ld, st, buf);
 }
@@ -261,6 +296,55 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
   }
   count_launch(2);
   return cudaGetLastError();
+}
+
+// Row groups sharing the batch strides: groups of length <= 4096 go into grouped launches (up to
+// kMaxFftJobs per launch), longer ones through fft_launch_t (four-step).
+template <class TI, class TO, class C>
+static cudaError_t fft_groups_t(const TI* in, TO* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                                int B, bool inverse, const FftTables& T, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_small_multi<TI, TO, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(8192 * sizeof(C)));
+    attr = true;
+  }
+  FftJobs J{};
+  int ctas = 0;
+  auto flush = [&]() -> cudaError_t {
+    if (J.n == 0) return cudaSuccess;
+    int maxL = 0;
+    for (int i = 0; i < J.n; ++i) maxL = std::max(maxL, 1 << J.j[i].lgL);
+    k_fft_small_multi<TI, TO, C><<<dim3((unsigned)ctas, (unsigned)B), 256, (size_t)(4096 + maxL) * sizeof(C), st>>>(
+        in, out, in_sb, out_sb, J, inverse ? 1 : 0, FftTw<C>::base(T));
+    count_launch();
+    J.n = 0;
+    ctas = 0;
+    return cudaGetLastError();
+  };
+  cudaError_t e;
+  for (int i = 0; i < ng; ++i) {
+    if (g[i].count <= 0 || B <= 0) continue;
+    if (g[i].L > 4096) {
+      Rows ri{in_sb, g[i].off, g[i].count, g[i].L}, ro{out_sb, g[i].off, g[i].count, g[i].L};
+      if ((e = fft_launch_t<TI, TO, C>(in, out, ri, ro, B, inverse, T, st))) return e;
+      continue;
+    }
+    const int lgL = ilog2_exact(g[i].L), lgM = 12 - lgL;
+    const int n = (int)((g[i].count + (1 << lgM) - 1) >> lgM);
+    if (J.n == kMaxFftJobs && (e = flush())) return e;
+    J.j[J.n++] = FftJob{g[i].off, g[i].count, lgL, ctas};
+    ctas += n;
+  }
+  return flush();
+}
+cudaError_t fft_groups(const float2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                       int B, bool inverse, const FftTables& T, cudaStream_t st) {
+  return fft_groups_t<float2, float2, float2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
+}
+cudaError_t fft_groups_df(const double2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                          int B, bool inverse, const FftTables& T, cudaStream_t st) {
+  return fft_groups_t<double2, float2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
 }
 
 cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,

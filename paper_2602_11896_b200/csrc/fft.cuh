@@ -29,6 +29,13 @@ cudaError_t fft_launch_dd(const double2* in, double2* out, Rows ri, Rows ro, int
                           const FftTables& T, cudaStream_t st);
 cudaError_t fft_launch_df(const double2* in, float2* out, Rows ri, Rows ro, int B, bool inverse,
                           const FftTables& T, cudaStream_t st);
+// Row groups {off, count, L} (offsets shared by in and out, per-signal strides in_sb / out_sb): groups of
+// length <= 4096 run in grouped launches, longer ones as four-step transforms.
+struct FftGroup;
+cudaError_t fft_groups(const float2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                       int B, bool inverse, const FftTables& T, cudaStream_t st);
+cudaError_t fft_groups_df(const double2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                          int B, bool inverse, const FftTables& T, cudaStream_t st);
 std::vector<float2> fft_twiddle_table();
 // Per-pass twiddles for the in-SMEM transforms of length L = 2^lg <= 4096, table of L at [L, 2L): pass p of
 // seq_fft (radix R_p, sub-transform size Ns_p) holds W_{Ns_p R_p}^{r k} at (Ns_p - 1) + (r - 1) Ns_p + k,

@@ -483,17 +483,14 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   // A2: layer 1: cdgmm + subsample_fourier (float64), ifft (float64 -> complex64 Z1),
   // modulus, fft (complex64)
   launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals, mb, st);
-  for (auto& g : p.l1_groups) {
-    Rows ri{sAd, g.off, g.count, g.L}, ro{w.s_L1, g.off, g.count, g.L};
-    if ((e = fft_launch_df(Ad, w.Z1, ri, ro, mb, true, d.fftt, st))) return e;
-  }
+  if ((e = fft_groups_df(Ad, w.Z1, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt, st)))
+    return e;
   launch_modulus(w.Z1, w.s_L1, w.A, w.s_A, p.sumL1, mb, st);  // A rows use the L1 layout
   RET();
   if (stop == 1) return cudaSuccess;
-  for (auto& g : p.l1_groups) {
-    Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_L1, g.off, g.count, g.L};
-    if ((e = fft_launch(w.A, w.U1h, ri, ro, mb, false, d.fftt, st))) return e;
-  }
+  if ((e = fft_groups(w.A, w.U1h, w.s_A, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, false, d.fftt,
+                      st)))
+    return e;
   // S0 and S1 time averages (Eq.3 time part)
   launch_gather_df(Xhd, sd, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
   launch_gather(w.U1h, w.s_L1, w.cs + p.Ft, w.s_c, d.s1_jobs, d.s1_tiles, d.n_s1, d.s1_ntiles, d.spec_vals, mb, st);
@@ -507,10 +504,9 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   // A4: layer 2, width-first
   if (!p.blocks.empty()) {
     launch_gather(w.U1h, w.s_L1, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st);
-    for (auto& g : p.y2_groups) {
-      Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
-      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, true, d.fftt, st))) return e;
-    }
+    if ((e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, p.y2_groups.data(), (int)p.y2_groups.size(), mb, true, d.fftt,
+                        st)))
+      return e;
     RET();
     if (stop == 3) return cudaSuccess;
     // A5: joint lambda_1 stage + phi_F; A6: phi_T
@@ -550,10 +546,9 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     fan_join(fo, st);
     prof_end(st, 2 + 4 * lane);
     // FFT of g_Y2 rows -> G_Y (into Y2)
-    for (auto& g : p.y2_groups) {
-      Rows ri{w.s_A, g.off, g.count, g.L}, ro{w.s_Y2, g.off, g.count, g.L};
-      if ((e = fft_launch(w.A, w.Y2, ri, ro, mb, false, d.fftt, st))) return e;
-    }
+    if ((e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, p.y2_groups.data(), (int)p.y2_groups.size(), mb, false, d.fftt,
+                        st)))
+      return e;
   }
   // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)
   launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, w.thr, mb, st);
@@ -561,16 +556,14 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
   if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, N1, p.Ft, mb, false, st))) return e;
   // A8: g_hat_U1 -> U1h ; g_U1 = Re IFFT -> A
   launch_adj_gather_u1(p, d, w.ct, w.s_c, w.Y2, w.s_Y2, w.U1h, w.s_L1, mb, st);
-  for (auto& g : p.l1_groups) {
-    Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
-    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, true, d.fftt, st))) return e;
-  }
+  if ((e = fft_groups(w.U1h, w.A, w.s_L1, w.s_A, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt,
+                      st)))
+    return e;
   // A9: modulus adjoint, FFT, layer-1 adjoint gather, IFFT, reflect adjoint
   launch_phase_mul(w.Z1, w.A, w.s_A, w.U1h, p.sumL1, w.s_L1, w.thr, mb, st);  // Z1, U1h share the L1 stride
-  for (auto& g : p.l1_groups) {
-    Rows ri{w.s_L1, g.off, g.count, g.L}, ro{w.s_A, g.off, g.count, g.L};
-    if ((e = fft_launch(w.U1h, w.A, ri, ro, mb, false, d.fftt, st))) return e;
-  }
+  if ((e = fft_groups(w.U1h, w.A, w.s_L1, w.s_A, p.l1_groups.data(), (int)p.l1_groups.size(), mb, false, d.fftt,
+                      st)))
+    return e;
   launch_adj_gather_x(p, d, w.A, w.s_A, w.Xh, w.s_xp, mb, st);
   if ((e = fft_rows(p, w.Xh, w.s_xp, w.xp, w.s_xp, 0, 1, p.N_pad, mb, true, st))) return e;
   launch_reflect_adj(w.xp, w.s_xp, grad, sg, p, mb, st);
