@@ -32,4 +32,4 @@ def main(path, per_step):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 159)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 126)
