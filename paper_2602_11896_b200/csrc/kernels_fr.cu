@@ -91,31 +91,40 @@ __global__ void k_o1_time(const float2* __restrict__ W1, int64_t W1_sb, float* _
 }
 
 // order-1 outputs (paths 1 .. nfr1): f = 0: Re W1 (Eq.3); f > 0: phi_F rows of V2, stride F.
-__global__ void k_o1_out(const float2* __restrict__ W1, int64_t W1_sb, const float* __restrict__ V2,
+__global__ void __launch_bounds__(256) k_o1_out(const float2* __restrict__ W1, int64_t W1_sb, const float* __restrict__ V2,
                          int64_t V2_sb, float* __restrict__ S, int64_t S_sb, const int64_t* __restrict__ rlo,
                          const int64_t* __restrict__ nrows, const int32_t* __restrict__ kf_of,
                          const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off, int log2F, int P,
                          int64_t Ft, int64_t frames, int64_t m0, int rows1) {
+  // 64 outputs per CTA, 4 threads each (part = threadIdx.x / 64 takes rows i = part mod 4); partials
+  // combined in part order (deterministic)
+  __shared__ double part_acc[4][64];
   const int f = blockIdx.y, b = blockIdx.z;
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int o = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const int64_t q = (int64_t)blockIdx.x * 64 + o;
   const int64_t rho = q / frames, tp = q % frames;
-  if (rho >= rows1) return;
-  float out;
-  if (f == 0) {
-    out = W1[b * W1_sb + rho * Ft + m0 + tp].x;
-  } else {
+  const bool valid = rho < rows1;
+  double acc = 0;
+  if (valid && f > 0) {
     const int kf = kf_of[f], d = log2F - kf;
     const int64_t Lf = P >> kf;
     const float* g = phiF_k + phiF_off[kf];
     const float* v = V2 + b * V2_sb + (int64_t)f * P * frames + tp;
-    double acc = 0;
     const int nr = (int)nrows[f], r0 = (int)rlo[f], Lm = (int)Lf - 1;   // L_f: power of two
-    for (int i = 0; i < nr; ++i) {
+    for (int i = part; i < nr; i += 4) {
       const int r = (r0 + i) & Lm;
       const int e = (((int)rho << d) - r) & Lm;
       acc += (double)__ldg(g + e) * (double)v[(int64_t)i * frames];
     }
-    out = (float)acc;
+  }
+  part_acc[part][o] = acc;
+  __syncthreads();
+  if (part != 0 || !valid) return;
+  float out;
+  if (f == 0) {
+    out = W1[b * W1_sb + rho * Ft + m0 + tp].x;
+  } else {
+    out = (float)(((part_acc[0][o] + part_acc[1][o]) + part_acc[2][o]) + part_acc[3][o]);
   }
   S[b * S_sb + frames + ((int64_t)f * rows1 + rho) * frames + tp] = out;
 }
@@ -178,45 +187,57 @@ __global__ void k_o1_bwd_time(const float* __restrict__ rres, int64_t r_sb, floa
 }
 
 // gS1t[n][tau] = sum_f sum_i Re(conj(h_f[(r_i 2^k_f - n) mod P]) gW1[f][i][tau])
-__global__ void k_o1_bwd_S1t(const float2* __restrict__ W1, int64_t W1_sb, float* __restrict__ gS1t,
+constexpr int kO1Parts = 4;   // threads per output of the order-1 reductions (few outputs: latency bound)
+__global__ void __launch_bounds__(256) k_o1_bwd_S1t(const float2* __restrict__ W1, int64_t W1_sb, float* __restrict__ gS1t,
                              int64_t gS_sb, const float2* __restrict__ hfr, const int64_t* __restrict__ rlo,
                              const int64_t* __restrict__ nrows, const int32_t* __restrict__ kf_of,
                              const int32_t* __restrict__ hH, int nfr1, int N1, int P, int64_t Ft) {
+  // 64 outputs per CTA, kO1Parts threads each (part = threadIdx.x / 64 takes filters f = part mod
+  // kO1Parts); partial sums combined in part order (deterministic)
+  __shared__ double part_acc[kO1Parts][64];
   const int b = blockIdx.y;
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int o = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const int64_t q = (int64_t)blockIdx.x * 64 + o;
   const int64_t n = q / Ft, tau = q % Ft;
-  if (n >= N1) return;
   double acc = 0;
-  for (int f = 0; f < nfr1; ++f) {
-    const int kf = kf_of[f];
-    const int64_t Lf = P >> kf;
-    const float2* h = hfr + (int64_t)f * P;
-    const float2* g = W1 + b * W1_sb + (int64_t)f * P * Ft + tau;
-    float accf = 0.f;
-    // rows r with |r 2^kf - n| <= H (circular on P): r in [ceil((n-H)/2^kf), floor((n+H)/2^kf)] mod L_f
-    const int H = hH[f];
-    const int nr = (int)nrows[f], r0 = (int)rlo[f], Lm = (int)Lf - 1;
-    int rs, cnt;
-    if (2 * H + 1 >= P) { rs = 0; cnt = (int)Lf; }
-    else {
-      const int s = 1 << kf;
-      const int a = (int)n - H, bnd = (int)n + H;
-      rs = a >= 0 ? (a + s - 1) >> kf : -((-a) >> kf);
-      const int rhi = bnd >> kf;                          // bnd >= 0
-      cnt = min(rhi - rs + 1, (int)Lf);
+  if (n < N1) {
+    for (int f = part; f < nfr1; f += kO1Parts) {
+      const int kf = kf_of[f];
+      const int64_t Lf = P >> kf;
+      const float2* h = hfr + (int64_t)f * P;
+      const float2* g = W1 + b * W1_sb + (int64_t)f * P * Ft + tau;
+      float accf = 0.f;
+      // rows r with |r 2^kf - n| <= H (circular on P): r in [ceil((n-H)/2^kf), floor((n+H)/2^kf)] mod L_f
+      const int H = hH[f];
+      const int nr = (int)nrows[f], r0 = (int)rlo[f], Lm = (int)Lf - 1;
+      int rs, cnt;
+      if (2 * H + 1 >= P) { rs = 0; cnt = (int)Lf; }
+      else {
+        const int s = 1 << kf;
+        const int a = (int)n - H, bnd = (int)n + H;
+        rs = a >= 0 ? (a + s - 1) >> kf : -((-a) >> kf);
+        const int rhi = bnd >> kf;                          // bnd >= 0
+        cnt = min(rhi - rs + 1, (int)Lf);
+      }
+      for (int qq = 0; qq < cnt; ++qq) {
+        const int r = (rs + qq) & Lm;
+        const int i = (r - r0) & Lm;
+        if (i >= nr) continue;
+        const int hb = (r << kf) & (P - 1);
+        const float2 hv = __ldg(h + ((hb - (int)n) & (P - 1)));
+        const float2 gv = g[(int64_t)i * Ft];
+        accf = fmaf(hv.x, gv.x, fmaf(hv.y, gv.y, accf));
+      }
+      acc += accf;
     }
-    for (int q = 0; q < cnt; ++q) {
-      const int r = (rs + q) & Lm;
-      const int i = (r - r0) & Lm;
-      if (i >= nr) continue;
-      const int hb = (r << kf) & (P - 1);
-      const float2 hv = __ldg(h + ((hb - (int)n) & (P - 1)));
-      const float2 gv = g[(int64_t)i * Ft];
-      accf = fmaf(hv.x, gv.x, fmaf(hv.y, gv.y, accf));
-    }
-    acc += accf;
   }
-  gS1t[b * gS_sb + n * Ft + tau] = (float)acc;
+  part_acc[part][o] = acc;
+  __syncthreads();
+  if (part == 0 && n < N1) {
+    double t = part_acc[0][o];
+    for (int k = 1; k < kO1Parts; ++k) t += part_acc[k][o];
+    gS1t[b * gS_sb + n * Ft + tau] = (float)t;
+  }
 }
 
 // =====================================================================================
@@ -866,7 +887,7 @@ void launch_o1_fwd(const Plan& p, const DeviceTables& d, const float* S1t, int64
     k_o1_time<<<g2, 256, 0, st>>>(W1, W1_sb, V2, V2_sb, d.o1_nrows, d.phiT_half + p.phiT_off[p.log2T],
                                   p.phiT_H[p.log2T], P, p.Ft, p.frames, m0);
   }
-  dim3 g3((unsigned)((p.o1_rows_out * p.frames + 255) / 256), (unsigned)nfr1, (unsigned)B);
+  dim3 g3((unsigned)((p.o1_rows_out * p.frames + 63) / 64), (unsigned)nfr1, (unsigned)B);
   k_o1_out<<<g3, 256, 0, st>>>(W1, W1_sb, V2, V2_sb, S, S_sb, d.o1_rlo, d.o1_nrows, d.kf_of, d.phiF_k, d.phiF_off,
                                p.log2F, P, p.Ft, p.frames, m0, p.o1_rows_out);
   count_launch(nfr1 > 1 ? 3 : 2);
@@ -888,7 +909,7 @@ void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t
   dim3 g2((unsigned)((p.P * p.Ft + 255) / 256), (unsigned)nfr1, (unsigned)B);
   k_o1_bwd_time<<<g2, 256, 0, st>>>(r, r_sb, W1, W1_sb, V2, V2_sb, d.o1_nrows, d.phiT_half + p.phiT_off[p.log2T],
                                     p.phiT_H[p.log2T], P, p.Ft, p.frames, m0, thr);
-  dim3 g3((unsigned)((p.psi1.size() * p.Ft + 255) / 256), (unsigned)B);
+  dim3 g3((unsigned)((p.psi1.size() * p.Ft + 63) / 64), (unsigned)B);
   k_o1_bwd_S1t<<<g3, 256, 0, st>>>(W1, W1_sb, gS1t, gS1t_sb, d.hfr, d.o1_rlo, d.o1_nrows, d.kf_of, d.hfr_H,
                                    nfr1, (int)p.psi1.size(), P, p.Ft);
   count_launch(2);
