@@ -121,7 +121,8 @@ def run_reference(args) -> None:
     y = batch(args.config, 1, which="y")
     St = o.forward(x)
     # one reference step = fwd+grad of ONE signal (~1 min on 16 cores); capped at 2 steps so the
-    # arm ends within a few minutes whatever --steps says (reported as "steps")
+    # arm ends within a few minutes whatever --steps says (reported as "steps"); no warm-up steps: the
+    # float64 numpy oracle has no JIT or device state to warm (reported as "warmup": 0)
     steps = max(1, min(args.steps, 2))
     times = []
     for _ in range(steps):
