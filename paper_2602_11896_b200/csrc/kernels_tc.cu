@@ -858,8 +858,12 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           const float re = v[2 * i], im = v[2 * i + 1];
           const float m2 = fmaf(re, re, im * im);
           const float s = m2 > th2 ? gv[i] * tc::rsqrt_approx(m2) : 0.f;
-          tc::split_tf32_fast(re * s, ghi[2 * i], glo[2 * i]);
-          tc::split_tf32_fast(im * s, ghi[2 * i + 1], glo[2 * i + 1]);
+          // (re, im) s and the lo halves as packed pairs (FMUL2 / FADD2); hi rounded on the integer pipe
+          const float2 g2 = tc::mul2(make_float2(re, im), make_float2(s, s));
+          const float2 h2 = make_float2(tc::tf32_rna(g2.x), tc::tf32_rna(g2.y));
+          const float2 l2 = tc::sub2(g2, h2);
+          ghi[2 * i] = h2.x; ghi[2 * i + 1] = h2.y;
+          glo[2 * i] = l2.x; glo[2 * i + 1] = l2.y;
         }
         // A2 buffer ab (TMEM) is free once the GEMM2 that last read it completed
         if (warp == 4 && lane == 0) TC_TRACE(6, g);

@@ -216,5 +216,19 @@ __device__ __forceinline__ void split_tf32_fast(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
+// packed FP32 pair ops (FMUL2 / FADD2 on sm_100a): one instruction for the re/im pair
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  float2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
+
 }  // namespace tc
 }  // namespace jtfs
