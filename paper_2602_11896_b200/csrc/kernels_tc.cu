@@ -362,7 +362,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
           for (int i = 0; i < 32; ++i) {
             const float mod = tc::sqrt_approx(fmaf(v[2 * i], v[2 * i], v[2 * i + 1] * v[2 * i + 1]));
 #pragma unroll
-            for (int r = 0; r < KAP; ++r) oacc[m][r] = fmaf(__shfl_sync(0xffffffffu, wl[r], i), mod, oacc[m][r]);
+            for (int r = 0; r < KAP; r += 2) {   // outputs r, r + 1 as one packed FMA (FFMA2, bit-identical)
+              const float2 w2 = make_float2(__shfl_sync(0xffffffffu, wl[r], i), __shfl_sync(0xffffffffu, wl[r + 1], i));
+              const float2 o2 = tc::fma2(w2, make_float2(mod, mod), make_float2(oacc[m][r], oacc[m][r + 1]));
+              oacc[m][r] = o2.x;
+              oacc[m][r + 1] = o2.y;
+            }
           }
         }
         if (warp == 4 && lane == 0) TC_TRACE(6, ge);
