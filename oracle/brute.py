@@ -91,3 +91,125 @@ def forward(plan: Plan, x: np.ndarray) -> np.ndarray:
     S = np.concatenate([np.ravel(o) for o in out])
     assert S.shape[0] == p.n_coef
     return S
+
+
+# ----------------------------------------------------------------------------------------------
+# Gradient by explicit adjoints, direct sums, no FFT and no autodiff: an
+# independent route to dE/dy (reading R20: through every stage incl. both pads and phi_F).
+# ----------------------------------------------------------------------------------------------
+
+def _circ_adj(h: np.ndarray, g: np.ndarray, s: int) -> np.ndarray:
+    """Adjoint of u -> _circ(h, u, s) along the last axis: the conjugate transpose of the same
+    [L/s, L] matrix, A^H g (no use of the Hermitian-kernel shortcut R21)."""
+    L = h.shape[0]
+    n = np.arange(L // s)[:, None] * s
+    m = np.arange(L)[None, :]
+    M = h[(n - m) % L]
+    return g @ M.conj()
+
+
+def _circ_rows_adj(h: np.ndarray, G: np.ndarray, s: int) -> np.ndarray:
+    return _circ_adj(h, G.T, s).T
+
+
+def _reflect_adj(plan: Plan, g_xp: np.ndarray) -> np.ndarray:
+    """Adjoint of R10's padding: each padded sample's gradient goes back to its source sample."""
+    N = plan.N
+    out = np.zeros(N)
+    for i in range(plan.N_pad):
+        t = (i - plan.pad_left) % (2 * N)
+        out[t if t < N else 2 * N - 1 - t] += g_xp[i]
+    return out
+
+
+EPS_MOD = 1e-12   # R22 (SPEC S:372): z/|z| := 0 where |z| < EPS_MOD * RMS(y)
+
+
+def _phase(z: np.ndarray, thr: float) -> np.ndarray:
+    """Adjoint factor of |.| (R22): z/|z|, 0 where |z| < thr (thr > 0)."""
+    a = np.abs(z)
+    keep = a >= thr
+    d = np.where(keep, a, 1.0)
+    return np.where(keep, z.real / d + 1j * (z.imag / d), 0.0)
+
+
+def loss_grad(plan: Plan, y: np.ndarray, S_target: np.ndarray) -> tuple[float, np.ndarray]:
+    """E = 1/2 sum_{orders 1,2} (S(y) - S_target)^2 (R19) and dE/dy for one signal, by reversing
+    `forward` stage by stage with the explicit adjoints above (modulus: g_z = (z/|z|) g_v)."""
+    p = plan
+    assert p.N_pad <= 4096, "brute force is for tiny configurations only"
+    S = forward(p, y)
+    r = S - np.asarray(S_target, dtype=np.float64)
+    r[: p.frames] = 0.0                                                  # S0 not in the loss
+    E = 0.5 * float(r @ r)
+    y = np.asarray(y, dtype=np.float64)
+    thr = max(EPS_MOD * float(np.sqrt(np.mean(y * y))), np.finfo(np.float64).tiny)
+    xp = _reflect(p, y)
+    f0, nfr = p.pad_left // p.T, p.frames
+    hT = lambda k: time_kernel_closed_form(p.phiT, p.N_pad, k)
+    hF = lambda k: time_kernel_closed_form(p.phiF, p.P, k)
+    hfr = lambda f: time_kernel_closed_form(p.L_fr[f], p.P, 0)
+
+    # forward intermediates of layer 1
+    h1 = [time_kernel_closed_form(p.psi1[n1], p.N_pad, 0) for n1 in range(p.N1)]
+    Z1 = [_circ(h1[n1], xp, 2 ** p.k1(n1)) for n1 in range(p.N1)]
+    U1 = [np.abs(z) for z in Z1]
+    g_U1 = [np.zeros(u.shape[0]) for u in U1]
+    off = nfr
+
+    # order 1 (spinned = False)
+    S1t = np.stack([_circ(hT(p.k1(n1)), U1[n1], 2 ** (p.log2T - p.k1(n1))).real for n1 in range(p.N1)])
+    X = np.zeros((p.P, S1t.shape[1]))
+    X[: p.N1] = S1t
+    rows1 = -(-p.N1 // p.F)
+    gX = np.zeros((p.P, S1t.shape[1]), dtype=np.complex128)
+    for f in range(p.n_fr_order1):
+        kf = p.k_fr(f)
+        W = _circ_rows(hfr(f), X, 2 ** kf)
+        gY = np.zeros((W.shape[0], W.shape[1]))
+        gY[:rows1, f0:f0 + nfr] = r[off:off + rows1 * nfr].reshape(rows1, nfr)
+        off += rows1 * nfr
+        if f == 0:
+            gW = gY.astype(np.complex128)
+        else:
+            V0 = np.abs(W)
+            V1 = _circ(hT(p.log2T), V0, 1).real
+            gV1 = _circ_rows_adj(hF(kf), gY[: V1.shape[0] >> (p.log2F - kf)], 2 ** (p.log2F - kf)).real
+            gV0 = _circ_adj(hT(p.log2T), gV1, 1).real
+            gW = _phase(W, thr) * gV0
+        gX += _circ_rows_adj(hfr(f), gW, 2 ** kf)
+    gS1t = gX[: p.N1].real
+    for n1 in range(p.N1):
+        k1 = p.k1(n1)
+        g_U1[n1] += _circ_adj(hT(k1), gS1t[n1], 2 ** (p.log2T - k1)).real
+
+    # order 2, depth-first per (block, filter)
+    for blk in p.blocks:
+        rows2 = -(-blk.n1_max // p.F)
+        T2 = p.N_pad >> blk.s2
+        h2 = [time_kernel_closed_form(p.psi2[blk.n2], p.N_pad, p.k1(n1)) for n1 in range(blk.n1_max)]
+        X = np.zeros((p.P, T2), dtype=np.complex128)
+        for n1 in range(blk.n1_max):
+            X[n1] = _circ(h2[n1], U1[n1], 2 ** (blk.s2 - p.k1(n1)))
+        for f in range(len(p.L_fr)):
+            kf = p.k_fr(f)
+            W = _circ_rows(hfr(f), X, 2 ** kf)
+            V0 = np.abs(W)
+            n_rows_F = W.shape[0] >> (p.log2F - kf)                     # P / F rows before the crop
+            gY = np.zeros((rows2, p.N_pad // p.T))
+            gY[:, f0:f0 + nfr] = r[off:off + rows2 * nfr].reshape(rows2, nfr)
+            off += rows2 * nfr
+            gV1 = np.zeros((n_rows_F, T2))
+            gV1[:rows2] = _circ_adj(hT(blk.s2), gY, 2 ** (p.log2T - blk.s2)).real
+            gV0 = _circ_rows_adj(hF(kf), gV1, 2 ** (p.log2F - kf)).real
+            gW = _phase(W, thr) * gV0
+            gXf = _circ_rows_adj(hfr(f), gW, 2 ** kf)
+            for n1 in range(blk.n1_max):
+                g_U1[n1] += _circ_adj(h2[n1], gXf[n1], 2 ** (blk.s2 - p.k1(n1))).real
+    assert off == p.n_coef
+
+    # layer 1 and the padding
+    g_xp = np.zeros(p.N_pad)
+    for n1 in range(p.N1):
+        g_xp += _circ_adj(h1[n1], _phase(Z1[n1], thr) * g_U1[n1], 2 ** p.k1(n1)).real
+    return E, _reflect_adj(p, g_xp)

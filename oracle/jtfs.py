@@ -51,14 +51,17 @@ class _Recompute(torch.autograd.Function):
         return gx, None
 
 
-# Reading R22 (modulus subgradient, after SPEC S:372's relative eps_mod): the phase z/|z| used by
-# the modulus adjoint is set to 0 where |z| <= MOD_TAU * max_t |y_b(t)| (per signal). The gradient
-# of |z| is ill-conditioned at |z| -> 0 (the phase of a vanishing quantity); the dead zone gives
-# both implementations one well-conditioned definition. The forward value |z| is unchanged.
-MOD_TAU = 1e-6
+# Reading R22 (modulus subgradient): the phase z/|z| of the modulus adjoint is 0 where
+# |z| < EPS_MOD * RMS(y_b) (per signal b, the "block" of S:372), at every modulus site (Z1, order-1
+# W, joint W). Everywhere else the adjoint is exactly PyTorch's (Kymatio's autograd):
+# g * z/|z|. The dead zone sits at the float64 rounding floor of the transforms (~1e-16 RMS), so it
+# only decides cells whose value is rounding noise (exactly silent stretches), where the phase -- and
+# with it the gradient -- is not determined by the arithmetic; for generic inputs it changes nothing
+# (tests/test_oracle_grad.py, R22 gives the measured effect at c2-c5).
+EPS_MOD = 1e-12
 
 
-class _ModulusDZ(torch.autograd.Function):
+class _Modulus(torch.autograd.Function):
     @staticmethod
     def forward(ctx, z, thr):
         a = z.abs()
@@ -68,14 +71,21 @@ class _ModulusDZ(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         z, a, thr = ctx.saved_tensors
-        keep = a > thr
+        keep = a >= thr
         phase = torch.where(keep, z / torch.where(keep, a, torch.ones_like(a)), torch.zeros_like(z))
         return g * phase, None
 
 
 def modulus(z: torch.Tensor, thr: torch.Tensor) -> torch.Tensor:
-    """Complex modulus (Eq.2) with the R22 adjoint; thr broadcasts per signal."""
-    return _ModulusDZ.apply(z, thr.reshape((-1,) + (1,) * (z.dim() - 1)).to(z.real.dtype))
+    """Complex modulus |z| (Eq.2, listing P:210) with the R22 adjoint; `thr` [B] broadcasts
+    per signal (thr = 0 gives torch.abs's own adjoint, sgn(0) = 0)."""
+    thr = thr.reshape((-1,) + (1,) * (z.dim() - 1)).to(z.real.dtype)
+    return _Modulus.apply(z, torch.clamp(thr, min=torch.finfo(z.real.dtype).tiny))
+
+
+def mod_threshold(y: torch.Tensor) -> torch.Tensor:
+    """R22 dead-zone radius per signal: EPS_MOD * RMS(y_b)."""
+    return EPS_MOD * y.detach().pow(2).mean(dim=1).sqrt()
 
 
 def subsample_fourier(X: torch.Tensor, k: int, dim: int = -1) -> torch.Tensor:
@@ -164,7 +174,7 @@ class Oracle:
     def layer1(self, x: torch.Tensor):
         """Padding (R10) + first layer + S0 + time-averaged S1 (Eq.3 time part)."""
         p = self.plan
-        self._thr = MOD_TAU * x.detach().abs().amax(dim=1)                  # R22 dead zone
+        self._thr = mod_threshold(x)                                         # R22
         xp = x[:, self.src]
         U0_hat = torch.fft.fft(xp.to(C128))                                  # P:203 (rfft, full circle)
         S0 = torch.fft.ifft(subsample_fourier(U0_hat * self.phiT().to(C128), p.T)).real

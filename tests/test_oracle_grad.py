@@ -3,15 +3,80 @@ import numpy as np
 import pytest
 import torch
 
-from oracle import metamer
+import oracle.jtfs as OJ
+from oracle import brute, metamer
 from oracle.jtfs import Oracle
 from oracle.plan import make_plan
 from synth import TINY, CONFIGS, plan_args, noise
 
 
+def _silent(y: np.ndarray) -> np.ndarray:
+    """y with an exactly silent stretch (the second quarter zeroed)."""
+    ys = np.array(y, dtype=np.float64, copy=True)
+    N = ys.shape[-1]
+    ys[..., N // 4:N // 2] = 0.0
+    return ys
+
+
+@pytest.mark.parametrize("name", ["t1", "t2", "spec"])
+@pytest.mark.parametrize("silent", [False, True], ids=["noise", "silent"])
+def test_gradient_two_routes(name, silent):
+    # Independent routes to dE/dy (SURVEY §8(c) O4): brute.loss_grad reverses the direct-sum forward
+    # with hand-written adjoints (conjugate-transpose matrices, explicit pad adjoint, no FFT, no
+    # autodiff); Oracle.loss_grad is autograd through the FFT route (P:126-130). With an exactly
+    # silent stretch the phases of rounding-noise cells would differ between the two routes; the R22
+    # dead zone (|z| < 1e-12 RMS, S:372) gives them one definition.
+    p = make_plan(*plan_args(TINY[name]))
+    o = Oracle(p)
+    x = noise(p.N, 1, seed=21).astype(np.float64)
+    y = noise(p.N, 1, seed=22).astype(np.float64)
+    if silent:
+        y = _silent(y)
+    St = o.forward(x)
+    E, g = o.loss_grad(y, St)
+    Eb, gb = brute.loss_grad(p, y[0], St[0].numpy())
+    assert abs(Eb - float(E[0])) <= 1e-12 * float(E[0])
+    # silent: cells just above the 1e-12 RMS radius keep only ~4 digits of phase in either route
+    # (float64 rounding ~1e-16 of the signal scale), so the routes agree to ~1e-6 there, not 1e-9
+    tol = 1e-5 if silent else 1e-9
+    assert np.linalg.norm(gb - g[0].numpy()) <= tol * np.linalg.norm(gb)
+
+
+def test_dead_zone_inactive_on_generic_inputs():
+    # R22: the dead zone sits at the rounding floor; on a generic input no modulus input lies in it,
+    # so the gradient equals the exact-phase (torch.sgn) gradient to rounding
+    p = make_plan(*plan_args(TINY["spec"]))
+    o = Oracle(p)
+    x, y = noise(p.N, 2, seed=31), noise(p.N, 2, seed=32)
+    St = o.forward(x)
+    _, g = o.loss_grad(y, St)
+    eps = OJ.EPS_MOD
+    try:
+        OJ.EPS_MOD = 0.0
+        _, g0 = o.loss_grad(y, St)
+    finally:
+        OJ.EPS_MOD = eps
+    assert float((g - g0).norm()) <= 1e-13 * float(g.norm())
+
+
+def test_dead_zone_effect_at_baseline_configs():
+    # The measured effect of the R22 dead zone on the float64 gradient at the BASELINE configs
+    # (tests/golden/r22_effect.json, written by tools/r22_effect.py, which calls only oracle/):
+    # |g(EPS_MOD = 1e-12) - g(EPS_MOD = 0)| / |g| <= 1e-5 on every recorded case.
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "r22_effect.json")
+    rec = json.load(open(path))
+    assert {"c2:all", "c4:0", "c4:11", "c5:11"} <= set(rec["cases"])
+    for case, v in rec["cases"].items():
+        assert v["rel_effect"] <= 1e-5, (case, v)
+
+
 @pytest.mark.parametrize("name", ["t1", "t2", "spec"])
 def test_gradient_finite_differences(name):
-    # SPEC S:362 / S:526: directional derivative vs central differences, >= 99% within 1e-4
+    # SPEC S:362 / S:526: directional derivative vs central differences along 100 random
+    # directions, >= 99% within 1e-4 (best of h in {1e-4, 1e-5, 1e-6} * |y|); the perturbed
+    # signals of all directions run as one batch through the oracle
     p = make_plan(*plan_args(TINY[name]))
     o = Oracle(p)
     x = noise(p.N, 1, seed=21).astype(np.float64)
@@ -19,21 +84,40 @@ def test_gradient_finite_differences(name):
     St = o.forward(x)
     E, g = o.loss_grad(y, St)
     rng = np.random.default_rng(3)
-    ok = 0
-    nd = 12
-    for _ in range(nd):
-        d = rng.standard_normal(y.shape)
-        d /= np.linalg.norm(d)
-        dd = float((g.numpy() * d).sum())
-        best = np.inf
-        for h in (1e-4, 1e-5, 1e-6):
-            hs = h * np.linalg.norm(y)
-            Ep = o.loss(o.forward(y + hs * d), St)
-            Em = o.loss(o.forward(y - hs * d), St)
-            fd = float((Ep - Em).sum() / (2 * hs))
-            best = min(best, abs(fd - dd) / max(abs(dd), 1e-12))
-        ok += best <= 1e-4
-    assert ok >= nd - 0 if nd < 100 else ok >= 0.99 * nd
+    nd = 100
+    D = rng.standard_normal((nd, p.N))
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    dd = D @ g[0].numpy()
+    best = np.full(nd, np.inf)
+    for h in (1e-4, 1e-5, 1e-6):
+        hs = h * np.linalg.norm(y)
+        Ep = o.loss(o.forward(y + hs * D), St.expand(nd, -1)).numpy()
+        Em = o.loss(o.forward(y - hs * D), St.expand(nd, -1)).numpy()
+        fd = (Ep - Em) / (2 * hs)
+        best = np.minimum(best, np.abs(fd - dd) / np.maximum(np.abs(dd), 1e-12))
+    assert (best <= 1e-4).sum() >= 99
+
+
+def test_adjoint_dot_products():
+    # SPEC "Invariants": <A u, v> = <u, A^H v> within 1e-10 for every linear stage of the explicit
+    # backward: decimating circular convolutions along time and along rows (filters + subsampling,
+    # complex kernels), the reflect padding, and the order-2 crop/zero-fill pair
+    rng = np.random.default_rng(5)
+    p = make_plan(*plan_args(TINY["spec"]))
+    cplx = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)
+    ip = lambda a, b: np.vdot(b, a)           # <a, b> = sum a conj(b)
+    from oracle.plan import time_kernel_closed_form as tk
+    for flt, L0, k, s in [(p.psi1[3], p.N_pad, 0, 2), (p.psi2[4], p.N_pad, 1, 4), (p.phiT, p.N_pad, 2, 2),
+                          (p.L_fr[2], p.P, 0, 1), (p.L_fr[-1], p.P, 0, 2), (p.phiF, p.P, 1, 2)]:
+        h = tk(flt, L0, k)
+        L = h.shape[0]
+        u, v = cplx(3, L), cplx(3, L // s)
+        assert abs(ip(brute._circ(h, u, s), v) - ip(u, brute._circ_adj(h, v, s))) <= 1e-10 * abs(ip(u, u))
+        U, V = cplx(L, 5), cplx(L // s, 5)
+        lhs = ip(brute._circ_rows(h, U, s), V)
+        assert abs(lhs - ip(U, brute._circ_rows_adj(h, V, s))) <= 1e-10 * abs(ip(U, U))
+    x, gp = rng.standard_normal(p.N), rng.standard_normal(p.N_pad)
+    assert abs(ip(brute._reflect(p, x), gp) - ip(x, brute._reflect_adj(p, gp))) <= 1e-10 * np.dot(gp, gp)
 
 
 def test_nullity_at_metamer():
