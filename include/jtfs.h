@@ -103,6 +103,8 @@ jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* S, 
 /* Loss and gradient (R19-R22). For each signal b:
  *   loss[b] = 1/2 sum_{orders 1,2} (S(y_b) - S_target_b)^2   (S0 excluded, R19)
  *   grad[b] = dE_b/dy_b, the TRUE gradient (the paper's "grad E" is its negative, R23).
+ *   Modulus adjoint (R22): the phase z/|z| is 0 where |z| < 1e-12 * RMS(y_b), at
+ *   every modulus site; elsewhere it is the exact phase (PyTorch autograd's).
  * y [B][N], S_target [B][n_coef], loss [B], grad [B][N]: device fp32.
  * shard/n_shards: second-order path shard (0,1 = whole). With n_shards > 1 the call computes the
  * contribution of order-2 units with (unit index mod n_shards) == shard, plus (shard 0 only)
@@ -118,6 +120,9 @@ typedef struct {
   float *y, *u, *y_prev, *g_prev, *mu, *loss_prev, *loss;
   int32_t* accepted;
   int64_t iter; /* incremented by each call (host field) */
+  const int32_t* active; /* [B] or NULL (all active): a signal with active[b] == 0 is frozen at its
+                            best iterate (y = y_prev, u = 0, mu and loss_prev kept, accepted = 0) --
+                            the host loop's early stop and rejection cap */
 } jtfs_metamer_state;
 
 /* One descent trial, entirely stream-ordered (no host sync): E, g = jtfs_loss_grad(y); per
@@ -127,6 +132,17 @@ typedef struct {
 jtfs_status metamer_step(jtfs_plan_t plan, jtfs_metamer_state* st, const float* S_target,
                          int64_t B, float momentum, float grow, float shrink, void* ws,
                          size_t ws_bytes, jtfs_stream_t stream);
+
+/* Colored Gaussian noise initialisation of the metamer loop (§2.3: "a colored Gaussian noise
+ * y0(t) whose power spectral density matches S1 x(t, lambda)"; reading R25 in DESIGN.md):
+ *   a[n1] = RMS over frames of the order-1 beta = 0 path of S_target, interpolated at row n1 / F;
+ *   g[n1] = a[n1] / sqrt(pi/4 * nu[n1]),  nu[n1] = (1/N_pad) sum_m |psi1_hat_n1[m]|^2;
+ *   G[m]  = sum_n1 g[n1] |psi1_hat_n1(|w_m|)|^2 / (sum_n1 |psi1_hat_n1(|w_m|)|^2 + delta);
+ *   y0    = Re IFFT(FFT(white) G) on samples [pad_left, pad_left + N)  (1e-4 white if a == 0).
+ * S_target [B][n_coef] (packed, R15), white [B][N_pad] standard-normal draws (the caller's random
+ * numbers), y0 [B][N] out: device fp32. ws as for jtfs_forward (micro-batched). Stream-ordered. */
+jtfs_status jtfs_colored_noise(jtfs_plan_t plan, const float* S_target, const float* white, int64_t B,
+                               float* y0, void* ws, size_t ws_bytes, jtfs_stream_t stream);
 
 /* End-to-end variants with HOST buffers (pinned or pageable): copy inputs host->device, run, copy
  * results device->host, synchronise `stream`. The library allocates device staging of the given

@@ -38,7 +38,8 @@ class PathT(ctypes.Structure):
 class MetamerState(ctypes.Structure):
     _fields_ = [("y", ctypes.c_void_p), ("u", ctypes.c_void_p), ("y_prev", ctypes.c_void_p),
                 ("g_prev", ctypes.c_void_p), ("mu", ctypes.c_void_p), ("loss_prev", ctypes.c_void_p),
-                ("loss", ctypes.c_void_p), ("accepted", ctypes.c_void_p), ("iter", ctypes.c_int64)]
+                ("loss", ctypes.c_void_p), ("accepted", ctypes.c_void_p), ("iter", ctypes.c_int64),
+                ("active", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p
@@ -58,6 +59,7 @@ _SIGS = {
     "jtfs_loss_grad": (_I, [_P, _P, _P, _I64, _P, _P, _I, _I, _P, _SZ, _P]),
     "metamer_step": (_I, [_P, ctypes.POINTER(MetamerState), _P, _I64, ctypes.c_float, ctypes.c_float,
                           ctypes.c_float, _P, _SZ, _P]),
+    "jtfs_colored_noise": (_I, [_P, _P, _P, _I64, _P, _P, _SZ, _P]),
     "jtfs_host_staging_size": (_SZ, [_P, _I64, _I]),
     "jtfs_loss_grad_host": (_I, [_P, _P, _P, _I64, _P, _P, _P, _SZ, _P]),
     "jtfs_last_error": (ctypes.c_char_p, []),

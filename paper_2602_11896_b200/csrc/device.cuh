@@ -34,6 +34,9 @@ struct FfList {                    // blocks on the FFT route of the joint stage
 
 struct DeviceTables {
   float* spec_vals = nullptr;
+  double* spec_vals_d = nullptr;   // float64 psi1 spectra (l1_jobs)
+  double* cn_nu = nullptr;          // colored-noise tables (R25)
+  float* cn_den = nullptr;
   GatherJob* l1_jobs = nullptr;     int64_t* l1_tiles = nullptr;   int n_l1 = 0;   int64_t l1_ntiles = 0;
   GatherJob* s1_jobs = nullptr;     int64_t* s1_tiles = nullptr;   int n_s1 = 0;   int64_t s1_ntiles = 0;
   GatherJob* l2_jobs = nullptr;     int64_t* l2_tiles = nullptr;   int n_l2 = 0;   int64_t l2_ntiles = 0;
@@ -97,11 +100,13 @@ void launch_reflect_pad(const float* x, int64_t sx, double2* xp, const Plan& p, 
 void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
                    const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
 void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
-                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
+                      const int64_t* tiles, int njobs, int64_t ntiles, const double* vals, int B, cudaStream_t st);
 void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
                       const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
-void launch_modulus(const float2* z, int64_t zsb, float2* u, int64_t usb, int64_t n_per_b, int B,
+void launch_modulus(const float2* z, int64_t zsb, double2* u, int64_t usb, int64_t n_per_b, int B,
                     cudaStream_t st);
+void launch_real_rows_d(const double2* in, int64_t in_sb, float* out, int64_t out_sb, int64_t n, int B,
+                        cudaStream_t st);
 void launch_real_rows(const float2* in, int64_t in_sb, int64_t in_off, float* out, int64_t out_sb,
                       int64_t out_off, int64_t n, int B, cudaStream_t st);
 void launch_s0_out(const float2* s0c, int64_t s0_sb, float* S, int64_t S_sb, const Plan& p, int B,
@@ -111,18 +116,26 @@ void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS
                           cudaStream_t st);
 void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
                       const float* thr, int B, cudaStream_t st);
-// reading R22: the modulus adjoint uses phase 0 where |z| <= kModTau * max_t |y_b(t)|
-constexpr float kModTau = 1e-6f;
-void launch_absmax(const float* y, int64_t N, float tau, float* thr, int B, cudaStream_t st);
+// reading R22: the modulus adjoint uses phase 0 where |z| < kEpsMod * RMS(y_b)
+constexpr float kEpsMod = 1e-12f;
+void launch_mod_threshold(const float* y, int64_t N, float eps, float* thr, int B, cudaStream_t st);
 void launch_adj_gather_x(const Plan& p, const DeviceTables& d, const float2* GZ, int64_t GZ_sb, float2* out,
                          int64_t out_sb, int B, cudaStream_t st);
 void launch_real_to_complex(const float* in, int64_t in_sb, float2* out, int64_t out_sb, int64_t n, int B,
                             cudaStream_t st);
 void launch_reflect_adj(const float2* gxp, int64_t sxp, float* g, int64_t sg, const Plan& p, int B,
                         cudaStream_t st);
+// colored-noise initialisation (R25): per-band gains from the order-1 beta = 0 path of S_target
+// (g [B][N1 + 1], last entry = fallback flag), spectral shaping of X = FFT(white), crop of the IFFT
+void launch_cn_gains(const Plan& p, const DeviceTables& d, const float* St, int64_t St_sb, float* g, int64_t g_sb,
+                     int B, cudaStream_t st);
+void launch_cn_shape(const Plan& p, const DeviceTables& d, float2* X, int64_t X_sb, const float* g, int64_t g_sb,
+                     int B, cudaStream_t st);
+void launch_cn_crop(const Plan& p, const float2* X, int64_t X_sb, const float* white, const float* g, int64_t g_sb,
+                    float* y0, int B, cudaStream_t st);
 void launch_metamer(float* y, float* u, float* y_prev, float* g_prev, float* mu, float* loss_prev,
-                    const float* loss, int32_t* accepted, const float* g, int64_t sg, int64_t N, int B,
-                    float momentum, float grow, float shrink, cudaStream_t st);
+                    const float* loss, int32_t* accepted, const int32_t* active, const float* g, int64_t sg,
+                    int64_t N, int B, float momentum, float grow, float shrink, cudaStream_t st);
 
 // ---- kernels_fr.cu
 void launch_o1_fwd(const Plan& p, const DeviceTables& d, const float* S1t, int64_t S1t_sb, float2* W1,

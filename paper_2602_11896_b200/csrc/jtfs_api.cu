@@ -64,7 +64,7 @@ static Fanout* fanout_get(int lane) {
   static thread_local std::vector<Fanout*> per_dev;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int slot = dev * kMaxLanes + lane;
+  const int slot = dev * (kMaxLanes + 1) + lane;   // slots 0..kMaxLanes-1: per-lane fan-out sets; kMaxLanes: the lane streams
   if ((int)per_dev.size() <= slot) per_dev.resize(slot + 1, nullptr);
   if (!per_dev[slot]) {
     Fanout* f = new Fanout();
@@ -147,7 +147,7 @@ static std::vector<int64_t> prefix(const std::vector<int64_t>& counts) {
 
 static void free_tables(DeviceTables* d) {
   if (!d) return;
-  void* ptrs[] = {d->spec_vals, d->l1_jobs, d->l1_tiles, d->s1_jobs, d->s1_tiles, d->l2_jobs, d->l2_tiles,
+  void* ptrs[] = {d->spec_vals, d->spec_vals_d, d->cn_nu, d->cn_den, d->l1_jobs, d->l1_tiles, d->s1_jobs, d->s1_tiles, d->l2_jobs, d->l2_tiles,
                   d->s0_job, d->s0_tiles, d->psi1_sup, d->psi2_sup, d->phiT_sup, d->hfr, d->phiF_k,
                   d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
                   d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_owner_unit, d->l1_off,
@@ -185,6 +185,9 @@ static cudaError_t upload(Plan& p) {
 #define UP(v, f) \
   if ((e = up(v, &d->f)) != cudaSuccess) { free_tables(d); return e; }
   UP(p.spec_vals, spec_vals);
+  UP(p.spec_vals_d, spec_vals_d);
+  UP(p.cn_nu, cn_nu);
+  UP(p.cn_den, cn_den);
   auto job_tiles = [](const std::vector<GatherJob>& jobs) {
     std::vector<int64_t> c;
     for (auto& j : jobs) c.push_back((j.L_out + kGatherTile - 1) / kGatherTile);
@@ -481,15 +484,16 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     if ((e = fft_launch_dd(xpd, Xhd, ri, ro, mb, false, d.fftt, st))) return e;
   }
   // A2: layer 1: cdgmm + subsample_fourier (float64), ifft (float64 -> complex64 Z1),
-  // modulus, fft (complex64)
-  launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals, mb, st);
+  // modulus (-> float64 rows), fft (float64 -> complex64 U1_hat)
+  launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals_d, mb, st);
   if ((e = fft_groups_df(Ad, w.Z1, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt, st)))
     return e;
-  launch_modulus(w.Z1, w.s_L1, w.A, w.s_A, p.sumL1, mb, st);  // A rows use the L1 layout
+  launch_modulus(w.Z1, w.s_L1, Ad, sAd, p.sumL1, mb, st);  // A rows (complex128) use the L1 layout
   RET();
   if (stop == 1) return cudaSuccess;
-  if ((e = fft_groups(w.A, w.U1h, w.s_A, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, false, d.fftt,
-                      st)))
+  // U1_hat = FFT(U1) in float64, rounded to complex64 per bin (R22 precision)
+  if ((e = fft_groups_df(Ad, w.U1h, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, false, d.fftt,
+                         st)))
     return e;
   // S0 and S1 time averages (Eq.3 time part)
   launch_gather_df(Xhd, sd, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
@@ -551,7 +555,12 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
       return e;
   }
   // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)
-  launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, w.thr, mb, st);
+  // order 1 belongs to shard 0 (its forward W1/V2 exist only there): other shards contribute g_S1t = 0
+  if (shard == 0) {
+    launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, w.thr, mb, st);
+  } else if ((e = cudaMemsetAsync(w.gS1t, 0, (size_t)w.s_S1t * 4 * mb, st))) {
+    return e;
+  }
   launch_real_to_complex(w.gS1t, w.s_S1t, w.cs, w.s_c, N1 * p.Ft, mb, st);
   if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, N1, p.Ft, mb, false, st))) return e;
   // A8: g_hat_U1 -> U1h ; g_U1 = Re IFFT -> A
@@ -795,7 +804,7 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
   // gather stages. Per-signal results do not depend on the lane or micro-batch.
   const int lanes = (g_lanes > 1 && mb >= 2 && B >= 2) ? 2 : 1;
   const int mbl = mb / lanes;
-  Fanout* fl = lanes > 1 ? fanout_get(kMaxLanes - 1) : nullptr;   // lane streams: fl->s[0], fl->s[1]
+  Fanout* fl = lanes > 1 ? fanout_get(kMaxLanes) : nullptr;   // lane streams: fl->s[0], fl->s[1] (own slot)
   if (lanes > 1) {
     cudaEventRecord(fl->fork, st);
     for (int l = 0; l < lanes; ++l) cudaStreamWaitEvent(fl->s[l], fl->fork, 0);
@@ -809,14 +818,15 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
     float* lossp = mstate ? mstate->loss + b0 : loss + b0;
     launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, (double*)w.loss, shard,
                 n_shards, n, ls);
-    launch_absmax(y + b0 * p.N, p.N, kModTau, w.thr, n, ls);
+    launch_mod_threshold(y + b0 * p.N, p.N, kEpsMod, w.thr, n, ls);
     float* gp = mstate ? w.g : grad + b0 * p.N;
     int64_t sg = mstate ? w.s_g : p.N;
     CK(run_backward(p, w, gp, sg, n, shard, n_shards, ls, l));
     if (mstate) {
       launch_metamer(mstate->y + b0 * p.N, mstate->u + b0 * p.N, mstate->y_prev + b0 * p.N,
                      mstate->g_prev + b0 * p.N, mstate->mu + b0, mstate->loss_prev + b0, lossp,
-                     mstate->accepted + b0, gp, sg, p.N, n, momentum, grow, shrink, ls);
+                     mstate->accepted + b0, mstate->active ? mstate->active + b0 : nullptr, gp, sg, p.N, n,
+                     momentum, grow, shrink, ls);
       CK(cudaGetLastError());
     }
     }
@@ -881,6 +891,32 @@ jtfs_status jtfs_loss_grad_host(jtfs_plan_t plan, const float* y_host, const flo
   return JTFS_OK;
 }
 
+jtfs_status jtfs_colored_noise(jtfs_plan_t plan, const float* S_target, const float* white, int64_t B, float* y0,
+                               void* ws, size_t ws_bytes, jtfs_stream_t stream) {
+  int mb;
+  jtfs_status s = check_common(plan, B, ws_bytes, 0, ws, &mb);
+  if (s) return s;
+  if (!S_target || !white || !y0) return fail(JTFS_ERR_SIZE, "NULL argument");
+  const Plan& p = plan->p;
+  if ((p.psi1.size() + p.F - 1) / p.F > 1024) return fail(JTFS_ERR_CONFIG, "more than 1024 order-1 rows");
+  Layout L = layout(p, 0);
+  Bufs w = carve(p, L, (char*)ws, mb);
+  cudaStream_t st = (cudaStream_t)stream;
+  const DeviceTables& d = *p.dev;
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    const int n = (int)std::min<int64_t>(mb, B - b0);
+    launch_cn_gains(p, d, S_target + b0 * p.n_coef, p.n_coef, w.S1t, w.s_S1t, n, st);
+    launch_real_to_complex(white + b0 * p.N_pad, p.N_pad, w.xp, w.s_xp, p.N_pad, n, st);
+    CK(fft_rows(p, w.xp, w.s_xp, w.Xh, w.s_xp, 0, 1, p.N_pad, n, false, st));
+    launch_cn_shape(p, d, w.Xh, w.s_xp, w.S1t, w.s_S1t, n, st);
+    CK(fft_rows(p, w.Xh, w.s_xp, w.xp, w.s_xp, 0, 1, p.N_pad, n, true, st));
+    launch_cn_crop(p, w.xp, w.s_xp, white + b0 * p.N_pad, w.S1t, w.s_S1t, y0 + b0 * p.N, n, st);
+    CK(cudaGetLastError());
+  }
+  t_err.clear();
+  return JTFS_OK;
+}
+
 jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_t B, void* out, size_t out_bytes,
                              void* ws, size_t ws_bytes, jtfs_stream_t stream) {
   int mb;
@@ -895,7 +931,7 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
   if (stage == 1) {
     if (out_bytes < (size_t)B * p.sumL1 * 4) return fail(JTFS_ERR_SIZE, "out too small");
     CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 1));
-    launch_real_rows(w.A, w.s_A, 0, (float*)out, p.sumL1, 0, p.sumL1, n, st);
+    launch_real_rows_d(reinterpret_cast<const double2*>(w.A), w.s_A / 2, (float*)out, p.sumL1, p.sumL1, n, st);
   } else if (stage == 2) {
     int64_t per = (int64_t)p.psi1.size() * p.Ft;
     if (out_bytes < (size_t)B * per * 4) return fail(JTFS_ERR_SIZE, "out too small");

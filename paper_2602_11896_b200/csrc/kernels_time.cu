@@ -46,12 +46,12 @@ template <> struct GAcc<double2> { using T = double2; using R = double; };
 __device__ __forceinline__ void st_c(float2* p, double re, double im) { *p = make_float2((float)re, (float)im); }
 __device__ __forceinline__ void st_c(double2* p, double re, double im) { *p = make_double2(re, im); }
 
-template <class TI, class TO>
+template <class TI, class TO, class VT>
 __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict__ in, int64_t in_sb,
                                                             TO* __restrict__ out, int64_t out_sb,
                                                             const GatherJob* __restrict__ jobs,
                                                             const int64_t* __restrict__ tiles, int njobs,
-                                                            const float* __restrict__ vals) {
+                                                            const VT* __restrict__ vals) {
   using R = typename GAcc<TI>::R;
   const int64_t tile = blockIdx.x;
   const int b = blockIdx.y;
@@ -73,12 +73,12 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
   }
 }
 
-template <class TI, class TO>
+template <class TI, class TO, class VT>
 static void gather_t(const TI* in, int64_t in_sb, TO* out, int64_t out_sb, const GatherJob* jobs,
-                     const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+                     const int64_t* tiles, int njobs, int64_t ntiles, const VT* vals, int B, cudaStream_t st) {
   if (njobs <= 0 || ntiles <= 0) return;
   dim3 g((unsigned)ntiles, (unsigned)B);
-  k_gather<TI, TO><<<g, kGatherThreads, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
+  k_gather<TI, TO, VT><<<g, kGatherThreads, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
   count_launch();
 }
 void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
@@ -86,7 +86,7 @@ void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb,
   gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
 }
 void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
-                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
+                      const int64_t* tiles, int njobs, int64_t ntiles, const double* vals, int B, cudaStream_t st) {
   gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
 }
 void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
@@ -94,19 +94,36 @@ void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out
   gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
 }
 
-// U1 = |Z1|, stored as a complex row with zero imaginary part for the next FFT.
-__global__ void k_modulus(const float2* __restrict__ z, int64_t zsb, float2* __restrict__ u, int64_t usb,
+// U1 = |Z1|, stored as a float64 complex row with zero imaginary part for the next FFT
+// (P:211), which runs in float64: the FFT's rounding is relative to the whole row (dominated by the
+// envelope's mean), and the second-layer bands it feeds are far below that (reading R22).
+__global__ void k_modulus(const float2* __restrict__ z, int64_t zsb, double2* __restrict__ u, int64_t usb,
                           int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float2 v = z[blockIdx.y * zsb + i];
-  u[blockIdx.y * usb + i] = make_float2(sqrtf(v.x * v.x + v.y * v.y), 0.f);
+  u[blockIdx.y * usb + i] = make_double2((double)sqrtf(v.x * v.x + v.y * v.y), 0.0);
 }
 
-void launch_modulus(const float2* z, int64_t zsb, float2* u, int64_t usb, int64_t n_per_b, int B,
+void launch_modulus(const float2* z, int64_t zsb, double2* u, int64_t usb, int64_t n_per_b, int B,
                     cudaStream_t st) {
   dim3 g((unsigned)((n_per_b + 255) / 256), (unsigned)B);
   k_modulus<<<g, 256, 0, st>>>(z, zsb, u, usb, n_per_b);
+  count_launch();
+}
+
+// real parts of float64 complex rows -> fp32 (debug stage U1)
+__global__ void k_real_rows_d(const double2* __restrict__ in, int64_t in_sb, float* __restrict__ out, int64_t out_sb,
+                              int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[blockIdx.y * out_sb + i] = (float)in[blockIdx.y * in_sb + i].x;
+}
+
+void launch_real_rows_d(const double2* in, int64_t in_sb, float* out, int64_t out_sb, int64_t n, int B,
+                        cudaStream_t st) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
+  k_real_rows_d<<<g, 256, 0, st>>>(in, in_sb, out, out_sb, n);
   count_launch();
 }
 
@@ -210,18 +227,19 @@ void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS
   count_launch();
 }
 
-// Modulus adjoint (R22): g_Z1 = (Z1/|Z1|) * Re(g_U1), 0 where |Z1| = 0.
+// Modulus adjoint (R22): g_Z1 = (Z1/|Z1|) * Re(g_U1), 0 where |Z1| < thr (in float64: Z1 is the
+// complex64 copy of the float64 first layer, and cells down to the dead zone keep their phase).
 __global__ void k_phase_mul(const float2* __restrict__ z, const float2* __restrict__ gu, int64_t gsb,
                             float2* __restrict__ out, int64_t n, int64_t sb, const float* __restrict__ thr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t o = blockIdx.y * sb + i;
-  float2 v = z[o];
-  float m2 = v.x * v.x + v.y * v.y;
-  float g = gu[blockIdx.y * gsb + i].x;
-  const float t = thr[blockIdx.y];
-  float s = (m2 > 1.17549435e-38f && m2 > t * t) ? g * rsqrtf(m2) : 0.f;
-  out[o] = make_float2(v.x * s, v.y * s);
+  const float2 v = z[o];
+  const double m2 = (double)v.x * v.x + (double)v.y * v.y;
+  const double g = gu[blockIdx.y * gsb + i].x;
+  const double t = thr[blockIdx.y];
+  const double s = (m2 > 0.0 && m2 >= t * t) ? g / sqrt(m2) : 0.0;
+  out[o] = make_float2((float)(v.x * s), (float)(v.y * s));
 }
 
 void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
@@ -231,24 +249,25 @@ void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* ou
   count_launch();
 }
 
-// R22 dead zone of the modulus adjoint: thr[b] = tau * max_t |y_b(t)| (tau = 1e-6)
-__global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ y, int64_t N, float tau,
-                                                float* __restrict__ thr) {
-  __shared__ float red[256];
+// R22 dead-zone radius of the modulus adjoint: thr[b] = eps * RMS(y_b), eps = 1e-12;
+// float64 partial sums combined in a fixed tree order (deterministic)
+__global__ void __launch_bounds__(256) k_mod_threshold(const float* __restrict__ y, int64_t N, float eps,
+                                                       float* __restrict__ thr) {
+  __shared__ double red[256];
   const float* src = y + (int64_t)blockIdx.x * N;
-  float m = 0.f;
-  for (int64_t i = threadIdx.x; i < N; i += 256) m = fmaxf(m, fabsf(src[i]));
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += 256) m += (double)src[i] * (double)src[i];
   red[threadIdx.x] = m;
   __syncthreads();
   for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
     __syncthreads();
   }
-  if (threadIdx.x == 0) thr[blockIdx.x] = tau * red[0];
+  if (threadIdx.x == 0) thr[blockIdx.x] = (float)((double)eps * sqrt(red[0] / (double)N));
 }
 
-void launch_absmax(const float* y, int64_t N, float tau, float* thr, int B, cudaStream_t st) {
-  k_absmax<<<B, 256, 0, st>>>(y, N, tau, thr);
+void launch_mod_threshold(const float* y, int64_t N, float eps, float* thr, int B, cudaStream_t st) {
+  k_mod_threshold<<<B, 256, 0, st>>>(y, N, eps, thr);
   count_launch();
 }
 
@@ -332,11 +351,107 @@ void launch_reflect_adj(const float2* gxp, int64_t sxp, float* g, int64_t sg, co
   count_launch();
 }
 
+// ---- colored-noise initialisation ("a colored Gaussian noise y0 whose power spectral density
+// matches S1 x"; reading R25): per-band gains g[n1] = a[n1] / sqrt(pi/4 nu[n1]) where a is the
+// per-row RMS (over frames) of the order-1 beta = 0 path of S_target interpolated at rho = n1 / F.
+__global__ void __launch_bounds__(256) k_cn_gains(const float* __restrict__ St, int64_t St_sb, float* __restrict__ g,
+                                                  int64_t g_sb, const double* __restrict__ nu, int64_t off,
+                                                  int rows, int64_t frames, int N1, int F) {
+  __shared__ double r[1024];
+  __shared__ int any;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int rho = threadIdx.x; rho < rows; rho += blockDim.x) {
+    const float* s = St + b * St_sb + off + (int64_t)rho * frames;
+    double acc = 0.0;
+    for (int64_t t = 0; t < frames; ++t) acc += (double)s[t] * (double)s[t];
+    r[rho] = sqrt(acc / (double)frames);
+    if (r[rho] > 0.0) any = 1;
+  }
+  __syncthreads();
+  for (int n1 = threadIdx.x; n1 < N1; n1 += blockDim.x) {
+    const double pos = (double)n1 / (double)F;     // np.interp semantics: clamp beyond the last row
+    int i0 = (int)floor(pos);
+    double a;
+    if (i0 >= rows - 1) a = r[rows - 1];
+    else a = r[i0] + (pos - (double)i0) * (r[i0 + 1] - r[i0]);
+    g[b * g_sb + n1] = (float)(a / sqrt(0.78539816339744831 * nu[n1]));
+  }
+  if (threadIdx.x == 0) g[b * g_sb + N1] = any ? 0.f : 1.f;   // 1 = all-zero profile: white fallback
+}
+
+void launch_cn_gains(const Plan& p, const DeviceTables& d, const float* St, int64_t St_sb, float* g, int64_t g_sb,
+                     int B, cudaStream_t st) {
+  const int rows = (int)((p.psi1.size() + p.F - 1) / p.F);
+  k_cn_gains<<<B, 256, 0, st>>>(St, St_sb, g, g_sb, d.cn_nu, p.frames, rows, p.frames, (int)p.psi1.size(),
+                                (int)p.F);
+  count_launch();
+}
+
+// X[m] *= G[m], G[m] = sum_n1 g[n1] |psi1_hat(m')|^2 / den[m'], m' = min(m, N_pad - m) (even: y0 real);
+// the filters meeting bin m' come from the per-256-bin CSR list of the layer-1 adjoint gather
+__global__ void __launch_bounds__(256) k_cn_shape(float2* __restrict__ X, int64_t X_sb, const float* __restrict__ g,
+                                                  int64_t g_sb, const int32_t* __restrict__ tstart,
+                                                  const int32_t* __restrict__ list, const Support* __restrict__ sup,
+                                                  const float* __restrict__ vals, const float* __restrict__ den,
+                                                  int64_t N_pad, int64_t tile) {
+  const int b = blockIdx.y;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= N_pad) return;
+  const int64_t mm = m <= N_pad / 2 ? m : N_pad - m;
+  const int64_t tl = mm / tile;
+  float acc = 0.f;
+  for (int q = tstart[tl]; q < tstart[tl + 1]; ++q) {
+    const int n1 = list[q];
+    const Support sp = sup[n1];
+    int64_t t = (mm - sp.lo) % N_pad;
+    if (t < 0) t += N_pad;
+    if (t < sp.len) {
+      const float h = __ldg(vals + sp.off + t);
+      acc = fmaf(g[b * g_sb + n1] * h, h, acc);
+    }
+  }
+  const float G = acc / den[mm];
+  float2* x = X + b * X_sb + m;
+  *x = make_float2(x->x * G, x->y * G);
+}
+
+void launch_cn_shape(const Plan& p, const DeviceTables& d, float2* X, int64_t X_sb, const float* g, int64_t g_sb,
+                     int B, cudaStream_t st) {
+  dim3 gr((unsigned)((p.N_pad + 255) / 256), (unsigned)B);
+  k_cn_shape<<<gr, 256, 0, st>>>(X, X_sb, g, g_sb, d.gx_tile_start, d.gx_list, d.psi1_sup, d.spec_vals, d.cn_den,
+                                 p.N_pad, p.gx_tile);
+  count_launch();
+}
+
+// y0[i] = Re X[pad_left + i] (the IFFT output), or 1e-4 white[pad_left + i] for an all-zero profile
+__global__ void k_cn_crop(const float2* __restrict__ X, int64_t X_sb, const float* __restrict__ white,
+                          const float* __restrict__ g, int64_t g_sb, float* __restrict__ y0, int64_t N,
+                          int64_t N_pad, int64_t pad_left, int N1) {
+  const int b = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const bool fb = g[b * g_sb + N1] != 0.f;
+  y0[b * N + i] = fb ? 1e-4f * white[b * N_pad + pad_left + i] : X[b * X_sb + pad_left + i].x;
+}
+
+void launch_cn_crop(const Plan& p, const float2* X, int64_t X_sb, const float* white, const float* g, int64_t g_sb,
+                    float* y0, int B, cudaStream_t st) {
+  dim3 gr((unsigned)((p.N + 255) / 256), (unsigned)B);
+  k_cn_crop<<<gr, 256, 0, st>>>(X, X_sb, white, g, g_sb, y0, p.N, p.N_pad, p.pad_left, (int)p.psi1.size());
+  count_launch();
+}
+
 // ---- metamer update (R23-R24): per-signal bold-driver decision, then momentum step.
-__global__ void k_metamer_decide(float* mu, float* loss_prev, const float* loss, int32_t* accepted, int B,
-                                 float grow, float shrink) {
+__global__ void k_metamer_decide(float* mu, float* loss_prev, const float* loss, int32_t* accepted,
+                                 const int32_t* active, int B, float grow, float shrink) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
+  if (active && !active[b]) {   // frozen (early stop / rejection cap): state kept
+    accepted[b] = 0;
+    return;
+  }
   float E = loss[b];
   if (E <= loss_prev[b]) {
     accepted[b] = 1;
@@ -350,12 +465,17 @@ __global__ void k_metamer_decide(float* mu, float* loss_prev, const float* loss,
 
 __global__ void k_metamer_apply(float* __restrict__ y, float* __restrict__ u, float* __restrict__ y_prev,
                                 float* __restrict__ g_prev, const float* __restrict__ mu,
-                                const int32_t* __restrict__ accepted, const float* __restrict__ g, int64_t sg,
-                                int64_t N, float momentum) {
+                                const int32_t* __restrict__ accepted, const int32_t* __restrict__ active,
+                                const float* __restrict__ g, int64_t sg, int64_t N, float momentum) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int b = blockIdx.y;
   const int64_t o = (int64_t)b * N + i;
+  if (active && !active[b]) {   // frozen at the best iterate
+    y[o] = y_prev[o];
+    u[o] = 0.f;
+    return;
+  }
   float gg, yy, uu;
   if (accepted[b]) {
     yy = y[o];
@@ -374,11 +494,11 @@ __global__ void k_metamer_apply(float* __restrict__ y, float* __restrict__ u, fl
 }
 
 void launch_metamer(float* y, float* u, float* y_prev, float* g_prev, float* mu, float* loss_prev,
-                    const float* loss, int32_t* accepted, const float* g, int64_t sg, int64_t N, int B,
-                    float momentum, float grow, float shrink, cudaStream_t st) {
-  k_metamer_decide<<<(B + 127) / 128, 128, 0, st>>>(mu, loss_prev, loss, accepted, B, grow, shrink);
+                    const float* loss, int32_t* accepted, const int32_t* active, const float* g, int64_t sg,
+                    int64_t N, int B, float momentum, float grow, float shrink, cudaStream_t st) {
+  k_metamer_decide<<<(B + 127) / 128, 128, 0, st>>>(mu, loss_prev, loss, accepted, active, B, grow, shrink);
   dim3 gr((unsigned)((N + 255) / 256), (unsigned)B);
-  k_metamer_apply<<<gr, 256, 0, st>>>(y, u, y_prev, g_prev, mu, accepted, g, sg, N, momentum);
+  k_metamer_apply<<<gr, 256, 0, st>>>(y, u, y_prev, g_prev, mu, accepted, active, g, sg, N, momentum);
   count_launch(2);
 }
 

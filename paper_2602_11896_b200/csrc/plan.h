@@ -136,6 +136,12 @@ struct Plan {
   // kernels
   std::vector<float> spec_vals;                 // all support-limited spectra
   std::vector<Support> psi1_sup;                // [N1] on N_pad
+  std::vector<double> spec_vals_d;              // float64 psi1 spectra of the forward first layer
+  std::vector<Support> psi1_sup_d;              // [N1] on N_pad, offsets into spec_vals_d (l1_jobs)
+  // colored-noise initialisation (reading R25): nu[n1] = (1/N_pad) sum_m |psi1_hat[m]|^2,
+  // den[m] = sum_n1 |psi1_hat(m/N_pad)|^2 + delta for m in [0, N_pad/2]
+  std::vector<double> cn_nu;
+  std::vector<float> cn_den;
   std::vector<Support> psi2_sup;                // [n_blocks][log2T+1] on N_pad>>k (len 0 unused)
   std::vector<Support> phiT_sup;                // [log2T+1] on N_pad>>k
   std::vector<float> hfr;                       // [n_fr_all][P][2] row kernels (complex)

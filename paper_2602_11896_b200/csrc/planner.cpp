@@ -79,19 +79,21 @@ void level_response(const Filter& f, int64_t L0, int k, std::vector<double>* out
   for (int64_t m = 0; m < L; ++m) (*out)[m] = response_level_nu(f, k, (double)m / (double)L);
 }
 
-// Support (bins where |response| may exceed 1e-10) of the level-k response on an L-bin grid.
-static Support support_of(const Filter& f, int k, int64_t L, std::vector<float>* vals) {
+// Support (bins where |response| may exceed `cut`, relative to the Gaussian peak) of the level-k response
+// on an L-bin grid; the values are appended to *vals (float or double).
+template <class V>
+static Support support_of(const Filter& f, int k, int64_t L, std::vector<V>* vals, double cut = 1e-10) {
   double sc = std::ldexp(1.0, k);
   double s = f.sigma * sc, c = f.xi * sc;
   double a, b;
   if (f.phi) {
-    double w = std::sqrt(2 * std::log(1e10));
+    double w = std::sqrt(2 * std::log(1.0 / cut));
     a = -w * s; b = w * s;
   } else {
-    double w = std::sqrt(2 * std::log(2e10));
+    double w = std::sqrt(2 * std::log(2.0 / cut));
     a = c - w * s; b = c + w * s;
-    if (2e10 * f.kappa > 1.0) {
-      double w2 = std::sqrt(2 * std::log(2e10 * f.kappa));
+    if (2.0 / cut * f.kappa > 1.0) {
+      double w2 = std::sqrt(2 * std::log(2.0 / cut * f.kappa));
       a = std::min(a, -w2 * s); b = std::max(b, w2 * s);
     }
   }
@@ -100,7 +102,7 @@ static Support support_of(const Filter& f, int k, int64_t L, std::vector<float>*
   if (len >= L) { lo = 0; len = L; }
   Support sp{lo, len, (int64_t)vals->size(), L};
   for (int64_t t = 0; t < len; ++t)
-    vals->push_back((float)response_level_nu(f, k, (double)(lo + t) / (double)L));
+    vals->push_back((V)response_level_nu(f, k, (double)(lo + t) / (double)L));
   return sp;
 }
 
@@ -478,6 +480,11 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
   // ---- spectra (support-limited; threshold 1e-10 absolute, DESIGN R26)
   std::vector<float>& V = p->spec_vals;
   for (int n1 = 0; n1 < N1; ++n1) p->psi1_sup.push_back(support_of(p->psi1[n1], 0, p->N_pad, &V));
+  // the forward first layer (float64) uses float64 psi1 spectra cut at 1e-17 of the peak: its
+  // rounding floor must sit below the R22 dead zone (1e-12 RMS) so that the phase Z1/|Z1| of every
+  // cell outside the dead zone is computed, not noise (R22)
+  for (int n1 = 0; n1 < N1; ++n1)
+    p->psi1_sup_d.push_back(support_of(p->psi1[n1], 0, p->N_pad, &p->spec_vals_d, 1e-17));
   for (int k = 0; k <= log2T; ++k) p->phiT_sup.push_back(support_of(p->phiT, k, p->N_pad >> k, &V));
   p->psi2_sup.assign(p->blocks.size() * (log2T + 1), Support{0, 0, 0, 0});
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
@@ -486,9 +493,28 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
       p->psi2_sup[bi * (log2T + 1) + k] = support_of(p->psi2[b.n2], k, p->N_pad >> k, &V);
   }
 
+  // colored-noise initialisation tables (reading R25): band energies and the partition denominator
+  {
+    const int64_t half = p->N_pad / 2;
+    std::vector<double> den(half + 1, 0.0);
+    p->cn_nu.assign(N1, 0.0);
+    for (int n1 = 0; n1 < N1; ++n1) {
+      double nu = 0.0;
+      for (int64_t m = 0; m < p->N_pad; ++m) {
+        const double h = response_level_nu(p->psi1[n1], 0, (double)m / (double)p->N_pad);
+        nu += h * h;
+        if (m <= half) den[m] += h * h;
+      }
+      p->cn_nu[n1] = nu / (double)p->N_pad;
+    }
+    double mx = 0.0;
+    for (double v : den) mx = std::max(mx, v);
+    p->cn_den.resize(half + 1);
+    for (int64_t m = 0; m <= half; ++m) p->cn_den[m] = (float)(den[m] + 1e-3 * mx);
+  }
   // gather jobs: layer 1, S0, S1 time part, layer 2
   for (int n1 = 0; n1 < N1; ++n1) {
-    auto& sp = p->psi1_sup[n1];
+    auto& sp = p->psi1_sup_d[n1];
     int k1 = std::min(p->psi1[n1].j, log2T);
     p->l1_jobs.push_back({0, p->N_pad, sp.lo, sp.len, sp.off, p->L1_off[n1], p->L1[n1],
                           (float)std::ldexp(1.0, -k1), 0});

@@ -51,6 +51,7 @@ class DistJTFS:
 
     def __init__(self, plan=None, path_shards: int = 1, group=None,
                  compute: Callable | None = None):
+        self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if self.world % path_shards:
@@ -86,8 +87,16 @@ class DistJTFS:
         return loss, grad
 
     def gather_losses(self, loss: torch.Tensor, B_total: int) -> torch.Tensor:
-        """All per-signal losses (logging only), ordered by signal index."""
-        out = [torch.zeros_like(loss) for _ in range(self.world)]
-        dist.all_gather(out, loss)
-        parts = [out[g * self.path_shards] for g in range(self.n_batch_groups)]
-        return torch.cat(parts)[:B_total]
+        """All per-signal losses (logging only), ordered by signal index. Batch groups may hold
+        unequal signal counts (batch_slice), so every rank pads its losses to ceil(B_total / groups)
+        before the all_gather (which needs equal sizes) over the same group as the constructor."""
+        cap = -(-B_total // self.n_batch_groups)
+        buf = torch.zeros(cap, dtype=loss.dtype, device=loss.device)
+        buf[: loss.numel()] = loss.reshape(-1)
+        out = [torch.zeros_like(buf) for _ in range(self.world)]
+        dist.all_gather(out, buf, group=self.group)
+        parts = []
+        for g in range(self.n_batch_groups):
+            sl = batch_slice(B_total, self.n_batch_groups, g)
+            parts.append(out[g * self.path_shards][: sl.stop - sl.start])
+        return torch.cat(parts)

@@ -155,14 +155,33 @@ class Plan:
                      shrink: float = 0.5, ws: torch.Tensor | None = None, stream=None) -> dict:
         """metamer_step: one bold-driver momentum trial, stream-ordered."""
         B = state["y"].shape[0]
+        act = state.get("active")
         ms = MetamerState(_ptr(state["y"]), _ptr(state["u"]), _ptr(state["y_prev"]), _ptr(state["g_prev"]),
                           _ptr(state["mu"]), _ptr(state["loss_prev"]), _ptr(state["loss"]),
-                          _ptr(state["accepted"]), state["iter"])
+                          _ptr(state["accepted"]), state["iter"], None if act is None else _ptr(act))
         ws = ws if ws is not None else self.workspace(B, True, state["y"].device)
         check(self.lib.metamer_step(self.h, ctypes.byref(ms), _ptr(S_target), B, momentum, grow, shrink,
                                     _ptr(ws), ws.numel(), _stream(stream)))
         state["iter"] = ms.iter
         return state
+
+    def colored_noise(self, S_target: torch.Tensor, seed: int = 0, white: torch.Tensor | None = None,
+                      ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """jtfs_colored_noise: y0 [B, N], colored Gaussian noise whose band energies follow the
+        order-1 profile of S_target (PAPER.md:123, reading R25). `white` [B, N_pad] standard normal;
+        drawn here from a seeded torch generator on the device when not given."""
+        assert S_target.is_cuda and S_target.dtype == torch.float32 and S_target.is_contiguous()
+        B = S_target.shape[0]
+        if white is None:
+            gen = torch.Generator(device=S_target.device).manual_seed(seed)
+            white = torch.randn(B, self.info.N_pad, generator=gen, device=S_target.device, dtype=torch.float32)
+        assert white.is_cuda and white.dtype == torch.float32 and white.is_contiguous()
+        assert white.shape == (B, self.info.N_pad)
+        y0 = torch.empty(B, self.N, device=S_target.device, dtype=torch.float32)
+        ws = ws if ws is not None else self.workspace(B, False, S_target.device)
+        check(self.lib.jtfs_colored_noise(self.h, _ptr(S_target), _ptr(white), B, _ptr(y0), _ptr(ws), ws.numel(),
+                                          _stream(stream)))
+        return y0
 
     def debug_stage(self, stage: int, x: torch.Tensor) -> torch.Tensor:
         B = x.shape[0]

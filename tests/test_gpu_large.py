@@ -1,23 +1,27 @@
 """GPU parity at the BASELINE.json sizes (configs c2..c5), one signal each, in the launch
-configuration bench.py uses. The float64 oracle evaluates a subset of second-order blocks
-(`Oracle.forward(blocks=...)`): the first block (tensor-core path) and/or the last block (CUDA-core
-path), plus S0 and order 1; those coefficients are compared element by element.
+configuration bench.py uses, against the float64 oracle (R22: both sides use the modulus
+dead zone |z| < 1e-12 RMS(y) of SPEC S:372, which changes the float64 gradient by <= 1e-9 at these
+inputs; tests/golden/r22_effect.json).
 
-Gradient: the loss is restricted to the same subset of paths by giving the GPU a target equal
-to its own (bitwise deterministic) S(y) outside the subset, so its residual is exactly zero
-there; the oracle differentiates the subset loss. Bars: rel-L2 1e-4 (S), 1e-3 (dE/dy)."""
+c2 runs whole: every second-order block, the full loss. c3-c5: the first and the last block (the
+oracle evaluates a subset of blocks, `Oracle.forward(blocks=...)`), plus S0 and order 1; the GPU's
+loss is restricted to the same paths by a target equal to its own (bitwise deterministic) S(y)
+outside the subset, so its residual is exactly zero there. Special inputs at c2: y with exactly
+silent stretches (the regime the dead zone exists for), a zero target (S(0) = 0), and y = x
+(nullity). Bars: rel-L2 1e-4 (S, loss), 1e-3 (dE/dy)."""
 import numpy as np
 import pytest
 import torch
 
 from oracle.jtfs import Oracle
+from oracle.plan import make_plan
 from synth import CONFIGS, plan_args, batch
 
 pytestmark = pytest.mark.gpu
 
-# (config, sampled blocks): at c2 block 0 = CT = 2 SS form, 2 = two forward MMA issuers over 4-chunk tiles
-# (one B ring each), 5 = split-K (2 parts, W kept for the backward), 9 = split-K with filter groups
-CASES = [("c2", [0, 9]), ("c2", [2, 5]), ("c3", [10]), ("c4", [11]), ("c5", [11])]
+# (config, blocks or None = all, input variant)
+CASES = [("c2", None, "music"), ("c2", None, "silent"), ("c2", None, "zero_target"),
+         ("c3", [0, 10], "music"), ("c4", [0, 11], "music"), ("c4", [11], "silent"), ("c5", [0, 11], "music")]
 
 
 def rel(a, b):
@@ -29,59 +33,102 @@ def rel(a, b):
 def subset_mask(plan, blocks):
     m = np.zeros(plan.n_coef, bool)
     for q in plan.paths:
-        if q.order == 1 or (q.order == 2 and q.block in blocks) or q.order == 0:
+        if q.order <= 1 or blocks is None or q.block in blocks:
             m[q.offset:q.offset + q.rows * q.frames] = True
     return m
 
 
-@pytest.mark.parametrize("name,blocks", CASES, ids=[f"{c}-b{'-'.join(map(str, b))}" for c, b in CASES])
-def test_large_forward_and_gradient(name, blocks):
+def silent(y):
+    """four exactly silent runs of N/16 samples"""
+    y = y.copy()
+    N = y.shape[1]
+    for k in range(4):
+        y[:, (4 * k + 1) * N // 16:(4 * k + 2) * N // 16] = 0.0
+    return y
+
+
+@pytest.fixture(scope="module")
+def plans():
     from paper_2602_11896_b200 import Plan
-    cfg = CONFIGS[name]
-    args = plan_args(cfg)
-    p = Plan(*args)
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = Plan(*plan_args(CONFIGS[name]))
+        return cache[name]
+    return get
+
+
+@pytest.mark.parametrize("name,blocks,variant", CASES,
+                         ids=[f"{c}-{'all' if b is None else 'b' + '-'.join(map(str, b))}-{v}" for c, b, v in CASES])
+def test_large_forward_and_gradient(plans, name, blocks, variant):
+    args = plan_args(CONFIGS[name])
+    p = plans(name)
     o = Oracle(args)
     x = batch(name, 1)
     y = batch(name, 1, which="y")
-    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
-    # forward: GPU runs everything, the oracle the sampled blocks
-    Sg = p.forward(xd).cpu().numpy()[0]
-    So = o.forward(x, blocks=blocks).numpy()[0]
+    if variant == "silent":
+        y = silent(y)
+    if variant == "zero_target":
+        x = np.zeros_like(x)
     m = subset_mask(o.plan, blocks)
-    assert rel(Sg[m], So[m]) <= 1e-4
-    for q in o.plan.paths:
-        if m[q.offset]:
-            sl = slice(q.offset, q.offset + q.rows * q.frames)
-            assert rel(Sg[sl], So[sl]) <= 2e-3, (name, q)
-    # gradient of the loss restricted to the sampled paths (order 1 + blocks); S0 is never in the loss
-    Sy = p.forward(yd)
-    St = Sy.clone()
-    mt = torch.from_numpy(m).cuda()
-    St[0, mt] = torch.from_numpy(So.astype(np.float32)).cuda()[mt]
+    # forward: GPU runs everything, the oracle the sampled blocks
+    Sg = p.forward(torch.from_numpy(x).cuda()).cpu().numpy()[0]
+    So = o.forward(x, blocks=blocks).numpy()[0]
+    if variant == "zero_target":
+        assert not np.any(Sg) and not np.any(So)          # S(0) = 0 exactly on both sides
+    else:
+        assert rel(Sg[m], So[m]) <= 1e-4
+        for q in o.plan.paths:
+            if m[q.offset]:
+                sl = slice(q.offset, q.offset + q.rows * q.frames)
+                assert rel(Sg[sl], So[sl]) <= 2e-3, (name, q)
+    yd = torch.from_numpy(y).cuda()
+    if blocks is None:
+        St = torch.from_numpy(So[None].astype(np.float32)).cuda()
+        Eo, go = o.loss_grad(y, So[None])
+    else:
+        Sy = p.forward(yd)
+        St = Sy.clone()
+        mt = torch.from_numpy(m).cuda()
+        St[0, mt] = torch.from_numpy(So.astype(np.float32)).cuda()[mt]
+        Eo, go = o.loss_grad_subset(y, So[None], blocks)
     loss, g = p.loss_grad(yd, St)
-    Eo, go = o.loss_grad_subset(y, So[None], blocks)
     assert rel(loss.cpu().numpy(), Eo.numpy()) <= 1e-4
     assert rel(g.cpu().numpy(), go.numpy()) <= 1e-3
 
 
-def test_split_k_shards_and_microbatch():
+def test_nullity_c2(plans):
+    # P:153: the gradient is null when S(y) = S(x); here y = x exactly and the target is the GPU's own
+    # (bitwise deterministic) S(x): every residual is exactly 0, so loss and gradient are exactly 0
+    p = plans("c2")
+    x = torch.from_numpy(batch("c2", 2)).cuda()
+    S = p.forward(x)
+    loss, g = p.loss_grad(x, S)
+    assert float(loss.abs().max()) == 0.0 and float(g.abs().max()) == 0.0
+
+
+def test_split_k_shards_and_microbatch(plans):
     """c2 exercises the split-K tensor-core blocks (W kept by the forward, GEMM2-only backward) and the
     filter-group split with g_Y2 partials: per-signal results are bitwise independent of the micro-batch,
-    and path shards sum to the whole (only fp32 summation order differs)."""
-    from paper_2602_11896_b200 import Plan
-    p = Plan(*plan_args(CONFIGS["c2"]))
+    and path shards sum to the whole. Shard 1 runs first on a workspace filled with NaN bytes (it must
+    not read order-1 buffers only shard 0 writes)."""
+    p = plans("c2")
     x = torch.from_numpy(batch("c2", 2)).cuda()
     y = torch.from_numpy(batch("c2", 2, which="y")).cuda()
     S = p.forward(x)
     for _ in range(3):   # repeated launches are bitwise identical (no races in the pipelined kernels)
         assert torch.equal(p.forward(x), S)
+    ws = torch.full((p.workspace_size(2, True),), 0xFF, dtype=torch.uint8, device="cuda")
+    l1s, g1s = p.loss_grad(y, S, shard=1, n_shards=2, ws=ws)
+    assert bool(torch.isfinite(g1s).all()) and bool(torch.isfinite(l1s).all())
     loss, g = p.loss_grad(y, S)
-    ws = torch.empty(p.workspace_size(1, True), dtype=torch.uint8, device="cuda")
-    l1, g1 = p.loss_grad(y, S, ws=ws)
+    ws1 = torch.empty(p.workspace_size(1, True), dtype=torch.uint8, device="cuda")
+    l1, g1 = p.loss_grad(y, S, ws=ws1)
     assert torch.equal(g1, g) and torch.equal(l1, loss)
-    ls, gs = 0, 0
-    for sh in range(2):
-        l_, g_ = p.loss_grad(y, S, shard=sh, n_shards=2)
-        ls, gs = ls + l_, gs + g_
+    l0s, g0s = p.loss_grad(y, S, shard=0, n_shards=2)
+    gs, ls = g0s + g1s, l0s + l1s
+    # the shards' partial gradients run the same fp32 adjoint chain (FFTs up to 2^17 points) on
+    # different partial sums; their sum differs from the whole-signal gradient by rounding only
     assert rel(gs.cpu().numpy(), g.cpu().numpy()) <= 1e-5
-    assert rel(ls.cpu().numpy(), loss.cpu().numpy()) <= 1e-5
+    assert rel(ls.cpu().numpy(), loss.cpu().numpy()) <= 1e-6
