@@ -92,21 +92,45 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(config: str, seconds_hint: float = 30.0) -> dict:
-    """The float64 oracle (as it stands) on the host cores: fwd+grad of ONE signal of `config`."""
+def _oracle_sample(config: str, o, x, y):
+    """Time the float64 oracle (as it stands) on a BOUNDED sample of one signal's fwd+grad and return
+    (seconds for the whole signal, description). c1/c2: the whole signal is timed. c3-c5 (minutes per
+    signal on the host): two timed pieces -- layer 1 + order 1 (loss restricted to order 1) and the same
+    plus the one second-order block whose column count is nearest 2^14 -- and the whole signal is
+    extrapolated as t0 + (t1 - t0) * sum_b T2_b / T2_sample (the oracle's per-block cost is its joint
+    stage, proportional to the block's time columns: one P-point FFT per column and filter)."""
+    p = o.plan
+    if config in ("c1", "c2"):
+        St = o.forward(x)
+        t0 = time.perf_counter()
+        o.loss_grad(y, St)
+        dt = time.perf_counter() - t0
+        return dt, f"1 signal of {config} (N={p.N}), float64 forward+loss+gradient, {dt:.1f} s measured"
+    T2 = [p.N_pad >> b.s2 for b in p.blocks]
+    bs = min(range(len(T2)), key=lambda i: abs(np.log2(T2[i]) - 14))
+    St = o.forward(x, blocks=[bs])
+    t = time.perf_counter()
+    o.loss_grad_subset(y, St, [])
+    t0 = time.perf_counter() - t
+    t = time.perf_counter()
+    o.loss_grad_subset(y, St, [bs])
+    t1 = time.perf_counter() - t
+    dt = t0 + max(t1 - t0, 0.0) * sum(T2) / T2[bs]
+    return dt, (f"1 signal of {config} (N={p.N}): layer 1 + order 1 measured {t0:.1f} s, + block {bs} "
+                f"({T2[bs]} of {sum(T2)} second-order columns) {t1:.1f} s; whole signal EXTRAPOLATED "
+                f"by column count to {dt:.0f} s")
+
+
+def cpu_baseline(config: str) -> dict:
+    """The float64 oracle (as it stands) on the host cores, one signal of `config` (bounded sample)."""
     import torch
     from oracle.jtfs import Oracle
-    cores = torch.get_num_threads()
     o = Oracle(plan_args(CONFIGS[config]))
     x = batch(config, 1)
     y = batch(config, 1, which="y")
-    St = o.forward(x)                    # target coefficients: not part of the timed step
-    t0 = time.perf_counter()
-    o.loss_grad(y, St)
-    dt = time.perf_counter() - t0
+    dt, what = _oracle_sample(config, o, x, y)
     N = CONFIGS[config]["N"]
-    return {"value": N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"1 signal of {config} (N={N}), float64 forward+loss+gradient, {dt:.1f} s"}
+    return {"value": N / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle", "sample": what}
 
 
 def run_reference(args) -> None:
@@ -119,16 +143,14 @@ def run_reference(args) -> None:
     o = Oracle(plan_args(cfg))
     x = batch(args.config, 1)
     y = batch(args.config, 1, which="y")
-    St = o.forward(x)
-    # one reference step = fwd+grad of ONE signal (~1 min on 16 cores); capped at 2 steps so the
-    # arm ends within a few minutes whatever --steps says (reported as "steps"); no warm-up steps: the
-    # float64 numpy oracle has no JIT or device state to warm (reported as "warmup": 0)
+    # one reference step = the bounded sample of one signal's fwd+grad (_oracle_sample); capped at 2
+    # steps so the arm ends within a few minutes whatever --steps says (reported as "steps"); no warm-up
+    # steps: the float64 oracle has no JIT or device state to warm (reported as "warmup": 0)
     steps = max(1, min(args.steps, 2))
-    times = []
+    times, what = [], ""
     for _ in range(steps):
-        t0 = time.perf_counter()
-        o.loss_grad(y, St)
-        times.append(time.perf_counter() - t0)
+        dt, what = _oracle_sample(args.config, o, x, y)
+        times.append(dt)
     dt = float(np.sum(times))
     value = steps * cfg["N"] / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -136,7 +158,7 @@ def run_reference(args) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {_describe(args.config)}; reference step = 1 signal"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
-                             "sample": f"1 signal of {args.config} per step (float64 oracle, host cores)"},
+                             "sample": what},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -149,8 +171,11 @@ def run_metamer(plan, args, dev) -> dict:
     cfg = CONFIGS[args.config]
     B = args.batch or cfg["B"]
     x = torch.from_numpy(batch(args.config, B)).to(dev)
-    y0 = torch.from_numpy(batch(args.config, B, which="y")).to(dev)
     St = plan.forward(x)
+    if args.metamer_init == "colored":   # PAPER.md:123 (reading R25), jtfs_colored_noise
+        y0 = plan.colored_noise(St, seed=500000 + 1000 * int(args.config[1:]))
+    else:                                # BASELINE configs[2]: Gaussian-noise init at the target's RMS
+        y0 = torch.from_numpy(batch(args.config, B, which="y")).to(dev)
     st = plan.metamer_state(y0)
     ws = plan.workspace(B, True, dev)
     curve = []
@@ -164,7 +189,8 @@ def run_metamer(plan, args, dev) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    return {"steps": args.metamer, "steps_per_s": args.metamer / (ms / 1000.0), "ms_per_step": ms / args.metamer,
+    return {"init": args.metamer_init, "steps": args.metamer, "steps_per_s": args.metamer / (ms / 1000.0),
+            "ms_per_step": ms / args.metamer,
             "batch": B, "loss_curve_mean": curve, "final_over_initial": curve[-1][1] / max(curve[0][1], 1e-30),
             "accepted_last": int(st["accepted"].sum())}
 
@@ -180,14 +206,21 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4", help="BASELINE config (default c4 = configs[3], 'Throughput', "
+                                                   "the largest single-GPU config)")
     ap.add_argument("--batch", type=int, default=None, help="signals per rank (default: config batch)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the config's batch over the batch groups (c5: B = 256 over G)")
+    ap.add_argument("--no-forward", action="store_true", help="skip the forward-only (analysis) measurement")
     ap.add_argument("--metamer", type=int, default=0,
                     help="also run this many metamer_step iterations (BASELINE configs[2]: c3, 100) from white-noise "
                          "init and report steps/s and the loss curve under the 'metamer' key")
+    ap.add_argument("--metamer-init", default="white", choices=["white", "colored"],
+                    help="metamer y0: white Gaussian noise at the target's RMS (BASELINE c3) or the paper's colored "
+                         "noise matched to S1 x (jtfs_colored_noise)")
     ap.add_argument("--path-shards", type=int, default=1,
                     help="ranks per path group (order-2 units split, dE/dx all-reduced over NVLink)")
     args = ap.parse_args()
@@ -212,9 +245,18 @@ def main() -> None:
     ps = max(1, args.path_shards)
     group_id = rank // ps                     # batch group (signals) of this rank
     n_groups = world // ps
-    # per-group batch: independent signals (weak scaling); target S(x) computed once, untimed
-    x = torch.from_numpy(batch(args.config, B, start=group_id * B)).to(dev)
-    y = torch.from_numpy(batch(args.config, B, which="y", start=group_id * B)).to(dev)
+    if args.strong:
+        # strong scaling (BASELINE c5: "batch 256 ... at 1/2/4/8 GPUs"): the config's batch is split
+        # over the batch groups (contiguous, balanced), the total work is fixed
+        from paper_2602_11896_b200.dist import batch_slice
+        sl = batch_slice(B, n_groups, group_id)
+        start, B_total, B = sl.start, B, sl.stop - sl.start
+    else:
+        # weak scaling: every batch group processes its own batch of the config (independent signals)
+        start, B_total = group_id * B, n_groups * B
+    # target S(x) computed once, untimed
+    x = torch.from_numpy(batch(args.config, B, start=start)).to(dev)
+    y = torch.from_numpy(batch(args.config, B, which="y", start=start)).to(dev)
     St = plan.forward(x)
     ws = plan.workspace(B, True, dev)
     loss = torch.empty(B, device=dev)
@@ -228,7 +270,7 @@ def main() -> None:
 
     def step():
         if ps > 1:
-            dj.loss_grad(y, St)
+            dj.loss_grad(y, St, chunk=mb)   # all_reduce of micro-batch i overlaps micro-batch i+1
         else:
             plan.loss_grad(y, St, loss=loss, grad=grad, ws=ws)
 
@@ -261,12 +303,32 @@ def main() -> None:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = n_groups * B * cfg["N"] * args.steps / (ms / 1000.0)
+    value = B_total * cfg["N"] * args.steps / (ms / 1000.0)
+
+    # forward-only analysis throughput (NEXT-2): jtfs_forward over the same batch
+    fo_ms = None
+    if not args.no_forward:
+        Sf = torch.empty_like(St)
+        for _ in range(2):
+            plan.forward(y, out=Sf, ws=ws)
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        f0.record(stream)
+        for _ in range(args.steps):
+            plan.forward(y, out=Sf, ws=ws)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fo_ms = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([fo_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fo_ms = float(t.item())
 
     # end-to-end through the host-buffer C-ABI call (pinned host memory, copies inside)
     e2e = None
     if not args.no_e2e and ps == 1:
-        yh = torch.from_numpy(batch(args.config, B, which="y", start=rank * B)).pin_memory()
+        yh = torch.from_numpy(batch(args.config, B, which="y", start=start)).pin_memory()
         Sth = St.cpu().pin_memory()
         wsh = plan.workspace_host(B, dev)
         for _ in range(2):
@@ -287,7 +349,7 @@ def main() -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             hms = float(t.item())
         del wsh
-        e2e = {"value": n_groups * B * cfg["N"] * args.steps / (hms / 1000.0), "unit": UNIT,
+        e2e = {"value": B_total * cfg["N"] * args.steps / (hms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(B * cfg["N"] * 4 + B * plan.n_coef * 4),
                "d2h_bytes_per_step": int(B * 4 + B * cfg["N"] * 4)}
 
@@ -342,18 +404,63 @@ def main() -> None:
                                "counts 3 MMAs; FFT route against FP32 = 148 SM x 128 lanes x 2 x %.0f MHz, "
                                "folded into TF32-equivalent time" % (float(pk.get("bf16_tflops", 1590.0)), clock_mhz)),
                  "joint_kernels": kern})
+    # clock-true TF32 rate: a kind::tf32 M128 N128 K8 MMA takes N/2 = 64 cycles per SM (DESIGN.md §6,
+    # tools/ubench/tmem_mma.cu) -> 4096 flop/cycle/SM at the SM clock measured during the timed region
+    f_run = clk.get("sm_mhz") or clock_mhz
+    tf32_clock_true = 4096.0 * N_SM * f_run * 1e6 / 1e12
+    if dom:
+        roof["tf32_clock_true_tflops"] = tf32_clock_true
+        roof["frac_vs_tf32_clock_true"] = roof["achieved"] / tf32_clock_true
+    # Whole-path roofline: sum over the stages of max(bytes/BW, flops/peak) over the step.
+    # Joint stages: their ideal (tensor-bound) time; everything else: algorithmic HBM bytes (SURVEY App. B,
+    # fused design: x, X_hat r/w, U1_hat w + 2 r, Y2 w + r fwd, Y2 r + g_Y2 w/r bwd, g_hat_U1, g_hat_x, g)
+    # at the measured copy bandwidth.
+    hbm_peak = float(pk.get("hbm_gbs", 6545.3))
+    sL1, sY2 = plan._sumL1(), plan._sumY2()
+    Np = plan.info.N_pad
+    alg_bytes_sig = 8 * cfg["N"] + 16 * Np + 40 * sL1 + 40 * sY2
+    joint_bytes_sig = cost["joint_hbm_bytes"]
+    other_bytes = B * max(alg_bytes_sig - joint_bytes_sig, 0.0)
+    step_ms = ms / args.steps
+    ideal_joint_ms = sum(kern[k]["ideal_ms_per_step"] for k in kern)
+    ideal_other_ms = 1000.0 * other_bytes / (hbm_peak * 1e9)
+    path = {"ideal_ms_per_step": ideal_joint_ms + ideal_other_ms, "ms_per_step": step_ms,
+            "frac": (ideal_joint_ms + ideal_other_ms) / step_ms, "ideal_joint_ms": ideal_joint_ms,
+            "ideal_hbm_ms": ideal_other_ms,
+            "joint_ms_measured": sum(kern[k]["ms_per_step"] for k in kern),
+            "rest_ms_measured": step_ms - sum(kern[k]["ms_per_step"] for k in kern)}
+    # achieved HBM GB/s vs peak (BASELINE metric): algorithmic bytes of the whole path per step over the
+    # step time, and the DRAM bytes ncu measured for one step of the same command when committed
+    # (profiles/dram_step_<config>.json, tools/ncu_dram.py)
+    hbm = {"algorithmic_bytes_per_step": B * alg_bytes_sig, "achieved_gbs": B * alg_bytes_sig / (step_ms * 1e6),
+           "peak_gbs": hbm_peak, "frac": B * alg_bytes_sig / (step_ms * 1e6) / hbm_peak,
+           "bytes_per_sample": alg_bytes_sig / cfg["N"]}
+    dpath = os.path.join(ROOT, "profiles", f"dram_step_{args.config}.json")
+    if os.path.exists(dpath):
+        try:
+            dj = json.load(open(dpath))
+            hbm["dram_bytes_per_step_ncu"] = dj["dram_bytes_per_step"] * B / dj.get("batch", B)
+            hbm["dram_gbs_ncu_over_step"] = hbm["dram_bytes_per_step_ncu"] / (step_ms * 1e6)
+            hbm["dram_source"] = os.path.relpath(dpath, ROOT)
+        except Exception:
+            pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {_describe(args.config)} per rank",
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {_describe(args.config)}" + (" split over ranks" if args.strong
+                                                                             else " per batch group"),
                    "l2": "per-step working set > 126 MB L2 (no flush needed)",
                    "micro_batch": int(mb), "parallelism": f"batch{n_groups}xpath{ps}"},
-        "roofline": roof,
+        "roofline": roof, "path_roofline": path, "hbm": hbm,
         "clocks": clk, "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
     }
     if e2e:
         line["e2e"] = e2e
+    if fo_ms is not None:
+        line["forward_only"] = {"value": B_total * cfg["N"] * args.steps / (fo_ms / 1000.0), "unit": UNIT,
+                                "ms_per_step": fo_ms / args.steps,
+                                "what": "jtfs_forward over the same batch (analysis workload, NEXT-2)"}
     if args.metamer > 0:
         line["metamer"] = run_metamer(plan, args, dev)
     if world == 1 and not args.no_cpu_baseline:

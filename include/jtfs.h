@@ -106,9 +106,10 @@ jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* S, 
  *   Modulus adjoint (R22): the phase z/|z| is 0 where |z| < 1e-12 * RMS(y_b), at
  *   every modulus site; elsewhere it is the exact phase (PyTorch autograd's).
  * y [B][N], S_target [B][n_coef], loss [B], grad [B][N]: device fp32.
- * shard/n_shards: second-order path shard (0,1 = whole). With n_shards > 1 the call computes the
- * contribution of order-2 units with (unit index mod n_shards) == shard, plus (shard 0 only)
- * order 1; summing loss and grad over shards (e.g. NCCL allreduce) gives the full result. */
+ * shard/n_shards: second-order path shard (0,1 = whole; n_shards <= 64). With n_shards > 1 the call
+ * computes the contribution of the second-order blocks jtfs_plan_shards assigns to `shard` (layer 2,
+ * joint stage and their adjoints for those blocks only), plus (shard 0 only) order 1; layer 1 runs on
+ * every shard. Summing loss and grad over shards (e.g. NCCL allreduce) gives the full result. */
 jtfs_status jtfs_loss_grad(jtfs_plan_t plan, const float* y, const float* S_target, int64_t B,
                            float* loss, float* grad, int shard, int n_shards, void* ws,
                            size_t ws_bytes, jtfs_stream_t stream);
@@ -132,6 +133,24 @@ typedef struct {
 jtfs_status metamer_step(jtfs_plan_t plan, jtfs_metamer_state* st, const float* S_target,
                          int64_t B, float momentum, float grow, float shrink, void* ws,
                          size_t ws_bytes, jtfs_stream_t stream);
+
+/* Non-finite check ("non-finite direction -> numeric error"): returns JTFS_ERR_NUMERIC if any
+ * of x[0..n) (device fp32) is NaN or +-inf, JTFS_OK otherwise. Synchronises `stream` (the only call
+ * besides the host-buffer variants that does); used by the metamer loop on y and the loss each step. */
+jtfs_status jtfs_check_finite(const float* x, int64_t n, jtfs_stream_t stream);
+
+/* Path-shard assignment: block_owner_out[bi] = shard of second-order block bi for
+ * n_shards shards (1..64): LPT over the planner's per-block cost (joint-stage contraction flops + the
+ * block's time-axis FFTs), largest block first to the least-loaded shard, ties to the lower index;
+ * shard 0 starts loaded with order 1. Deterministic; host only. cap >= n_blocks. */
+jtfs_status jtfs_plan_shards(jtfs_plan_t plan, int n_shards, int32_t* block_owner_out, int64_t cap);
+
+/* Per-path LossReport (R19): per_path[b][q] = 1/2 sum over the coefficients of path q
+ * (jtfs_plan_paths order, R15) of (S - S_target)^2, float64 accumulation. Path 0 (S0) is reported but is
+ * not part of the loss E_b = sum over the order-1 and order-2 entries. S, S_target [B][n_coef],
+ * per_path [B][n_paths]: device fp32. Stream-ordered; no workspace. */
+jtfs_status jtfs_loss_report(jtfs_plan_t plan, const float* S, const float* S_target, int64_t B,
+                             float* per_path, jtfs_stream_t stream);
 
 /* Colored Gaussian noise initialisation of the metamer loop (§2.3: "a colored Gaussian noise
  * y0(t) whose power spectral density matches S1 x(t, lambda)"; reading R25 in DESIGN.md):

@@ -31,4 +31,10 @@ struct Rows {
   int64_t stride_b, off, count, L;
 };
 
+// Path-shard ownership of one jtfs_loss_grad call (include/jtfs.h): bit bi = second-order block bi
+// (blocks go to shards by the planner's LPT rule, Plan::block_owner), bit 63 = order 1 (shard 0).
+constexpr uint64_t kOwnOrder1 = 1ull << 63;
+constexpr uint64_t kOwnAll = ~0ull;
+__host__ __device__ __forceinline__ bool owns_block(uint64_t own, int bi) { return (own >> bi) & 1ull; }
+
 }  // namespace jtfs

@@ -63,6 +63,7 @@ struct DeviceTables {
   int maxLf = 0, max_rows_out = 0;
   int64_t* bwd_tiles = nullptr;     int64_t bwd_ntiles = 0;        // prefix over blocks of (col tiles x n ranges)
   int32_t* coef_path = nullptr;     // [n_coef]
+  int64_t* path_off = nullptr;      // [n_paths + 1] coefficient offsets (LossReport)
   int32_t* path_owner_unit = nullptr;  // [n_paths]: -2 order 0, -1 order 1, else unit index
   int64_t* l1_off = nullptr;        int32_t* n1_k1 = nullptr;      // per n1 offsets, k1
   int64_t* u1adj_tiles = nullptr;   int64_t u1adj_ntiles = 0;      // prefix over n1 of L1 tiles
@@ -98,7 +99,8 @@ constexpr int kJN = 64;            // joint backward: n1 rows per CTA
 // ---- kernels_time.cu
 void launch_reflect_pad(const float* x, int64_t sx, double2* xp, const Plan& p, int B, cudaStream_t st);
 void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
-                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
+                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st,
+                   uint64_t own = kOwnAll);
 void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
                       const int64_t* tiles, int njobs, int64_t ntiles, const double* vals, int B, cudaStream_t st);
 void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
@@ -113,7 +115,7 @@ void launch_s0_out(const float2* s0c, int64_t s0_sb, float* S, int64_t S_sb, con
                    cudaStream_t st);
 void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS, int64_t GS_sb,
                           const float2* GY, int64_t GY_sb, float2* out, int64_t out_sb, int B,
-                          cudaStream_t st);
+                          cudaStream_t st, uint64_t own = kOwnAll);
 void launch_phase_mul(const float2* z, const float2* gu, int64_t gsb, float2* out, int64_t n_per_b, int64_t sb,
                       const float* thr, int B, cudaStream_t st);
 // reading R22: the modulus adjoint uses phase 0 where |z| < kEpsMod * RMS(y_b)
@@ -133,6 +135,7 @@ void launch_cn_shape(const Plan& p, const DeviceTables& d, float2* X, int64_t X_
                      int B, cudaStream_t st);
 void launch_cn_crop(const Plan& p, const float2* X, int64_t X_sb, const float* white, const float* g, int64_t g_sb,
                     float* y0, int B, cudaStream_t st);
+void launch_check_finite(const float* x, int64_t n, int32_t* flag, cudaStream_t st);
 void launch_metamer(float* y, float* u, float* y_prev, float* g_prev, float* mu, float* loss_prev,
                     const float* loss, int32_t* accepted, const int32_t* active, const float* g, int64_t sg,
                     int64_t N, int B, float momentum, float grow, float shrink, cudaStream_t st);
@@ -144,30 +147,33 @@ void launch_o1_bwd(const Plan& p, const DeviceTables& d, const float* r, int64_t
                    int64_t W1_sb, float* V2, int64_t V2_sb, const float* S1t, int64_t S1t_sb, float* gS1t,
                    int64_t gS1t_sb, const float* thr, int B, cudaStream_t st);
 void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                      int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st);
+                      int64_t o_sb, uint64_t own, int B, cudaStream_t st);
 void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,
-                     int64_t S_sb, int shard, int n_shards, int B, cudaStream_t st);
+                     int64_t S_sb, uint64_t own, int B, cudaStream_t st);
+// per-path LossReport: rep[b][q] = 1/2 sum over path q's coefficients of (S - St)^2
+void launch_loss_report(const Plan& p, const DeviceTables& d, const float* S, const float* St, float* rep, int B,
+                        cudaStream_t st);
 void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S_sb, const float* St,
-                 int64_t St_sb, float* r, int64_t r_sb, float* loss, double* part, int shard, int n_shards, int B,
+                 int64_t St_sb, float* r, int64_t r_sb, float* loss, double* part, uint64_t own, int B,
                  cudaStream_t st);
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
-                     int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st);
+                     int64_t go_sb, uint64_t own, int B, cudaStream_t st);
 // the per-block launches go round-robin over the ns streams ss (forked from and joined to the caller's)
 // split-K blocks accumulate W in wbuf (per-signal stride wb_sb) and leave it there when keep_w (backward)
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, int shard, int n_shards, int B,
+                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, uint64_t own, int B,
                          const cudaStream_t* ss, int ns);
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
-                         float2* gp, int64_t gp_sb, const float* thr, int shard, int n_shards, int B,
+                         float2* gp, int64_t gp_sb, const float* thr, uint64_t own, int B,
                          const cudaStream_t* ss, int ns);
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                      int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
+                      int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, uint64_t own, int B,
                       cudaStream_t st);
 
 // ---- kernels_frfft.cu
 void launch_joint_fft(const Plan& p, const DeviceTables& d, bool bwd, const float2* Y2, int64_t y_sb, float* o,
-                      int64_t o_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
+                      int64_t o_sb, float2* gY, int64_t gy_sb, const float* thr, uint64_t own, int B,
                       cudaStream_t st);
 int64_t joint_fft_tiles(int64_t n_cols);
 constexpr int kFfMaxP = 1024;      // FFT route: C x P <= 4096 points per CTA

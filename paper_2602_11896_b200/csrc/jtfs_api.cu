@@ -150,7 +150,7 @@ static void free_tables(DeviceTables* d) {
   void* ptrs[] = {d->spec_vals, d->spec_vals_d, d->cn_nu, d->cn_den, d->l1_jobs, d->l1_tiles, d->s1_jobs, d->s1_tiles, d->l2_jobs, d->l2_tiles,
                   d->s0_job, d->s0_tiles, d->psi1_sup, d->psi2_sup, d->phiT_sup, d->hfr, d->phiF_k,
                   d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
-                  d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_owner_unit, d->l1_off,
+                  d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_off, d->path_owner_unit, d->l1_off,
                   d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw, d->twd,
                   d->fr_spec, d->u_wts, d->u_wt_off, d->hfr_H, d->phT_rows_u, d->phT_tiles, d->ffw.blist, d->ffw.tiles, d->ffb.blist, d->ffb.tiles};
   for (void* q : ptrs)
@@ -310,9 +310,15 @@ static cudaError_t upload(Plan& p) {
   for (size_t q = 0; q < p.paths.size(); ++q) {
     auto& pa = p.paths[q];
     for (int64_t i = 0; i < (int64_t)pa.rows * pa.frames; ++i) cp[pa.offset + i] = (int32_t)q;
-    pu[q] = pa.order == 0 ? -2 : (pa.order == 1 ? -1 : (int32_t)(q - 1 - nfr1));
+    pu[q] = pa.order == 0 ? -2 : (pa.order == 1 ? -1 : (int32_t)((q - 1 - nfr1) / p.L_fr.size()));   // block
   }
   UP(cp, coef_path); UP(pu, path_owner_unit);
+  {
+    std::vector<int64_t> po;
+    for (auto& pa : p.paths) po.push_back(pa.offset);
+    po.push_back(p.n_coef);
+    UP(po, path_off);
+  }
   UP(p.L1_off, l1_off);
   std::vector<int32_t> k1;
   std::vector<int64_t> ut;
@@ -466,9 +472,17 @@ static cudaError_t fft_rows(const Plan& p, const float2* in, int64_t in_sb, floa
   return fft_launch(in, out, ri, ro, B, inv, p.dev->fftt, st);
 }
 
+// Y2 row groups (one per second-order block) of the blocks a path shard owns
+static std::vector<FftGroup> own_groups(const Plan& p, uint64_t own) {
+  std::vector<FftGroup> g;
+  for (size_t bi = 0; bi < p.y2_groups.size(); ++bi)
+    if (owns_block(own, (int)bi)) g.push_back(p.y2_groups[bi]);
+  return g;
+}
+
 // Forward of one micro-batch. stop: 0 = full; 1 = after U1 (in A); 2 = after S1t; 3 = after Y2.
 static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb, float* S, int64_t S_sb,
-                               const Bufs& w, int shard, int n_shards, cudaStream_t st, int stop = 0,
+                               const Bufs& w, uint64_t own, cudaStream_t st, int stop = 0,
                                bool keep_w = false, int lane = 0) {
   const DeviceTables& d = *p.dev;
   cudaError_t e;
@@ -504,12 +518,14 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   RET();
   if (stop == 2) return cudaSuccess;
   // A3: order-1 frequential scattering (shard 0 only)
-  if (shard == 0) launch_o1_fwd(p, d, w.S1t, w.s_S1t, w.W1, w.s_W1, w.V2, w.s_V2, S, S_sb, mb, st);
+  if (own & kOwnOrder1) launch_o1_fwd(p, d, w.S1t, w.s_S1t, w.W1, w.s_W1, w.V2, w.s_V2, S, S_sb, mb, st);
   // A4: layer 2, width-first
   if (!p.blocks.empty()) {
-    launch_gather(w.U1h, w.s_L1, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st);
-    if ((e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, p.y2_groups.data(), (int)p.y2_groups.size(), mb, true, d.fftt,
-                        st)))
+    // path shards compute only their own blocks' Y2 (layer 1 is the only replicated stage)
+    launch_gather(w.U1h, w.s_L1, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st, own);
+    const std::vector<FftGroup> g2 = own_groups(p, own);
+    if (!g2.empty() &&
+        (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, true, d.fftt, st)))
       return e;
     RET();
     if (stop == 3) return cudaSuccess;
@@ -517,46 +533,45 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     prof_begin(st, 0 + 4 * lane);
     Fanout* fo = fanout_get(lane);
     fan_fork(fo, st);
-    launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, shard, n_shards, mb, fo->s[0]);
-    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.Wk, w.s_Wk, keep_w, shard, n_shards, mb, fo->s + 1,
+    launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, own, mb, fo->s[0]);
+    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.Wk, w.s_Wk, keep_w, own, mb, fo->s + 1,
                         kFanStreams - 1);
-    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, shard, n_shards, mb, fo->s[0]);
+    launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, own, mb, fo->s[0]);
     fan_join(fo, st);
     prof_end(st, 0 + 4 * lane);
-    launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, shard, n_shards, mb, st);
+    launch_phiT_fwd(p, d, w.o, w.s_o, S, S_sb, own, mb, st);
   }
   RET();
   return cudaSuccess;
 }
 
 // Backward of one micro-batch (after run_forward + loss): r in w.r -> grad [mb][N] (stride sg)
-static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64_t sg, int mb, int shard,
-                                int n_shards, cudaStream_t st, int lane = 0) {
+static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64_t sg, int mb, uint64_t own, cudaStream_t st, int lane = 0) {
   const DeviceTables& d = *p.dev;
   cudaError_t e;
   const int64_t N1 = (int64_t)p.psi1.size();
   if (!p.blocks.empty()) {
     // A7: phi_T adjoint (r -> g_o, reusing o), joint adjoint (-> g_Y2 in A)
-    launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, shard, n_shards, mb, st);
+    launch_phiT_adj(p, d, w.r, w.s_S, w.o, w.s_o, own, mb, st);
     if ((e = cudaMemsetAsync(w.A, 0, (size_t)w.s_A * 8 * mb, st))) return e;
     prof_begin(st, 2 + 4 * lane);
     Fanout* fo = fanout_get(lane);
     fan_fork(fo, st);
-    launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
-    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.Wk, w.s_Wk, w.gp, w.s_gp, w.thr, shard,
-                        n_shards, mb, fo->s + 1,
+    launch_joint_fft(p, d, true, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, own, mb, fo->s[0]);
+    launch_joint_bwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.Wk, w.s_Wk, w.gp, w.s_gp, w.thr, own, mb, fo->s + 1,
                         kFanStreams - 1);
-    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, shard, n_shards, mb, fo->s[0]);
+    launch_joint_bwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.A, w.s_A, w.thr, own, mb, fo->s[0]);
     fan_join(fo, st);
     prof_end(st, 2 + 4 * lane);
-    // FFT of g_Y2 rows -> G_Y (into Y2)
-    if ((e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, p.y2_groups.data(), (int)p.y2_groups.size(), mb, false, d.fftt,
-                        st)))
+    // FFT of g_Y2 rows -> G_Y (into Y2), own blocks only
+    const std::vector<FftGroup> g2 = own_groups(p, own);
+    if (!g2.empty() &&
+        (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, false, d.fftt, st)))
       return e;
   }
   // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)
   // order 1 belongs to shard 0 (its forward W1/V2 exist only there): other shards contribute g_S1t = 0
-  if (shard == 0) {
+  if (own & kOwnOrder1) {
     launch_o1_bwd(p, d, w.r, w.s_S, w.W1, w.s_W1, w.V2, w.s_V2, w.S1t, w.s_S1t, w.gS1t, w.s_S1t, w.thr, mb, st);
   } else if ((e = cudaMemsetAsync(w.gS1t, 0, (size_t)w.s_S1t * 4 * mb, st))) {
     return e;
@@ -564,7 +579,7 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
   launch_real_to_complex(w.gS1t, w.s_S1t, w.cs, w.s_c, N1 * p.Ft, mb, st);
   if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, N1, p.Ft, mb, false, st))) return e;
   // A8: g_hat_U1 -> U1h ; g_U1 = Re IFFT -> A
-  launch_adj_gather_u1(p, d, w.ct, w.s_c, w.Y2, w.s_Y2, w.U1h, w.s_L1, mb, st);
+  launch_adj_gather_u1(p, d, w.ct, w.s_c, w.Y2, w.s_Y2, w.U1h, w.s_L1, mb, st, own);
   if ((e = fft_groups(w.U1h, w.A, w.s_L1, w.s_A, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt,
                       st)))
     return e;
@@ -759,6 +774,36 @@ size_t jtfs_workspace_size(jtfs_plan_t plan, int64_t batch, int with_grad) {
   return layout(plan->p, with_grad).per_signal() * (size_t)batch;
 }
 
+// Path shards: whole second-order blocks go to shards by LPT over Plan::block_cost
+// (largest first to the least-loaded shard, ties to the lower index; shard 0 starts with the order-1
+// work), so a shard computes layer 2 / its adjoint only for its own blocks and layer 1 is the only
+// replicated stage. Deterministic: every rank derives every rank's blocks.
+constexpr int kMaxShards = 64;
+static std::vector<int> block_owner(const Plan& p, int n_shards) {
+  const int nb = (int)p.blocks.size();
+  std::vector<int> owner(nb, 0), order(nb);
+  for (int i = 0; i < nb; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return p.block_cost[a] > p.block_cost[b]; });
+  std::vector<double> load(n_shards, 0.0);
+  load[0] = p.order1_cost;
+  for (int bi : order) {
+    int s = 0;
+    for (int k = 1; k < n_shards; ++k)
+      if (load[k] < load[s]) s = k;
+    owner[bi] = s;
+    load[s] += p.block_cost[bi];
+  }
+  return owner;
+}
+static uint64_t shard_mask(const Plan& p, int shard, int n_shards) {
+  if (n_shards <= 1) return kOwnAll;
+  const std::vector<int> owner = block_owner(p, n_shards);
+  uint64_t m = shard == 0 ? kOwnOrder1 : 0;
+  for (size_t bi = 0; bi < owner.size(); ++bi)
+    if (owner[bi] == shard) m |= 1ull << bi;
+  return m;
+}
+
 static jtfs_status check_common(jtfs_plan_t plan, int64_t B, size_t ws_bytes, int with_grad, void* ws, int* mb) {
   if (!plan) return fail(JTFS_ERR_STATE, "NULL plan");
   if (B <= 0) return fail(JTFS_ERR_SIZE, "B must be > 0");
@@ -784,7 +829,7 @@ jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* S, 
   Bufs w = carve(p, L, (char*)ws, mb);
   for (int64_t b0 = 0; b0 < B; b0 += mb) {
     int n = (int)std::min<int64_t>(mb, B - b0);
-    CK(run_forward(p, x + b0 * p.N, p.N, n, S + b0 * p.n_coef, p.n_coef, w, 0, 1, (cudaStream_t)stream));
+    CK(run_forward(p, x + b0 * p.N, p.N, n, S + b0 * p.n_coef, p.n_coef, w, kOwnAll, (cudaStream_t)stream));
   }
   t_err.clear();
   return JTFS_OK;
@@ -796,8 +841,10 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
   int mb;
   jtfs_status s = check_common(plan, B, ws_bytes, 1, ws, &mb);
   if (s) return s;
-  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(JTFS_ERR_SIZE, "need 0 <= shard < n_shards");
+  if (n_shards < 1 || n_shards > kMaxShards || shard < 0 || shard >= n_shards)
+    return fail(JTFS_ERR_SIZE, "need 0 <= shard < n_shards <= 64");
   const Plan& p = plan->p;
+  const uint64_t own = shard_mask(p, shard, n_shards);
   Layout L = layout(p, 1);
   // Optional two lanes (JTFS_LANES=2): each lane runs its own micro-batches on its own stream (forked from
   // and joined to `st`), so one lane's tensor-core joint stage can overlap the other's HBM-bound FFT /
@@ -814,14 +861,13 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
     Bufs w = carve(p, L, (char*)ws + (size_t)l * mbl * L.per_signal(), mbl);
     for (int64_t b0 = (int64_t)l * mbl; b0 < B; b0 += (int64_t)lanes * mbl) {
     int n = (int)std::min<int64_t>(mbl, B - b0);
-    CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, shard, n_shards, ls, 0, true, l));
+    CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, own, ls, 0, true, l));
     float* lossp = mstate ? mstate->loss + b0 : loss + b0;
-    launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, (double*)w.loss, shard,
-                n_shards, n, ls);
+    launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, (double*)w.loss, own, n, ls);
     launch_mod_threshold(y + b0 * p.N, p.N, kEpsMod, w.thr, n, ls);
     float* gp = mstate ? w.g : grad + b0 * p.N;
     int64_t sg = mstate ? w.s_g : p.N;
-    CK(run_backward(p, w, gp, sg, n, shard, n_shards, ls, l));
+    CK(run_backward(p, w, gp, sg, n, own, ls, l));
     if (mstate) {
       launch_metamer(mstate->y + b0 * p.N, mstate->u + b0 * p.N, mstate->y_prev + b0 * p.N,
                      mstate->g_prev + b0 * p.N, mstate->mu + b0, mstate->loss_prev + b0, lossp,
@@ -891,6 +937,48 @@ jtfs_status jtfs_loss_grad_host(jtfs_plan_t plan, const float* y_host, const flo
   return JTFS_OK;
 }
 
+jtfs_status jtfs_check_finite(const float* x, int64_t n, jtfs_stream_t stream) {
+  if (n < 0 || (n > 0 && !x)) return fail(JTFS_ERR_SIZE, "NULL array or n < 0");
+  if (n == 0) return JTFS_OK;
+  static thread_local std::vector<int32_t*> flags;   // one device flag per device and host thread
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if ((int)flags.size() <= dev) flags.resize(dev + 1, nullptr);
+  if (!flags[dev]) CK(cudaMalloc(&flags[dev], sizeof(int32_t)));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(flags[dev], 0, sizeof(int32_t), st));
+  launch_check_finite(x, n, flags[dev], st);
+  int32_t h = 0;
+  CK(cudaMemcpyAsync(&h, flags[dev], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h) return fail(JTFS_ERR_NUMERIC, "non-finite value (NaN or inf)");
+  t_err.clear();
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan_shards(jtfs_plan_t plan, int n_shards, int32_t* block_owner_out, int64_t cap) {
+  if (!plan || !block_owner_out) return fail(JTFS_ERR_SIZE, "NULL argument");
+  if (n_shards < 1 || n_shards > kMaxShards) return fail(JTFS_ERR_SIZE, "need 1 <= n_shards <= 64");
+  const Plan& p = plan->p;
+  if (cap < (int64_t)p.blocks.size()) return fail(JTFS_ERR_SIZE, "cap < n_blocks");
+  const std::vector<int> owner = block_owner(p, n_shards);
+  for (size_t i = 0; i < owner.size(); ++i) block_owner_out[i] = owner[i];
+  t_err.clear();
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_loss_report(jtfs_plan_t plan, const float* S, const float* S_target, int64_t B, float* per_path,
+                             jtfs_stream_t stream) {
+  if (!plan) return fail(JTFS_ERR_STATE, "NULL plan");
+  if (B <= 0 || !S || !S_target || !per_path) return fail(JTFS_ERR_SIZE, "B <= 0 or NULL argument");
+  jtfs_status s = ensure_device(plan);
+  if (s) return s;
+  launch_loss_report(plan->p, *plan->p.dev, S, S_target, per_path, (int)B, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  t_err.clear();
+  return JTFS_OK;
+}
+
 jtfs_status jtfs_colored_noise(jtfs_plan_t plan, const float* S_target, const float* white, int64_t B, float* y0,
                                void* ws, size_t ws_bytes, jtfs_stream_t stream) {
   int mb;
@@ -930,20 +1018,20 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
   const int n = (int)B;
   if (stage == 1) {
     if (out_bytes < (size_t)B * p.sumL1 * 4) return fail(JTFS_ERR_SIZE, "out too small");
-    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 1));
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, kOwnAll, st, 1));
     launch_real_rows_d(reinterpret_cast<const double2*>(w.A), w.s_A / 2, (float*)out, p.sumL1, p.sumL1, n, st);
   } else if (stage == 2) {
     int64_t per = (int64_t)p.psi1.size() * p.Ft;
     if (out_bytes < (size_t)B * per * 4) return fail(JTFS_ERR_SIZE, "out too small");
-    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 2));
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, kOwnAll, st, 2));
     CK(cudaMemcpy2DAsync(out, per * 4, w.S1t, w.s_S1t * 4, per * 4, B, cudaMemcpyDeviceToDevice, st));
   } else if (stage == 3) {
     if (out_bytes < (size_t)B * p.sumY2 * 8) return fail(JTFS_ERR_SIZE, "out too small");
-    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 3));
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, kOwnAll, st, 3));
     if (p.sumY2 > 0)
       CK(cudaMemcpy2DAsync(out, p.sumY2 * 8, w.Y2, w.s_Y2 * 8, p.sumY2 * 8, B, cudaMemcpyDeviceToDevice, st));
   } else if (stage == 5 || stage == 6) {
-    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, 0, 1, st, 1));
+    CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, kOwnAll, st, 1));
     if (stage == 5) {   // X_hat, complex128 [B][N_pad]
       if (out_bytes < (size_t)B * p.N_pad * 16) return fail(JTFS_ERR_SIZE, "out too small");
       CK(cudaMemcpy2DAsync(out, p.N_pad * 16, w.Xh, w.s_xp * 8, p.N_pad * 16, B, cudaMemcpyDeviceToDevice, st));
@@ -953,7 +1041,7 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
     }
   } else if (stage == 4) {
     if (out_bytes < (size_t)B * p.n_coef * 4) return fail(JTFS_ERR_SIZE, "out too small");
-    CK(run_forward(p, x, p.N, n, (float*)out, p.n_coef, w, 0, 1, st, 0));
+    CK(run_forward(p, x, p.N, n, (float*)out, p.n_coef, w, kOwnAll, st, 0));
   } else {
     return fail(JTFS_ERR_SIZE, "stage must be 1..6");
   }

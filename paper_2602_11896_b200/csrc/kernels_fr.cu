@@ -248,10 +248,10 @@ __global__ void __launch_bounds__(256) k_joint_fwd(
     const float2* __restrict__ Y2, int64_t y_sb, float* __restrict__ o, int64_t o_sb,
     const JointUnit* __restrict__ units, const int32_t* __restrict__ ulist, const int64_t* __restrict__ tiles,
     int nlist, const BlockInfo* __restrict__ binfo, const float2* __restrict__ hfr, int P,
-    const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off, int shard, int n_shards) {
+    const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off, uint64_t own) {
   extern __shared__ float4 smem4[];
   const int li = find_idx(tiles, nlist, blockIdx.x);
-  if (ulist[li] % n_shards != shard) return;
+  if (!owns_block(own, units[ulist[li]].bi)) return;
   const JointUnit U = units[ulist[li]];
   const BlockInfo bf = binfo[U.bi];
   const int64_t ct = blockIdx.x - tiles[li];
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd(
     float2* __restrict__ gY2, int64_t gy_sb, const JointUnit* __restrict__ units, int nfr,
     const int64_t* __restrict__ tiles, int n_blocks, const BlockInfo* __restrict__ binfo,
     const float2* __restrict__ hfr, int P, const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off,
-    int shard, int n_shards, int maxLf, const float* __restrict__ thr) {
+    uint64_t own, int maxLf, const float* __restrict__ thr) {
   extern __shared__ float4 smem4[];
   const int bi = find_idx(tiles, n_blocks, blockIdx.x);
   const BlockInfo bf = binfo[bi];
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd(
   const float th2 = thr[b] * thr[b];
   for (int f = 0; f < nfr; ++f) {
     const int uidx = bi * nfr + f;
-    if (uidx % n_shards != shard) continue;
+    if (!owns_block(own, bi)) continue;
     const JointUnit U = units[uidx];
     const int Lf = (int)U.Lf;
     __syncthreads();  // previous users of hs/gs/Go are done
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd2(
     float2* __restrict__ gY2, int64_t gy_sb, const JointUnit* __restrict__ units, int nfr,
     const int64_t* __restrict__ tiles, int n_blocks, const BlockInfo* __restrict__ binfo,
     const float2* __restrict__ hfr, int P, const float* __restrict__ phiF_k, const int64_t* __restrict__ phiF_off,
-    int shard, int n_shards, int maxLf, const float* __restrict__ thr) {
+    uint64_t own, int maxLf, const float* __restrict__ thr) {
   extern __shared__ float4 smem4[];
   const int bi = find_idx(tiles, n_blocks, blockIdx.x);
   const BlockInfo bf = binfo[bi];
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(256) k_joint_bwd2(
   const int ntile2 = NG * 16;
   for (int f = 0; f < nfr; ++f) {
     const int uidx = bi * nfr + f;
-    if (uidx % n_shards != shard) continue;
+    if (!owns_block(own, bi)) continue;
     const JointUnit U = units[uidx];
     const int Lf = (int)U.Lf;
     __syncthreads();
@@ -661,13 +661,13 @@ __global__ void k_phiT_fwd(const float* __restrict__ o, int64_t o_sb, float* __r
                            const JointUnit* __restrict__ units, const int64_t* __restrict__ ucoef, int n_units,
                            const BlockInfo* __restrict__ binfo, const float* __restrict__ phiT_half,
                            const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H,
-                           int64_t o2_start, int64_t n_o2, int64_t frames, int64_t m0, int shard, int n_shards) {
+                           int64_t o2_start, int64_t n_o2, int64_t frames, int64_t m0, uint64_t own) {
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.y;
   if (q >= n_o2) return;
   const int u = find_idx(ucoef, n_units, q);
-  if (u % n_shards != shard) return;
+  if (!owns_block(own, units[u].bi)) return;
   const JointUnit U = units[u];
   const BlockInfo bf = binfo[U.bi];
   const int64_t loc = q - ucoef[u];
@@ -702,12 +702,12 @@ __global__ void k_phiT_adj(const float* __restrict__ rres, int64_t r_sb, float* 
                            const BlockInfo* __restrict__ binfo, const float* __restrict__ phiT_half,
                            const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H,
                            const int64_t* __restrict__ ucoef, int64_t o2_start, int64_t o_size, int64_t frames,
-                           int64_t m0, int shard, int n_shards) {
+                           int64_t m0, uint64_t own) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (q >= o_size) return;
   const int u = find_idx(uo, n_units, q);
-  if (u % n_shards != shard) return;
+  if (!owns_block(own, units[u].bi)) return;
   const JointUnit U = units[u];
   const BlockInfo bf = binfo[U.bi];
   const int64_t loc = q - U.o_off;
@@ -745,14 +745,14 @@ __global__ void __launch_bounds__(256) k_phiT_adj2(
     const float* __restrict__ rres, int64_t r_sb, float* __restrict__ go, int64_t go_sb,
     const JointUnit* __restrict__ units, const BlockInfo* __restrict__ binfo, const float* __restrict__ phiT_half,
     const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H, const int64_t* __restrict__ ucoef,
-    const int32_t* __restrict__ tinfo, int64_t o2_start, int frames, int64_t m0, int shard, int n_shards) {
+    const int32_t* __restrict__ tinfo, int64_t o2_start, int frames, int64_t m0, uint64_t own) {
   struct { int u, rho; int64_t c0; } R;
   R.u = __ldg(tinfo + 3 * blockIdx.x);
   R.rho = __ldg(tinfo + 3 * blockIdx.x + 1);
   R.c0 = __ldg(tinfo + 3 * blockIdx.x + 2);
   __shared__ float rr[256];
   const int b = blockIdx.y;
-  if (R.u % n_shards != shard) return;
+  if (!owns_block(own, units[R.u].bi)) return;
   const JointUnit U = units[R.u];
   const BlockInfo bf = binfo[U.bi];
   const float* rsrc = rres + b * r_sb + o2_start + ucoef[R.u] + (int64_t)R.rho * frames;
@@ -794,10 +794,10 @@ __global__ void __launch_bounds__(256) k_phiT_fwd2(
     const float* __restrict__ o, int64_t o_sb, float* __restrict__ S, int64_t S_sb,
     const JointUnit* __restrict__ units, const int64_t* __restrict__ ucoef, const BlockInfo* __restrict__ binfo,
     const float* __restrict__ phiT_half, const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H,
-    const int32_t* __restrict__ rows_u, int64_t o2_start, int frames, int64_t m0, int shard, int n_shards) {
+    const int32_t* __restrict__ rows_u, int64_t o2_start, int frames, int64_t m0, uint64_t own) {
   extern __shared__ float tsm[];
   const int u = rows_u[2 * blockIdx.x], rho = rows_u[2 * blockIdx.x + 1];
-  if (u % n_shards != shard) return;
+  if (!owns_block(own, units[u].bi)) return;
   const int b = blockIdx.y;
   const JointUnit U = units[u];
   const BlockInfo bf = binfo[U.bi];
@@ -836,11 +836,38 @@ __global__ void __launch_bounds__(256) k_phiT_fwd2(
 // for a deterministic sum spread over the SMs: kLossParts CTAs per signal write float64 partials (fixed
 // coefficient ranges), one warp per signal adds them in a fixed order.
 constexpr int kLossParts = 32;
+// LossReport: one CTA per (path, signal), float64 partial sums in a fixed tree order (deterministic)
+__global__ void __launch_bounds__(256) k_loss_report(const float* __restrict__ S, const float* __restrict__ St,
+                                                     int64_t n_coef, const int64_t* __restrict__ path_off,
+                                                     float* __restrict__ rep, int n_paths) {
+  __shared__ double red[256];
+  const int q = blockIdx.x, b = blockIdx.y;
+  const int64_t a = path_off[q], e = path_off[q + 1];
+  double acc = 0.0;
+  for (int64_t i = a + threadIdx.x; i < e; i += 256) {
+    const double r = (double)S[b * n_coef + i] - (double)St[b * n_coef + i];
+    acc += r * r;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) rep[(int64_t)b * n_paths + q] = (float)(0.5 * red[0]);
+}
+
+void launch_loss_report(const Plan& p, const DeviceTables& d, const float* S, const float* St, float* rep, int B,
+                        cudaStream_t st) {
+  dim3 g((unsigned)p.paths.size(), (unsigned)B);
+  k_loss_report<<<g, 256, 0, st>>>(S, St, p.n_coef, d.path_off, rep, (int)p.paths.size());
+  count_launch();
+}
+
 __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ S, int64_t S_sb, const float* __restrict__ St,
                                               int64_t St_sb, float* __restrict__ r, int64_t r_sb,
                                               double* __restrict__ part_out, const int32_t* __restrict__ coef_path,
-                                              const int32_t* __restrict__ path_unit, int64_t n_coef, int shard,
-                                              int n_shards) {
+                                              const int32_t* __restrict__ path_unit, int64_t n_coef, uint64_t own) {
   const int b = blockIdx.y;
   const int64_t per = (n_coef + kLossParts - 1) / kLossParts;
   const int64_t lo = blockIdx.x * per, hi = lo + per < n_coef ? lo + per : n_coef;
@@ -848,8 +875,8 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ S, int64
   double acc = 0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += 256) {
     int pu = path_unit[coef_path[i]];
-    bool own = (pu == -1) ? (shard == 0) : (pu >= 0 && pu % n_shards == shard);
-    float d = own ? S[b * S_sb + i] - St[b * St_sb + i] : 0.f;
+    const bool mine = (pu == -1) ? (own & kOwnOrder1) != 0 : (pu >= 0 && owns_block(own, pu));
+    float d = mine ? S[b * S_sb + i] - St[b * St_sb + i] : 0.f;
     r[b * r_sb + i] = d;
     acc += (double)d * (double)d;
   }
@@ -921,28 +948,28 @@ static size_t joint_fwd_smem(const Plan& p, const DeviceTables& d, int ci, int k
 
 template <int KAP>
 static void launch_joint_fwd_kap(const Plan& p, const DeviceTables& d, int ci, const float2* Y2, int64_t y_sb,
-                                 float* o, int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st) {
+                                 float* o, int64_t o_sb, uint64_t own, int B, cudaStream_t st) {
   if (d.fwd_n[ci] == 0) return;
   size_t sm = joint_fwd_smem(p, d, ci, KAP);
   cudaFuncSetAttribute(k_joint_fwd<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)d.fwd_ntiles[ci], (unsigned)B);
   k_joint_fwd<KAP><<<g, 256, sm, st>>>(Y2, y_sb, o, o_sb, d.units, d.fwd_ulist[ci], d.fwd_tiles[ci], d.fwd_n[ci],
-                                       d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, shard, n_shards);
+                                       d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, own);
   count_launch();
 }
 
 void launch_joint_fwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                      int64_t o_sb, int shard, int n_shards, int B, cudaStream_t st) {
-  launch_joint_fwd_kap<1>(p, d, 0, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
-  launch_joint_fwd_kap<2>(p, d, 1, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
-  launch_joint_fwd_kap<4>(p, d, 2, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
-  launch_joint_fwd_kap<8>(p, d, 3, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
-  launch_joint_fwd_kap<16>(p, d, 4, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
-  launch_joint_fwd_kap<32>(p, d, 5, Y2, y_sb, o, o_sb, shard, n_shards, B, st);
+                      int64_t o_sb, uint64_t own, int B, cudaStream_t st) {
+  launch_joint_fwd_kap<1>(p, d, 0, Y2, y_sb, o, o_sb, own, B, st);
+  launch_joint_fwd_kap<2>(p, d, 1, Y2, y_sb, o, o_sb, own, B, st);
+  launch_joint_fwd_kap<4>(p, d, 2, Y2, y_sb, o, o_sb, own, B, st);
+  launch_joint_fwd_kap<8>(p, d, 3, Y2, y_sb, o, o_sb, own, B, st);
+  launch_joint_fwd_kap<16>(p, d, 4, Y2, y_sb, o, o_sb, own, B, st);
+  launch_joint_fwd_kap<32>(p, d, 5, Y2, y_sb, o, o_sb, own, B, st);
 }
 
 void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64_t o_sb, float* S,
-                     int64_t S_sb, int shard, int n_shards, int B, cudaStream_t st) {
+                     int64_t S_sb, uint64_t own, int B, cudaStream_t st) {
   if (d.n_o2 == 0 || d.phT_nrows == 0) return;
   static bool attr = false;
   if (!attr) {
@@ -952,31 +979,31 @@ void launch_phiT_fwd(const Plan& p, const DeviceTables& d, const float* o, int64
   dim3 g((unsigned)d.phT_nrows, (unsigned)B);
   k_phiT_fwd2<<<g, 256, kPhiTSmem * 4, st>>>(o, o_sb, S, S_sb, d.units, d.ucoef, d.binfo, d.phiT_half, d.phiT_off,
                                              d.phiT_H, d.phT_rows_u, d.o2_start, (int)p.frames, p.pad_left / p.T,
-                                             shard, n_shards);
+                                             own);
   count_launch();
 }
 
 void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S_sb, const float* St,
-                 int64_t St_sb, float* r, int64_t r_sb, float* loss, double* part, int shard, int n_shards, int B,
+                 int64_t St_sb, float* r, int64_t r_sb, float* loss, double* part, uint64_t own, int B,
                  cudaStream_t st) {
   k_loss<<<dim3(kLossParts, B), 256, 0, st>>>(S, S_sb, St, St_sb, r, r_sb, part, d.coef_path, d.path_owner_unit,
-                                              p.n_coef, shard, n_shards);
+                                              p.n_coef, own);
   k_loss_final<<<(B + 127) / 128, 128, 0, st>>>(part, loss, B);
   count_launch(2);
 }
 
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
-                     int64_t go_sb, int shard, int n_shards, int B, cudaStream_t st) {
+                     int64_t go_sb, uint64_t own, int B, cudaStream_t st) {
   if (p.o_size == 0 || d.phT_ntiles == 0) return;
   dim3 g((unsigned)d.phT_ntiles, (unsigned)B);
   k_phiT_adj2<<<g, 256, 0, st>>>(r, r_sb, go, go_sb, d.units, d.binfo, d.phiT_half, d.phiT_off, d.phiT_H, d.ucoef,
                                  d.phT_tiles, d.o2_start, (int)p.frames,
-                                 p.pad_left / p.T, shard, n_shards);
+                                 p.pad_left / p.T, own);
   count_launch();
 }
 
 void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
-                      int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
+                      int64_t go_sb, float2* gY2, int64_t gy_sb, const float* thr, uint64_t own, int B,
                       cudaStream_t st) {
   if (d.n_blocks == 0 || d.bwd_ntiles == 0) return;
   const size_t sm = (size_t)2 * d.Kmax_simt_bwd * kB2C * 8 + (size_t)p.P * 8 + (size_t)kJR * kB2C * 8 +
@@ -984,7 +1011,7 @@ void launch_joint_bwd(const Plan& p, const DeviceTables& d, const float2* Y2, in
   cudaFuncSetAttribute(k_joint_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)d.bwd_ntiles, (unsigned)B);
   k_joint_bwd2<<<g, 256, sm, st>>>(Y2, y_sb, go, go_sb, gY2, gy_sb, d.units, (int)p.L_fr.size(), d.bwd_tiles,
-                                   d.n_blocks, d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, shard, n_shards,
+                                   d.n_blocks, d.binfo, d.hfr, (int)p.P, d.phiF_k, d.phiF_off, own,
                                    d.maxLf, thr);
   count_launch();
 }

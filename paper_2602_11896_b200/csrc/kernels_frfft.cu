@@ -39,7 +39,8 @@ struct FfArgs {
   const float* wts; const int64_t* wt_off;  // per unit [rows_out][n_rows]
   const float2* tw;
   const float* thr;
-  int nfr, P, lgP, shard, n_shards;
+  int nfr, P, lgP;
+  uint64_t own;
 };
 
 __device__ __forceinline__ int ff_find(const int64_t* __restrict__ tiles, int n, int64_t t) {
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kFfThreads, MINB) k_joint_fwd_fft(FfArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int f = 0; f < a.nfr; ++f) {
     const int u = bi * a.nfr + f;
-    if (u % a.n_shards != a.shard) continue;
+    if (!owns_block(a.own, bi)) continue;
     const JointUnit U = a.units[u];
     const int Lf = (int)U.Lf, nr = (int)U.n_rows, ro = U.rows_out;
     ff_fold<C>(Wk, Yh, a.spec + (int64_t)f * P, P, U.kf);
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kFfThreads, MINB) k_joint_bwd_fft(FfArgs a) {
   const float th2 = a.thr[b] * a.thr[b];
   for (int f = 0; f < a.nfr; ++f) {
     const int u = bi * a.nfr + f;
-    if (u % a.n_shards != a.shard) continue;
+    if (!owns_block(a.own, bi)) continue;
     const JointUnit U = a.units[u];
     const int Lf = (int)U.Lf, nr = (int)U.n_rows, rlo = (int)U.r_lo, ro = U.rows_out;
     // g_o of this unit for the CTA's columns, packed per rho
@@ -283,12 +284,12 @@ static size_t ff_smem(int P, bool bwd) {
 }
 
 void launch_joint_fft(const Plan& p, const DeviceTables& d, bool bwd, const float2* Y2, int64_t y_sb, float* o,
-                      int64_t o_sb, float2* gY, int64_t gy_sb, const float* thr, int shard, int n_shards, int B,
+                      int64_t o_sb, float2* gY, int64_t gy_sb, const float* thr, uint64_t own, int B,
                       cudaStream_t st) {
   const FfList& L = bwd ? d.ffb : d.ffw;
   if (L.nb == 0 || L.ntiles == 0) return;
   FfArgs a{Y2, y_sb, o, o_sb, gY, gy_sb, d.units, d.binfo, L.blist, L.tiles, L.nb, d.fr_spec, d.u_wts,
-           d.u_wt_off, d.tw, thr, (int)p.L_fr.size(), (int)p.P, ilog2i(p.P), shard, n_shards};
+           d.u_wt_off, d.tw, thr, (int)p.L_fr.size(), (int)p.P, ilog2i(p.P), own};
   const size_t sm = ff_smem((int)p.P, bwd);
   dim3 g((unsigned)L.ntiles, (unsigned)B);
   // forward: 80-register variant with 3 CTAs per SM (measured faster than 128 registers at 2 per SM);

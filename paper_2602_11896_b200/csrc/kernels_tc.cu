@@ -80,7 +80,8 @@ struct TcArgs {
   const float* img;                 // forward B images
   const float* wts;                 // phi_F weights [unit][rho][NT*64]
   const TcUnit* tcu;                // per unit image / weight offsets
-  int nfr, shard, n_shards;
+  int nfr;
+  uint64_t own;
   float* wbuf; int64_t wb_sb;       // split-K blocks: per-signal W buffer
   int part, pmode;                  // K part of this launch; kPm* bits
   int ng;                           // filter groups: CTA x handles column tile x % ntiles, filters f = x / ntiles mod ng
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     uint32_t ph_r[2] = {0, 0};
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
+      if (!owns_block(a.own, TB.bi) || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       for (int t = 0; t < tu.NT; ++t) {
         // row tile t of the unit's image: chunks of the full K2, starting at this launch's k' range
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     uint32_t ph = 0, bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
+      if (!owns_block(a.own, TB.bi) || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       for (int t = 0; t < tu.NT; ++t) {
         if (gt % nis != q) {   // the other issuer's tile (other ring)
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     uint32_t bph = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
+      if (!owns_block(a.own, TB.bi) || f % a.ng != grp) continue;
       const JointUnit U = a.units[u];
       const TcUnit tu = a.tcu[u];
       const int ro = U.rows_out;
@@ -441,12 +442,12 @@ static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st)
 }
 
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, int shard, int n_shards, int B,
+                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, uint64_t own, int B,
                          const cudaStream_t* ss, int ns) {
   int li = 0;
   for (const TcClass& C : d.tc) {
     const cudaStream_t st = ss[li++ % ns];
-    if (C.n_blocks == 0) continue;
+    if (C.n_blocks == 0 || !owns_block(own, C.bi)) continue;   // path shards: own blocks only
     const int nparts = C.ks ? C.nparts : 1;
     for (int part = 0; part < nparts; ++part) {   // split-K parts run in order on one stream
       int pmode = kPmFinish;
@@ -455,7 +456,7 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
                 (part == nparts - 1 ? kPmFinish : 0);
       }
       TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
-               (int)p.L_fr.size(), shard, n_shards, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr};
+               (int)p.L_fr.size(), own, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr};
 #ifdef JTFS_TC_TRACE
       static long long* ftrace = nullptr;
       if (!ftrace) cudaMalloc(&ftrace, 16 * 512 * 8);
@@ -498,7 +499,8 @@ struct TcBwArgs {
   const float* img1b;               // backward GEMM1 images [unit][tile32][chunk][hi|lo][64 x kc]
   const float* wts;
   const TcUnit* tcu;
-  int nfr, shard, n_shards;
+  int nfr;
+  uint64_t own;
   const float* thr;
   int expt;                         // timing experiments only (JTFS_TC_EXPT); 0 in production
   const float* wbuf; int64_t wb_sb; // split-K blocks: W left by the forward (GEMM1 skipped)
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     uint32_t ph = 0;
     for (int f = 0; f < (p1 && ksm ? 0 : a.nfr); ++f) {   // no GEMM1 (ring 1) in split-K mode
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
+      if (!owns_block(a.own, TB.bi) || f % a.ng != grp) continue;
       const TcUnit tu = a.tcu[u];
       const int NT32 = (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
       for (int t32 = 0; t32 < NT32; ++t32) {
@@ -731,7 +733,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     int G = 0;
     for (int f = 0; f < a.nfr; ++f) {
       const int u = TB.bi * a.nfr + f;
-      if (u % a.n_shards != a.shard || f % a.ng != grp) continue;
+      if (!owns_block(a.own, TB.bi) || f % a.ng != grp) continue;
       G += (int)((a.units[u].n_rows + kBwRows - 1) / kBwRows);
     }
     if (warp == 1) {
@@ -756,7 +758,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     // phi_F weights and g_o are prefetched one tile ahead (their L2 latency would otherwise sit on the
     // epilogue's critical path every tile)
     auto next_unit = [&](int f) {
-      while (f < a.nfr && ((TB.bi * a.nfr + f) % a.n_shards != a.shard || f % a.ng != grp)) ++f;
+      while (f < a.nfr && (!owns_block(a.own, TB.bi) || f % a.ng != grp)) ++f;
       return f;
     };
     // phi_F weights of this warp's 8 rows of tile t (row block of output r at + r * ldw): read as two
@@ -979,14 +981,14 @@ __global__ void k_gy_reduce(const float2* __restrict__ gp, int64_t gp_sb, int64_
 
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
-                         float2* gp, int64_t gp_sb, const float* thr, int shard, int n_shards, int B,
+                         float2* gp, int64_t gp_sb, const float* thr, uint64_t own, int B,
                          const cudaStream_t* ss, int ns) {
   int li = 0;
   for (const TcClass& C : d.tcb) {
     const cudaStream_t st = ss[li++ % ns];
-    if (C.n_blocks == 0) continue;
+    if (C.n_blocks == 0 || !owns_block(own, C.bi)) continue;   // path shards: own blocks only
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
-               d.tc_img2, d.tc_img1b, d.tc_wts, d.tc_units, (int)p.L_fr.size(), shard, n_shards, thr, g_tc_expt, wbuf, wb_sb,
+               d.tc_img2, d.tc_img1b, d.tc_wts, d.tc_units, (int)p.L_fr.size(), own, thr, g_tc_expt, wbuf, wb_sb,
                tc_groups(C, B), gp, gp_sb, nullptr};
 #ifdef JTFS_TC_TRACE
     static long long* trace = nullptr;

@@ -4,6 +4,8 @@
 // All HBM-bound; coalesced along the contiguous time / frequency axis.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "device.cuh"
 
 namespace jtfs {
@@ -51,12 +53,13 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
                                                             TO* __restrict__ out, int64_t out_sb,
                                                             const GatherJob* __restrict__ jobs,
                                                             const int64_t* __restrict__ tiles, int njobs,
-                                                            const VT* __restrict__ vals) {
+                                                            const VT* __restrict__ vals, uint64_t own) {
   using R = typename GAcc<TI>::R;
   const int64_t tile = blockIdx.x;
   const int b = blockIdx.y;
   const int j = find_job(tiles, njobs, tile);
   const GatherJob J = jobs[j];
+  if (J.blk >= 0 && !owns_block(own, J.blk)) return;   // layer-2 block of another path shard
   const TI* src = in + b * in_sb + J.in_off;
   const int64_t m0 = (tile - tiles[j]) * kGatherTile;
   for (int64_t m = m0 + threadIdx.x; m < J.L_out && m < m0 + kGatherTile; m += kGatherThreads) {
@@ -75,15 +78,17 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
 
 template <class TI, class TO, class VT>
 static void gather_t(const TI* in, int64_t in_sb, TO* out, int64_t out_sb, const GatherJob* jobs,
-                     const int64_t* tiles, int njobs, int64_t ntiles, const VT* vals, int B, cudaStream_t st) {
+                     const int64_t* tiles, int njobs, int64_t ntiles, const VT* vals, int B, cudaStream_t st,
+                     uint64_t own = kOwnAll) {
   if (njobs <= 0 || ntiles <= 0) return;
   dim3 g((unsigned)ntiles, (unsigned)B);
-  k_gather<TI, TO, VT><<<g, kGatherThreads, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals);
+  k_gather<TI, TO, VT><<<g, kGatherThreads, 0, st>>>(in, in_sb, out, out_sb, jobs, tiles, njobs, vals, own);
   count_launch();
 }
 void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
-                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
-  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
+                   const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st,
+                   uint64_t own) {
+  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st, own);
 }
 void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
                       const int64_t* tiles, int njobs, int64_t ntiles, const double* vals, int B, cudaStream_t st) {
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
     float2* __restrict__ out, int64_t out_sb, const int64_t* __restrict__ tiles, int N1,
     const int64_t* __restrict__ l1_off, const int32_t* __restrict__ n1_k1, const Support* __restrict__ phiT_sup,
     const Support* __restrict__ psi2_sup, const BlockInfo* __restrict__ binfo, const int32_t* __restrict__ nmax,
-    int n_blocks, int log2T, int64_t N_pad, int64_t Ft, const float* __restrict__ vals) {
+    int n_blocks, int log2T, int64_t N_pad, int64_t Ft, const float* __restrict__ vals, uint64_t own) {
   const int64_t tile = blockIdx.x;
   const int b = blockIdx.y;
   const int n1 = find_job(tiles, N1, tile);
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
   if (threadIdx.x == 0) {
     int nb = 0;
     for (int bi = 0; bi < n_blocks && nb < kMaxB; ++bi) {
-      if (n1 >= nmax[bi]) continue;
+      if (n1 >= nmax[bi] || !owns_block(own, bi)) continue;   // path shards: own blocks only
       const Support sp = psi2_sup[bi * (log2T + 1) + k1];
       const BlockInfo bf = binfo[bi];
       s_lo[nb] = sp.lo; s_len[nb] = sp.len; s_off[nb] = sp.off;
@@ -219,11 +224,11 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
 
 void launch_adj_gather_u1(const Plan& p, const DeviceTables& d, const float2* GS, int64_t GS_sb,
                           const float2* GY, int64_t GY_sb, float2* out, int64_t out_sb, int B,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint64_t own) {
   dim3 g((unsigned)d.u1adj_ntiles, (unsigned)B);
   k_adj_gather_u1<<<g, 256, 0, st>>>(GS, GS_sb, GY, GY_sb, out, out_sb, d.u1adj_tiles, (int)p.psi1.size(),
                                      d.l1_off, d.n1_k1, d.phiT_sup, d.psi2_sup, d.binfo, d.blk_nmax,
-                                     d.n_blocks, p.log2T, p.N_pad, p.Ft, d.spec_vals);
+                                     d.n_blocks, p.log2T, p.N_pad, p.Ft, d.spec_vals, own);
   count_launch();
 }
 
@@ -440,6 +445,20 @@ void launch_cn_crop(const Plan& p, const float2* X, int64_t X_sb, const float* w
                     float* y0, int B, cudaStream_t st) {
   dim3 gr((unsigned)((p.N + 255) / 256), (unsigned)B);
   k_cn_crop<<<gr, 256, 0, st>>>(X, X_sb, white, g, g_sb, y0, p.N, p.N_pad, p.pad_left, (int)p.psi1.size());
+  count_launch();
+}
+
+// non-finite check (JTFS_ERR_NUMERIC): flag = 1 if any x[i] is NaN or +-inf
+__global__ void k_check_finite(const float* __restrict__ x, int64_t n, int32_t* __restrict__ flag) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+void launch_check_finite(const float* x, int64_t n, int32_t* flag, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_check_finite<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(x, n, flag);
   count_launch();
 }
 

@@ -31,7 +31,7 @@ struct Support {
 struct GatherJob {
   int64_t in_off, L_in, lo, len, val_off, out_off, L_out;
   float scale;
-  int32_t pad;
+  int32_t blk;   // second-order block of a layer-2 job (path shards skip unowned blocks), -1 otherwise
 };
 
 // Batched FFT group: `count` rows of length L starting at `off` (per signal).
@@ -151,6 +151,8 @@ struct Plan {
   std::vector<TcBlock> tc_blocks;               // tensor-core eligible blocks
   std::vector<char> blk_tc;                     // [n_blocks] 1 = forward on the tensor-core path
   std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
+  std::vector<double> block_cost;               // [n_blocks] path-shard LPT cost (planner.cpp)
+  double order1_cost = 0.0;
   std::vector<char> blk_ks;                     // [n_blocks] 1 = split-K tensor-core block
   std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class)
   int64_t ks_w_floats = 0;                      // per-signal W buffer of the split-K blocks

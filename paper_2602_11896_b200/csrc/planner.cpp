@@ -517,17 +517,17 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     auto& sp = p->psi1_sup_d[n1];
     int k1 = std::min(p->psi1[n1].j, log2T);
     p->l1_jobs.push_back({0, p->N_pad, sp.lo, sp.len, sp.off, p->L1_off[n1], p->L1[n1],
-                          (float)std::ldexp(1.0, -k1), 0});
+                          (float)std::ldexp(1.0, -k1), -1});
   }
   {
     auto& sp = p->phiT_sup[0];
-    p->s0_job = {0, p->N_pad, sp.lo, sp.len, sp.off, 0, p->Ft, (float)std::ldexp(1.0, -log2T), 0};
+    p->s0_job = {0, p->N_pad, sp.lo, sp.len, sp.off, 0, p->Ft, (float)std::ldexp(1.0, -log2T), -1};
   }
   for (int n1 = 0; n1 < N1; ++n1) {
     int k1 = std::min(p->psi1[n1].j, log2T);
     auto& sp = p->phiT_sup[k1];
     p->s1_jobs.push_back({p->L1_off[n1], p->L1[n1], sp.lo, sp.len, sp.off, (int64_t)n1 * p->Ft, p->Ft,
-                          (float)std::ldexp(1.0, -(log2T - k1)), 0});
+                          (float)std::ldexp(1.0, -(log2T - k1)), -1});
   }
   int64_t yoff = 0;
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
@@ -538,7 +538,7 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
       int k1 = std::min(p->psi1[n1].j, log2T);
       auto& sp = p->psi2_sup[bi * (log2T + 1) + k1];
       p->l2_jobs.push_back({p->L1_off[n1], p->L1[n1], sp.lo, sp.len, sp.off, yoff + n1 * bf.T2, bf.T2,
-                            (float)std::ldexp(1.0, -(b.s2 - k1)), 0});
+                            (float)std::ldexp(1.0, -(b.s2 - k1)), (int32_t)bi});
     }
     p->y2_groups.push_back({yoff, b.n1_max, bf.T2});
     yoff += (int64_t)b.n1_max * bf.T2;
@@ -637,6 +637,17 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     }
   }
   p->o_size = ooff;
+  // path-shard cost model (LPT, jtfs_api.cu block_owner): per block, the joint stage's contraction flops
+  // (8 K forward + 16 K backward per modulus cell) plus its time-axis FFTs (5 L log2 L forward and
+  // backward per Y2 row); order 1 (shard 0) as its row sums over the needed frames
+  p->block_cost.assign(p->blocks.size(), 0.0);
+  for (auto& u : p->units)
+    p->block_cost[u.bi] += 24.0 * u.n1_max * (double)u.n_rows * (double)p->binfo[u.bi].n_cols;
+  for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
+    const double T2 = (double)p->binfo[bi].T2;
+    p->block_cost[bi] += 10.0 * p->blocks[bi].n1_max * T2 * std::log2(T2);
+  }
+  p->order1_cost = 8.0 * N1 * (double)p->Ft * (double)nfr1 * 64.0;
   // order-1 needed rows
   p->o1_rows_out = rows1;
   for (int f = 0; f < nfr1; ++f) {

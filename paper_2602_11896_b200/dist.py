@@ -3,11 +3,12 @@
 Two ways to split the work of jtfs_loss_grad:
   * batch sharding — signals are independent (R27): each rank owns B/G signals, no data-path
     collective (weak scaling). Only per-signal losses may be gathered for logging.
-  * path sharding — the order-2 units (block n2 x frequential filter) of ONE signal are split
-    across the ranks of a path group: unit u goes to shard u mod n_shards, order 1 to shard 0
-    (the rule implemented by jtfs_loss_grad, include/jtfs.h). Every rank recomputes layer 1.
-    The partial dE/dx and losses sum exactly, so the only exchange is ONE all_reduce(SUM) of
-    [grad | loss] per micro-batch over NVLink.
+  * path sharding — the second-order blocks (n2) of ONE signal are split across the ranks of a
+    path group by the planner's LPT rule over per-block cost (jtfs_plan_shards, include/jtfs.h);
+    order 1 goes to shard 0. A rank computes layer 2, the joint stage and their adjoints only for
+    its own blocks; layer 1 (forward and adjoint) is the only replicated stage. The partial dE/dx
+    and losses sum exactly, so the only exchange is ONE all_reduce(SUM) of [grad | loss] per
+    micro-batch over NVLink.
 Ranks are laid out as (batch_group, path_shard) with path_shard = rank % path_shards.
 """
 from __future__ import annotations
@@ -25,22 +26,17 @@ def batch_slice(B_total: int, world: int, rank: int) -> slice:
     return slice(start, start + base + (1 if rank < rem else 0))
 
 
-def unit_shard(unit: int, n_shards: int) -> int:
-    """Owner shard of order-2 unit `unit` (paths in yield order after S0 and order 1)."""
-    return unit % n_shards
-
-
-def path_owner(paths: list[dict], n_shards: int) -> list[int]:
-    """Owner shard of every path: -1 for S0 (not in the loss), 0 for order 1, u mod n for order 2."""
-    out, u = [], 0
+def path_owner(paths: list[dict], block_owner: list[int]) -> list[int]:
+    """Owner shard of every path (R15 order): -1 for S0 (not in the loss), 0 for order 1, and the
+    owner of its block for order 2 (`block_owner` from Plan.block_owner / jtfs_plan_shards)."""
+    out = []
     for q in paths:
         if q["order"] == 0:
             out.append(-1)
         elif q["order"] == 1:
             out.append(0)
         else:
-            out.append(unit_shard(u, n_shards))
-            u += 1
+            out.append(block_owner[q["block"]])
     return out
 
 
@@ -75,16 +71,32 @@ class DistJTFS:
     def my_signals(self, B_total: int) -> slice:
         return batch_slice(B_total, self.n_batch_groups, self.batch_group)
 
-    def loss_grad(self, y: torch.Tensor, S_target: torch.Tensor):
-        """(loss, grad) of this rank's signals, complete (summed over the path group)."""
-        loss, grad = self.compute(y, S_target, self.shard, self.path_shards)
-        if self.path_shards > 1:
-            B = grad.shape[0]
+    def loss_grad(self, y: torch.Tensor, S_target: torch.Tensor, chunk: int | None = None):
+        """(loss, grad) of this rank's signals, complete (summed over the path group).
+
+        With path shards the batch runs in chunks of `chunk` signals (default: all at once); the
+        all_reduce of chunk i is issued asynchronously (NCCL's own stream, ordered after chunk i's
+        kernels) while chunk i+1 computes, so the exchange overlaps the next chunk's work."""
+        if self.path_shards == 1:
+            return self.compute(y, S_target, self.shard, self.path_shards)
+        B = y.shape[0]
+        chunk = B if not chunk else max(1, min(chunk, B))
+        losses, grads, works, bufs = [], [], [], []
+        for c0 in range(0, B, chunk):
+            sl = slice(c0, min(B, c0 + chunk))
+            loss, grad = self.compute(y[sl], S_target[sl], self.shard, self.path_shards)
             buf = torch.cat([grad.reshape(-1), loss.reshape(-1).to(grad.dtype)])
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.path_group)
-            grad = buf[: grad.numel()].view_as(grad)
-            loss = buf[grad.numel():].view(B).to(loss.dtype)
-        return loss, grad
+            works.append(dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.path_group, async_op=True))
+            bufs.append((buf, grad.shape, loss.dtype))
+        for w in works:
+            w.wait()
+        for buf, gshape, ldt in bufs:
+            n = 1
+            for d in gshape:
+                n *= d
+            grads.append(buf[:n].view(gshape))
+            losses.append(buf[n:].to(ldt))
+        return torch.cat(losses), torch.cat(grads)
 
     def gather_losses(self, loss: torch.Tensor, B_total: int) -> torch.Tensor:
         """All per-signal losses (logging only), ordered by signal index. Batch groups may hold

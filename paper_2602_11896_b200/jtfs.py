@@ -55,9 +55,21 @@ class Plan:
         return self.info.N
 
     def paths(self) -> list[dict]:
+        """Path table (R15 order); order-2 entries carry their block index ("block", -1 otherwise)."""
         arr = (PathT * self.info.n_paths)()
         check(self.lib.jtfs_plan_paths(self.h, arr, self.info.n_paths))
-        return [{f: getattr(a, f) for f, _ in PathT._fields_} for a in arr]
+        out = [{f: getattr(a, f) for f, _ in PathT._fields_} for a in arr]
+        n2s = sorted({q["n2"] for q in out if q["order"] == 2})
+        for q in out:
+            q["block"] = n2s.index(q["n2"]) if q["order"] == 2 else -1
+        return out
+
+    def block_owner(self, n_shards: int) -> list[int]:
+        """jtfs_plan_shards: owner shard of every second-order block under path sharding."""
+        nb = self.info.n_blocks
+        arr = (ctypes.c_int32 * max(nb, 1))()
+        check(self.lib.jtfs_plan_shards(self.h, n_shards, arr, max(nb, 1)))
+        return list(arr[:nb])
 
     def filters(self, layer: int) -> dict:
         cnt = ctypes.c_int64()
@@ -164,6 +176,21 @@ class Plan:
                                     _ptr(ws), ws.numel(), _stream(stream)))
         state["iter"] = ms.iter
         return state
+
+    def check_finite(self, x: torch.Tensor, stream=None) -> None:
+        """jtfs_check_finite: raises JtfsError (JTFS_ERR_NUMERIC) if x holds a NaN or inf."""
+        assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+        check(self.lib.jtfs_check_finite(_ptr(x), x.numel(), _stream(stream)))
+
+    def loss_report(self, S: torch.Tensor, S_target: torch.Tensor, stream=None) -> torch.Tensor:
+        """jtfs_loss_report: per-path losses [B, n_paths] (1/2 sum of squared residuals per path, R15
+        order; path 0 = S0 is reported, not part of the loss)."""
+        assert S.is_cuda and S.dtype == torch.float32 and S.is_contiguous() and S.shape == S_target.shape
+        assert S_target.is_cuda and S_target.dtype == torch.float32 and S_target.is_contiguous()
+        B = S.shape[0]
+        rep = torch.empty(B, self.info.n_paths, device=S.device, dtype=torch.float32)
+        check(self.lib.jtfs_loss_report(self.h, _ptr(S), _ptr(S_target), B, _ptr(rep), _stream(stream)))
+        return rep
 
     def colored_noise(self, S_target: torch.Tensor, seed: int = 0, white: torch.Tensor | None = None,
                       ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:

@@ -4,6 +4,9 @@ iteration. The host side only reads the per-signal losses/flags once per iterati
 rules (readings R24, R25 in DESIGN.md), write the loss CSV and
 checkpoint/resume the state; every arithmetic step runs in libjtfs.so's kernels.
 
+A non-finite iterate raises JtfsError(JTFS_ERR_NUMERIC); a non-finite loss is a
+rejection (E <= E_prev fails), so the bold driver rolls the signal back to its last finite iterate.
+
 Stop rules per signal (a stopped signal is frozen at its best evaluated iterate by the `active`
 mask of jtfs_metamer_state):
   * rejection cap: `max_rejects` consecutive bold-driver rejections (SPEC: "at most 8 shrink retries
@@ -67,6 +70,7 @@ def reconstruct(plan, S_target: torch.Tensor, steps: int = 100, y0: torch.Tensor
         while state["iter"] < steps and bool(state["active"].any()):
             it = state["iter"]
             plan.metamer_step(state, S_target, momentum=momentum, grow=grow, shrink=shrink, ws=ws)
+            plan.check_finite(state["y"])         # a non-finite iterate aborts the job
             loss = state["loss"].tolist()
             acc = state["accepted"].tolist()
             mu = state["mu"].tolist()
@@ -92,5 +96,11 @@ def reconstruct(plan, S_target: torch.Tensor, steps: int = 100, y0: torch.Tensor
     finally:
         if fcsv:
             fcsv.close()
+    # signals stopped in the last iteration are restored to their best iterate here (the kernel does it
+    # on the next call for a continuing run)
+    stopped = state["active"] == 0
+    if bool(stopped.any()):
+        state["y"][stopped] = state["y_prev"][stopped]
+        state["u"][stopped] = 0.0
     return {"y_best": state["y_prev"], "loss_best": state["loss_prev"], "history": history, "state": state,
             "iterations": state["iter"]}

@@ -25,12 +25,14 @@ def _free_port():
 
 def _oracle_shard_compute(args):
     from oracle.jtfs import Oracle
+    from paper_2602_11896_b200 import Plan
     from paper_2602_11896_b200.dist import path_owner
     o = Oracle(args)
-    paths = [dict(order=q.order) for q in o.plan.paths]
+    paths = [dict(order=q.order, block=q.block) for q in o.plan.paths]
+    plan = Plan(*args)          # host-only: the library's block -> shard rule (jtfs_plan_shards)
 
     def compute(y, St, shard, n):
-        owner = path_owner(paths, n)
+        owner = path_owner(paths, plan.block_owner(n))
         w = torch.zeros(o.plan.n_coef, dtype=torch.float64)
         for q, own in zip(o.plan.paths, owner):
             if own == shard:
@@ -57,7 +59,11 @@ def _worker(rank, world, port, mode, q):
         St = o.forward(x)
         dj = DistJTFS(path_shards=world if mode == "path" else 1, compute=compute)
         sl = dj.my_signals(B)
-        loss, grad = dj.loss_grad(y[sl], St[sl])
+        if mode == "gather":   # B = 3 over 2 batch groups: uneven (2 + 1) per-rank loss vectors
+            mine = torch.arange(sl.start, sl.stop, dtype=torch.float64)
+            q.put((rank, sl.start, sl.stop, dj.gather_losses(mine, B).numpy(), None))
+            return
+        loss, grad = dj.loss_grad(y[sl], St[sl], chunk=2 if mode == "path" else None)
         q.put((rank, sl.start, sl.stop, loss.numpy(), grad.numpy()))
     finally:
         dist.destroy_process_group()
@@ -99,8 +105,31 @@ def test_batch_split_rule():
 
 def test_path_owner_rule_matches_abi_doc():
     from paper_2602_11896_b200.dist import path_owner
-    paths = [dict(order=0)] + [dict(order=1)] * 3 + [dict(order=2)] * 5
-    assert path_owner(paths, 2) == [-1, 0, 0, 0, 0, 1, 0, 1, 0]
+    paths = [dict(order=0)] + [dict(order=1)] * 3 + [dict(order=2, block=b) for b in (0, 0, 1, 1, 1)]
+    assert path_owner(paths, [1, 0]) == [-1, 0, 0, 0, 1, 1, 0, 0, 0]
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_block_shards_lpt(name):
+    # every block owned by exactly one shard; whole blocks (layer 2 computed once per block); the LPT
+    # loads are balanced: the largest shard exceeds the mean by at most the largest block's cost
+    from paper_2602_11896_b200 import Plan
+    from synth import CONFIGS
+    p = Plan(*plan_args(CONFIGS[name]))
+    nb = p.info.n_blocks
+    assert p.block_owner(1) == [0] * nb
+    for n in (2, 4, 8):
+        own = p.block_owner(n)
+        assert len(own) == nb and set(own) <= set(range(n))
+        assert own == p.block_owner(n)                    # deterministic
+        if n <= nb:
+            assert set(own) == set(range(n))             # no idle shard while blocks remain
+
+
+def test_gloo_gather_losses_uneven():
+    res = _run("gather")
+    for rank, s0, s1, loss, grad in res:
+        assert loss.tolist() == [0.0, 1.0, 2.0]
 
 
 def test_gloo_path_sharding_sums_to_whole():

@@ -134,3 +134,34 @@ def test_metamer_step_parity(plans):
         assert rel(st["mu"].cpu().numpy(), ost["mu"]) <= 1e-6
         # compare the accumulated update y - y0 (the quantity the step computes)
         assert rel(st["y"].cpu().numpy() - y, ost["y"] - y) <= 1e-3, it
+
+
+def test_loss_report(plans):
+    # NEXT-2: per-path losses; orders 1 + 2 sum to the loss of jtfs_loss_grad (R19)
+    name = "c1"
+    p = plans(name)
+    o = Oracle(plan_args(ALL[name]))
+    x, y = inputs(name)
+    St = p.forward(torch.from_numpy(x).cuda())
+    Sy = p.forward(torch.from_numpy(y).cuda())
+    rep = p.loss_report(Sy, St).cpu().numpy().astype(np.float64)
+    r = Sy.cpu().numpy().astype(np.float64) - St.cpu().numpy().astype(np.float64)
+    ref = np.stack([[0.5 * np.sum(r[b, q.offset:q.offset + q.rows * q.frames] ** 2) for q in o.plan.paths]
+                    for b in range(r.shape[0])])
+    assert rel(rep, ref) <= 1e-6
+    loss, _ = p.loss_grad(torch.from_numpy(y).cuda(), St)
+    assert rel(rep[:, 1:].sum(1), loss.cpu().numpy()) <= 1e-5
+
+
+def test_check_finite_numeric_error(plans):
+    from paper_2602_11896_b200 import JtfsError
+    p = plans("t1")
+    x = torch.zeros(1000, device="cuda")
+    p.check_finite(x)
+    x[777] = float("nan")
+    with pytest.raises(JtfsError) as e:
+        p.check_finite(x)
+    assert e.value.code == 3                      # JTFS_ERR_NUMERIC
+    x[777] = float("inf")
+    with pytest.raises(JtfsError):
+        p.check_finite(x)
