@@ -212,6 +212,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="also time the step replayed from a CUDA graph")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: split the config's batch over the batch groups (c5: B = 256 over G)")
     ap.add_argument("--no-forward", action="store_true", help="skip the forward-only (analysis) measurement")
@@ -304,6 +305,33 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = B_total * cfg["N"] * args.steps / (ms / 1000.0)
+
+    # CUDA-graph replay of the same step (launch-latency-bound configs, c1: SURVEY §8(d)); the library
+    # only enqueues (no host sync inside jtfs_loss_grad), so one step captures whole, side streams included
+    graph = None
+    if args.graph and ps == 1:
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            plan.loss_grad(y, St, loss=loss, grad=grad, ws=ws)      # warm the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            plan.loss_grad(y, St, loss=loss, grad=grad, ws=ws)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1)
+        graph = {"ms_per_step": gms / args.steps, "ms_per_step_eager": ms / args.steps,
+                 "value": B_total * cfg["N"] * args.steps / (gms / 1000.0), "unit": UNIT,
+                 "what": "one jtfs_loss_grad captured in a CUDA graph (all its launches), replayed"}
 
     # forward-only analysis throughput (NEXT-2): jtfs_forward over the same batch
     fo_ms = None
@@ -457,6 +485,8 @@ def main() -> None:
     }
     if e2e:
         line["e2e"] = e2e
+    if graph:
+        line["cuda_graph"] = graph
     if fo_ms is not None:
         line["forward_only"] = {"value": B_total * cfg["N"] * args.steps / (fo_ms / 1000.0), "unit": UNIT,
                                 "ms_per_step": fo_ms / args.steps,

@@ -54,6 +54,10 @@ typedef enum {
  * Errors: JTFS_ERR_CONFIG (constraint named), JTFS_ERR_OOM. Touches no GPU. */
 jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
                       jtfs_plan_t* out);
+/* Same with the second-layer temporal quality factor Q2 = Q^{tm,2} ("its own hyperparameters";
+ * 1 <= Q2 <= 16). jtfs_plan is jtfs_plan_q2 with Q2 = 1 (R7). */
+jtfs_status jtfs_plan_q2(int64_t N, int J, int Q, int Q2, int J_fr, int Q_fr, int64_t T, int64_t F,
+                         jtfs_plan_t* out);
 jtfs_status jtfs_plan_destroy(jtfs_plan_t plan); /* frees host and device copies */
 
 typedef struct {

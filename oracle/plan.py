@@ -144,12 +144,15 @@ class Plan:
         return 1 + len(self.psi_fr_plus)
 
 
-def make_plan(N: int, J: int, Q: int, J_fr: int, Q_fr: int, T: int, F: int) -> Plan:
-    """Build the plan (readings R1-R3, R6-R8, R10-R16)."""
+def make_plan(N: int, J: int, Q: int, J_fr: int, Q_fr: int, T: int, F: int, Q2: int = 1) -> Plan:
+    """Build the plan (readings R1-R3, R6-R8, R10-R16). Q2 = Q^{tm,2}, the
+    second-layer temporal quality factor ("its own hyperparameters"; R7: 1 by default)."""
     def ispow2(v):
         return v >= 1 and (v & (v - 1)) == 0
     if J < 1 or Q < 1 or J_fr < 1 or Q_fr < 1:
         raise PlanError("J, Q, J_fr, Q_fr must be >= 1")
+    if not 1 <= Q2 <= 16:
+        raise PlanError("need 1 <= Q2 <= 16")
     if not ispow2(T):
         raise PlanError("T must be a power of two")
     if not ispow2(F):
@@ -163,7 +166,7 @@ def make_plan(N: int, J: int, Q: int, J_fr: int, Q_fr: int, T: int, F: int) -> P
         raise PlanError("N must be a positive multiple of T")
 
     psi1 = [Filter(xi, s, dyadic_scale(xi, s)) for xi, s in anden_generator(J, Q)]
-    psi2 = [Filter(xi, s, dyadic_scale(xi, s)) for xi, s in anden_generator(J, 1)]   # Q2 = 1 (R7)
+    psi2 = [Filter(xi, s, dyadic_scale(xi, s)) for xi, s in anden_generator(J, Q2)]  # Q^{tm,2} (R7)
     psi_fr_plus = [Filter(xi, s, dyadic_scale(xi, s)) for xi, s in anden_generator(J_fr, Q_fr)]
     # R6: sigma_phiT = sigma0 / T, sigma_phiF = sigma0 / F ; R3: j(phi_T)=log2T, j(phi_F)=log2F
     phiT = Filter(0.0, SIGMA0 / T, log2T, 0, "phi")

@@ -48,6 +48,7 @@ _I = ctypes.c_int
 _SZ = ctypes.c_size_t
 _SIGS = {
     "jtfs_plan": (_I, [_I64, _I, _I, _I, _I, _I64, _I64, ctypes.POINTER(_P)]),
+    "jtfs_plan_q2": (_I, [_I64, _I, _I, _I, _I, _I, _I64, _I64, ctypes.POINTER(_P)]),
     "jtfs_plan_destroy": (_I, [_P]),
     "jtfs_plan_info": (_I, [_P, ctypes.POINTER(PlanInfo)]),
     "jtfs_plan_paths": (_I, [_P, ctypes.POINTER(PathT), _I64]),

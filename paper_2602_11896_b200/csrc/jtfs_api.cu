@@ -677,6 +677,11 @@ jtfs_status jtfs_plan_cost(jtfs_plan_t plan, double* out, int64_t cap) {
 int64_t jtfs_launch_count(void) { return jtfs::g_launches.load(); }
 
 jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, jtfs_plan_t* out) {
+  return jtfs_plan_q2(N, J, Q, 1, J_fr, Q_fr, T, F, out);
+}
+
+jtfs_status jtfs_plan_q2(int64_t N, int J, int Q, int Q2, int J_fr, int Q_fr, int64_t T, int64_t F,
+                         jtfs_plan_t* out) {
   if (!out) return fail(JTFS_ERR_SIZE, "out is NULL");
   *out = nullptr;
   jtfs_plan_s* h = new (std::nothrow) jtfs_plan_s();
@@ -684,7 +689,7 @@ jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, in
   std::string err;
   int rc;
   try {
-    rc = make_plan(N, J, Q, J_fr, Q_fr, T, F, &h->p, &err);
+    rc = make_plan(N, J, Q, J_fr, Q_fr, T, F, &h->p, &err, Q2);
   } catch (const std::bad_alloc&) {
     delete h;
     return fail(JTFS_ERR_OOM, "host allocation failed");

@@ -115,6 +115,7 @@ struct Plan {
   // ---- hyper-parameters
   int64_t N = 0, T = 0, F = 0;
   int J = 0, Q = 0, J_fr = 0, Q_fr = 0, log2T = 0, log2F = 0;
+  int Q2 = 1;                                   // second-layer quality factor (R7)
   // ---- filterbanks
   std::vector<Filter> psi1, psi2, psi_fr_plus, L_fr;
   Filter phiT, phiF;
@@ -177,8 +178,8 @@ struct Plan {
 };
 
 // planner.cpp
-int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, Plan* p,
-              std::string* err);
+int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, Plan* p, std::string* err,
+              int Q2 = 1);
 double response_at(const Filter& f, double omega);   // periodised level-0 response
 void level_response(const Filter& f, int64_t L0, int k, std::vector<double>* out);
 

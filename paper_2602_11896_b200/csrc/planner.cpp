@@ -396,7 +396,7 @@ static void build_tc_tables(Plan* p) {
 }
 
 int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F, Plan* p,
-              std::string* err) {
+              std::string* err, int Q2) {
   auto ispow2 = [](int64_t v) { return v >= 1 && (v & (v - 1)) == 0; };
   if (J < 1 || Q < 1 || J_fr < 1 || Q_fr < 1) { *err = "J, Q, J_fr, Q_fr must be >= 1"; return 1; }
   if (!ispow2(T)) { *err = "T must be a power of two"; return 1; }
@@ -406,6 +406,7 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
   if (!(0 <= log2F && log2F <= J_fr)) { *err = "need 0 <= log2(F) <= J_fr"; return 1; }
   if (N < T || N % T != 0) { *err = "N must be a positive multiple of T"; return 1; }
   if (J > 24 || J_fr > 16 || Q > 64 || Q_fr > 16) { *err = "J <= 24, J_fr <= 16, Q <= 64, Q_fr <= 16"; return 1; }
+  if (Q2 < 1 || Q2 > 16) { *err = "need 1 <= Q2 <= 16"; return 1; }
 
   p->N = N; p->J = J; p->Q = Q; p->J_fr = J_fr; p->Q_fr = Q_fr; p->T = T; p->F = F;
   p->log2T = log2T; p->log2F = log2F;
@@ -414,7 +415,9 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     return f;
   };
   for (auto& q : anden_generator(J, Q)) p->psi1.push_back(mk(q.first, q.second));
-  for (auto& q : anden_generator(J, 1)) p->psi2.push_back(mk(q.first, q.second));   // R7
+  // second-layer temporal filterbank: Q^{tm,2} (R7: Q2 = 1 by default)
+  for (auto& q : anden_generator(J, Q2)) p->psi2.push_back(mk(q.first, q.second));
+  p->Q2 = Q2;
   for (auto& q : anden_generator(J_fr, Q_fr)) p->psi_fr_plus.push_back(mk(q.first, q.second));
   p->phiT.phi = true; p->phiT.sigma = kSigma0 / (double)T; p->phiT.j = log2T; p->phiT.spin = 0;
   p->phiF.phi = true; p->phiF.sigma = kSigma0 / (double)F; p->phiF.j = log2F; p->phiF.spin = 0;

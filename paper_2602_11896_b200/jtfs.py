@@ -26,12 +26,13 @@ def _stream(stream=None) -> int:
 class Plan:
     """jtfs_plan(N, J, Q, J_fr, Q_fr, T, F) (§3.1 filterbanks; readings in DESIGN.md §2)."""
 
-    def __init__(self, N: int, J: int, Q: int, J_fr: int, Q_fr: int, T: int, F: int):
+    def __init__(self, N: int, J: int, Q: int, J_fr: int, Q_fr: int, T: int, F: int, Q2: int = 1):
         self.lib = _lib.load()
         h = ctypes.c_void_p()
-        check(self.lib.jtfs_plan(N, J, Q, J_fr, Q_fr, T, F, ctypes.byref(h)))
+        check(self.lib.jtfs_plan_q2(N, J, Q, Q2, J_fr, Q_fr, T, F, ctypes.byref(h)))
         self.h = h
         self.args = (N, J, Q, J_fr, Q_fr, T, F)
+        self.Q2 = Q2
         info = PlanInfo()
         check(self.lib.jtfs_plan_info(self.h, ctypes.byref(info)))
         self.info = info

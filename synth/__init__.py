@@ -30,11 +30,21 @@ TINY = {
     "spec": dict(N=1024, J=5, Q=2, J_fr=3, Q_fr=1, T=8, F=2),
 }
 
+# plan variants described by the listings: a second-layer quality factor Q2 > 1
+# and second-layer scales beyond log2 T (j2 > log2 T, reading R13's common stride)
+VARIANTS = {
+    "q2": dict(N=1024, J=5, Q=2, J_fr=3, Q_fr=1, T=8, F=2, Q2=2),
+    "q2b": dict(N=4096, J=6, Q=8, J_fr=3, Q_fr=1, T=64, F=8, Q2=4),
+    "j2gtT": dict(N=2048, J=6, Q=4, J_fr=2, Q_fr=1, T=8, F=2),
+}
+
 _CINDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
 
 
 def plan_args(cfg: dict) -> tuple:
-    return (cfg["N"], cfg["J"], cfg["Q"], cfg["J_fr"], cfg["Q_fr"], cfg["T"], cfg["F"])
+    """(N, J, Q, J_fr, Q_fr, T, F[, Q2]) -- Q2 only when the config sets it (default 1)."""
+    a = (cfg["N"], cfg["J"], cfg["Q"], cfg["J_fr"], cfg["Q_fr"], cfg["T"], cfg["F"])
+    return a + (cfg["Q2"],) if cfg.get("Q2", 1) != 1 else a
 
 
 def _peak_normalise(x: np.ndarray, peak: float = 0.5) -> np.ndarray:

@@ -4,9 +4,9 @@ import numpy as np
 import pytest
 
 from oracle import plan as op
-from synth import CONFIGS, TINY, plan_args
+from synth import CONFIGS, TINY, VARIANTS, plan_args
 
-ALL = {**CONFIGS, **TINY}
+ALL = {**CONFIGS, **TINY, **VARIANTS}
 
 
 @pytest.fixture(scope="module")
@@ -74,3 +74,11 @@ def test_workspace_affine(jt):
     w1, w2, w5 = (p.workspace_size(b, True) for b in (1, 2, 5))
     assert w2 - w1 == w1 and w5 == 5 * w1
     assert p.workspace_size(1, True) >= p.workspace_size(1, False)
+
+
+def test_q2_filterbank():
+    # Q2 = Q^{tm,2}: the second-layer bank is the generator at Q2 (more blocks, same rules)
+    for name in ("q2", "q2b"):
+        o = op.make_plan(*plan_args(VARIANTS[name]))
+        assert len(o.psi2) > len(op.make_plan(*plan_args(VARIANTS[name])[:7]).psi2)
+        assert all(b.n1_max == sum(1 for f in o.psi1 if f.j < b.j2) for b in o.blocks)

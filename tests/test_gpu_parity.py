@@ -6,10 +6,10 @@ import torch
 
 from oracle.jtfs import Oracle
 from oracle import metamer as om
-from synth import CONFIGS, TINY, plan_args, noise, batch
+from synth import CONFIGS, TINY, VARIANTS, plan_args, noise, batch
 
 pytestmark = pytest.mark.gpu
-ALL = {**CONFIGS, **TINY}
+ALL = {**CONFIGS, **TINY, **VARIANTS}
 
 
 def rel(a, b):
@@ -32,7 +32,7 @@ def plans():
 
 def inputs(name, B=2):
     cfg = ALL[name]
-    if name in TINY:
+    if name in TINY or name in VARIANTS:
         return noise(cfg["N"], B, seed=31), noise(cfg["N"], B, seed=32)
     return batch(name, B), batch(name, B, which="y")
 
@@ -56,7 +56,7 @@ def test_stage_U1_S1t_Y2(plans, name):
         assert rel(g3, Y2) <= 1e-5
 
 
-@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1"])
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1", "q2", "q2b", "j2gtT"])
 def test_forward_parity(plans, name):
     p = plans(name)
     o = Oracle(plan_args(ALL[name]))
@@ -70,7 +70,7 @@ def test_forward_parity(plans, name):
         assert rel(S[:, sl], So[:, sl]) <= 1e-3, q
 
 
-@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1"])
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1", "q2", "q2b", "j2gtT"])
 def test_loss_grad_parity(plans, name):
     p = plans(name)
     o = Oracle(plan_args(ALL[name]))

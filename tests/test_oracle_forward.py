@@ -6,7 +6,7 @@ import torch
 from oracle import brute
 from oracle.jtfs import Oracle, subsample_fourier, reflect_index
 from oracle.plan import make_plan
-from synth import CONFIGS, TINY, plan_args, noise
+from synth import CONFIGS, TINY, VARIANTS, plan_args, noise
 
 
 def test_subsample_fourier_is_decimation():
@@ -29,10 +29,11 @@ def test_reflect_pad_example():
     assert (torch.tensor([1., 2., 3., 4.])[idx]).tolist() == [2, 1, 1, 2, 3, 4, 4, 3]
 
 
-@pytest.mark.parametrize("name", ["t1", "t2", "spec"])
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "q2", "j2gtT"])
 def test_fft_route_equals_direct_sums(name):
-    # brute.py: O(L^2) direct circular sums with closed-form kernels, depth-first, no FFT
-    p = make_plan(*plan_args(TINY[name]))
+    # brute.py: O(L^2) direct circular sums with closed-form kernels, depth-first, no FFT; also on the
+    # plan variants Q2 = 2 and j2 > log2 T (R13)
+    p = make_plan(*plan_args({**TINY, **VARIANTS}[name]))
     x = noise(p.N, 1, seed=11)
     So = Oracle(p).forward(x)[0].numpy()
     Sb = brute.forward(p, x[0])
