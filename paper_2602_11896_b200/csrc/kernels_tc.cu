@@ -86,8 +86,13 @@ struct TcArgs {
   int part, pmode;                  // K part of this launch; kPm* bits
   int ng;                           // filter groups: CTA x handles column tile x % ntiles, filters f = x / ntiles mod ng
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
+  int fexpt;                        // timing experiments only (JTFS_TC_FEXPT: 1 no W loads, 2 no W stores)
 };
 constexpr int kPmLoad = 1, kPmStore = 2, kPmFinish = 4;
+static const int g_tc_fexpt = [] {
+  const char* e = std::getenv("JTFS_TC_FEXPT");
+  return e ? std::atoi(e) : 0;
+}();
 #ifdef JTFS_TC_TRACE
 #define TC_TRACE(ev, g)                                                                  \
   do {                                                                                   \
@@ -342,20 +347,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
             if (lane == 0) tc::mbar_arrive(&tempty[buf]);
           }
           if (pmode != kPmFinish) {
-            // split-K: W of (tile t, column c, rows h*32 ..) accumulated across the K parts
-            float4* wp = reinterpret_cast<float4*>(
-                a.wbuf + b * a.wb_sb + TB.wp_off +
-                (((int64_t)ct * TB.wp_tiles + tu.wp_tile0 + t) * 128 + c) * 128 + h * 64);
-            if (pmode & kPmLoad) {
+            // split-K: W of (tile t, column c, rows h*32 ..) accumulated across the K parts. Layout per
+            // (column tile, 64-row tile): [float4 group g = (2 row + re/im) / 4][column c] -- a warp's 32
+            // columns of one group are 512 contiguous bytes (coalesced loads and stores)
+            float4* wp = reinterpret_cast<float4*>(a.wbuf + b * a.wb_sb + TB.wp_off) +
+                         ((int64_t)ct * TB.wp_tiles + tu.wp_tile0 + t) * (128 * 32) + (h * 16) * 128 + c;
+            if ((pmode & kPmLoad) && !(a.fexpt & 1)) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float4 w = wp[i];
+                const float4 w = wp[i * 128];
                 v[4 * i] += w.x; v[4 * i + 1] += w.y; v[4 * i + 2] += w.z; v[4 * i + 3] += w.w;
               }
             }
-            if (pmode & kPmStore) {
+            if ((pmode & kPmStore) && !(a.fexpt & 2)) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) wp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              for (int i = 0; i < 16; ++i)
+                wp[i * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
             if (!(pmode & kPmFinish)) continue;
           }
@@ -456,7 +463,7 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
                 (part == nparts - 1 ? kPmFinish : 0);
       }
       TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
-               (int)p.L_fr.size(), own, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr};
+               (int)p.L_fr.size(), own, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr, g_tc_fexpt};
 #ifdef JTFS_TC_TRACE
       static long long* ftrace = nullptr;
       if (!ftrace) cudaMalloc(&ftrace, 16 * 512 * 8);
@@ -782,14 +789,14 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
                                                        : 0.f;
     };
     // split-K mode: W of (tile, column, this warp's 8 rows) from the forward's buffer, one tile ahead
-    const float* wcol = ksm ? a.wbuf + b * a.wb_sb + TB.wp_off +
-                                  (((int64_t)ct * TB.wp_tiles) * 128 + c) * 128 + h * 16
-                            : nullptr;
+    // forward's W layout per (column tile, 64-row tile): [float4 group g][column], g = (2 row + re/im) / 4
+    const float4* wcol = ksm ? reinterpret_cast<const float4*>(a.wbuf + b * a.wb_sb + TB.wp_off) +
+                                   (int64_t)ct * TB.wp_tiles * (128 * 32) + (h * 4) * 128 + c
+                             : nullptr;
     auto load_wv = [&](int u, int t32, float4* wv) {
-      const float4* q4 = reinterpret_cast<const float4*>(
-          wcol + ((int64_t)(a.tcu[u].wp_tile0 + (t32 >> 1)) * 128) * 128 + (t32 & 1) * 64);
+      const float4* q4 = wcol + (int64_t)(a.tcu[u].wp_tile0 + (t32 >> 1)) * (128 * 32) + ((t32 & 1) * 16) * 128;
 #pragma unroll
-      for (int i = 0; i < kBwRpw / 2; ++i) wv[i] = q4[i];
+      for (int i = 0; i < kBwRpw / 2; ++i) wv[i] = q4[i * 128];
     };
     int f = next_unit(0);
     float gor_n[KAP];
