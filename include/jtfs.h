@@ -49,7 +49,8 @@ typedef enum {
  *  J,Q   first-layer scale and quality factor (J >= 1, Q >= 1)
  *  J_fr,Q_fr frequential scale and quality factor (>= 1)
  *  T,F   time / log-frequency averaging widths, powers of two, 1 <= log2 T <= J,
- *        0 <= log2 F <= J_fr; N_pad (R10) must be <= 2^22; ceil(N1/F) <= 32 (GPU limit).
+ *        0 <= log2 F <= J_fr; N_pad (R10) must be <= 2^22; ceil(N1/F) <= 32, or <= 64 when
+ *        P <= 1024 (GPU limit: rows beyond 32 take the FFT route of the joint stage).
  *  out   receives the handle; release with jtfs_plan_destroy.
  * Errors: JTFS_ERR_CONFIG (constraint named), JTFS_ERR_OOM. Touches no GPU. */
 jtfs_status jtfs_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
@@ -137,6 +138,13 @@ typedef struct {
 jtfs_status metamer_step(jtfs_plan_t plan, jtfs_metamer_state* st, const float* S_target,
                          int64_t B, float momentum, float grow, float shrink, void* ws,
                          size_t ws_bytes, jtfs_stream_t stream);
+
+/* Test-only: the library's batched C2C FFT (fft.cu) on device rows, for benchmarking against cuFFT
+ * (tools/fft_vs_cufft.py): out[b][r][.] = FFT(in[b][r][.]) for B x count rows of length L (power of two,
+ * 2 <= L <= the plan's N_pad); inverse includes 1/L; dbl = 0: complex64, 1: complex128. For L > 4096 the
+ * input is clobbered (four-step scheme). Stream-ordered. */
+jtfs_status jtfs_debug_fft(jtfs_plan_t plan, const void* in, void* out, int64_t L, int64_t count, int64_t B,
+                           int inverse, int dbl, jtfs_stream_t stream);
 
 /* Non-finite check ("non-finite direction -> numeric error"): returns JTFS_ERR_NUMERIC if any
  * of x[0..n) (device fp32) is NaN or +-inf, JTFS_OK otherwise. Synchronises `stream` (the only call

@@ -61,6 +61,7 @@ _SIGS = {
     "metamer_step": (_I, [_P, ctypes.POINTER(MetamerState), _P, _I64, ctypes.c_float, ctypes.c_float,
                           ctypes.c_float, _P, _SZ, _P]),
     "jtfs_check_finite": (_I, [_P, _I64, _P]),
+    "jtfs_debug_fft": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _I, _P]),
     "jtfs_plan_shards": (_I, [_P, _I, _P, _I64]),
     "jtfs_loss_report": (_I, [_P, _P, _P, _I64, _P, _P]),
     "jtfs_colored_noise": (_I, [_P, _P, _P, _I64, _P, _P, _SZ, _P]),

@@ -57,6 +57,10 @@ struct DeviceTables {
   // phi_T kernels: (unit, rho) rows in unit order and the prefix of their 256-column tiles
   int32_t* phT_rows_u = nullptr;    int32_t* phT_tiles = nullptr;   /* per adjoint tile: u, rho, c0 */  int phT_nrows = 0;  int64_t phT_ntiles = 0;
   int32_t* blk_nmax = nullptr;      // [n_blocks]
+  // phi_T banded-GEMM adjoint (k_phiT_adj3) for the halo-pruned blocks: 32-row groups {first row, rows,
+  // block, -, ...}, their (unit, rho) rows, tiles (group, 256-column tile), the mask of the blocks covered
+  int32_t* ph3_groups = nullptr;    int32_t* ph3_rows = nullptr;   int32_t* ph3_atiles = nullptr;
+  int ph3_ngroups = 0;  int64_t ph3_natiles = 0;  uint64_t ph3_mask = 0;
   int64_t* ucoef = nullptr;         // [n_units] coefficient offset of the unit's path - o2_start
   int64_t* uo = nullptr;            // [n_units] o_off
   int64_t o2_start = 0, n_o2 = 0;

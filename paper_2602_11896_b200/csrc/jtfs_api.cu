@@ -152,7 +152,7 @@ static void free_tables(DeviceTables* d) {
                   d->phiF_off, d->phiT_half, d->phiT_off, d->phiT_H, d->units, d->binfo, d->kf_of,
                   d->blk_nmax, d->ucoef, d->uo, d->bwd_tiles, d->coef_path, d->path_off, d->path_owner_unit, d->l1_off,
                   d->n1_k1, d->u1adj_tiles, d->gx_tile_start, d->gx_list, d->o1_rlo, d->o1_nrows, d->tw, d->twd,
-                  d->fr_spec, d->u_wts, d->u_wt_off, d->hfr_H, d->phT_rows_u, d->phT_tiles, d->ffw.blist, d->ffw.tiles, d->ffb.blist, d->ffb.tiles};
+                  d->fr_spec, d->u_wts, d->u_wt_off, d->hfr_H, d->phT_rows_u, d->phT_tiles, d->ph3_groups, d->ph3_rows, d->ph3_atiles, d->ffw.blist, d->ffw.tiles, d->ffb.blist, d->ffb.tiles};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int c = 0; c < 6; ++c) {
@@ -286,6 +286,12 @@ static cudaError_t upload(Plan& p) {
     d->phT_ntiles = (int64_t)(ti.size() / 3);
     UP(ru, phT_rows_u);
     UP(ti, phT_tiles);
+  }
+  if (!p.ph3_groups.empty()) {
+    UP(p.ph3_groups, ph3_groups); UP(p.ph3_rows, ph3_rows); UP(p.ph3_atiles, ph3_atiles);
+    d->ph3_ngroups = (int)(p.ph3_groups.size() / 8);
+    d->ph3_natiles = (int64_t)(p.ph3_atiles.size() / 2);
+    d->ph3_mask = p.ph3_mask;
   }
   std::vector<int32_t> nm;
   std::vector<int64_t> bt;
@@ -939,6 +945,24 @@ jtfs_status jtfs_loss_grad_host(jtfs_plan_t plan, const float* y_host, const flo
   CK(cudaMemcpyAsync(loss_host, loss, B * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(grad_host, grad, B * p.N * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_debug_fft(jtfs_plan_t plan, const void* in, void* out, int64_t L, int64_t count, int64_t B,
+                           int inverse, int dbl, jtfs_stream_t stream) {
+  if (!plan || !in || !out) return fail(JTFS_ERR_SIZE, "NULL argument");
+  jtfs_status s = ensure_device(plan);
+  if (s) return s;
+  const Plan& p = plan->p;
+  if (L < 2 || (L & (L - 1)) || L > p.N_pad || count < 1 || B < 1)
+    return fail(JTFS_ERR_SIZE, "need L a power of two in [2, N_pad], count >= 1, B >= 1");
+  Rows ri{count * L, 0, count, L}, ro{count * L, 0, count, L};
+  cudaError_t e = dbl ? fft_launch_dd((const double2*)in, (double2*)out, ri, ro, (int)B, inverse != 0, p.dev->fftt,
+                                      (cudaStream_t)stream)
+                      : fft_launch((const float2*)in, (float2*)out, ri, ro, (int)B, inverse != 0, p.dev->fftt,
+                                   (cudaStream_t)stream);
+  CK(e);
+  t_err.clear();
   return JTFS_OK;
 }
 

@@ -832,6 +832,87 @@ __global__ void __launch_bounds__(256) k_phiT_fwd2(
   }
 }
 
+// ---- phi_T adjoint as a banded GEMM (blocks whose needed columns are not the whole circle, i.e.
+// unwrapped halo-pruned columns). For one block all rows (unit, rho) share the column grid: column i sits
+// at x = m0 D - H + i, frame t' at (m0 + t') D, so Eq.4's phi_T + stride-T decimation is S[row][t'] =
+// sum_i Phi[t'][i] o[row][i] with Phi[t'][i] = tT_s2[|t' D + H - i|] (zero beyond H), and its adjoint is
+// g_o = R Phi. (The forward keeps the per-row kernel k_phiT_fwd2: one warp per frame reading a contiguous
+// window; a banded-GEMM forward measured slower, 18.0 vs 14.3 ms at c4.)
+// adjoint: g_o[row][i] = sum_t' Phi[t'][i] r[row][t'] for a 32-row group and a 256-column tile; the tile's
+// frame band (<= 32 frames per pass) and r staged in SMEM; 8 rows x 4 columns per thread
+__global__ void __launch_bounds__(256) k_phiT_adj3(
+    const float* __restrict__ rres, int64_t r_sb, float* __restrict__ go, int64_t go_sb,
+    const int32_t* __restrict__ grp, const int32_t* __restrict__ grows, const int32_t* __restrict__ atiles,
+    const JointUnit* __restrict__ units, const BlockInfo* __restrict__ binfo, const float* __restrict__ phiT_half,
+    const int64_t* __restrict__ phiT_off, const int64_t* __restrict__ phiT_H, const int64_t* __restrict__ ucoef,
+    int64_t o2_start, int frames, uint64_t own) {
+  __shared__ __align__(16) float sW[32][256];
+  __shared__ float sR[32][33];
+  const int gi = atiles[2 * blockIdx.x];
+  const int64_t c0 = (int64_t)atiles[2 * blockIdx.x + 1] * 256;
+  const int32_t* G = grp + 8 * gi;
+  const int r0 = G[0], nr = G[1], bi = G[2];
+  if (!owns_block(own, bi)) return;
+  const int b = blockIdx.y;
+  const BlockInfo bf = binfo[bi];
+  const int D = bf.D;
+  const int64_t H = phiT_H[bf.s2];
+  const float* tT = phiT_half + phiT_off[bf.s2];
+  const int tid = threadIdx.x, cq = tid & 63, rg = tid >> 6;
+  __shared__ int64_t rcoef[32];                             // residual offset of each row (per signal)
+  if (tid < 32)
+    rcoef[tid] = tid < nr ? o2_start + ucoef[grows[2 * (r0 + tid)]] + (int64_t)grows[2 * (r0 + tid) + 1] * frames : 0;
+  __syncthreads();
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // frames reaching columns [c0, c0 + 255]: t' D + 2H >= c0 and t' D <= c0 + 255
+  const int64_t mlo = (c0 - 2 * H) <= 0 ? 0 : (c0 - 2 * H + D - 1) / D;
+  const int64_t mhi = min((int64_t)frames - 1, (c0 + 255) / D);
+  for (int64_t m0 = mlo; m0 <= mhi; m0 += 32) {
+    const int nm = (int)min((int64_t)32, mhi - m0 + 1);
+    for (int idx = tid; idx < 32 * 32; idx += 256) {
+      const int r = idx >> 5, m = idx & 31;
+      float v = 0.f;
+      if (r < nr && m < nm) v = rres[b * r_sb + rcoef[r] + m0 + m];
+      sR[r][m] = v;
+    }
+    for (int idx = tid; idx < 32 * 256; idx += 256) {
+      const int m = idx >> 8, k = idx & 255;
+      const int64_t dd = (m0 + m) * D + H - (c0 + k);
+      const int64_t ad = dd < 0 ? -dd : dd;
+      sW[m][k] = (m < nm && ad <= H) ? __ldg(tT + ad) : 0.f;
+    }
+    __syncthreads();
+    for (int m = 0; m < nm; ++m) {
+      const float4 w = *reinterpret_cast<const float4*>(&sW[m][4 * cq]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float rv = sR[rg * 8 + i][m];
+        acc[i][0] = fmaf(rv, w.x, acc[i][0]);
+        acc[i][1] = fmaf(rv, w.y, acc[i][1]);
+        acc[i][2] = fmaf(rv, w.z, acc[i][2]);
+        acc[i][3] = fmaf(rv, w.w, acc[i][3]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = rg * 8 + i;
+    if (r >= nr) continue;
+    const int u = grows[2 * (r0 + r)], rho = grows[2 * (r0 + r) + 1];
+    float* dst = go + b * go_sb + units[u].o_off + (int64_t)rho * bf.n_cols;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = c0 + 4 * cq + j;
+      if (c < bf.n_cols) dst[c] = acc[i][j];
+    }
+  }
+}
+
 // loss (R19): r = S - St on owned order-1/2 coefficients (0 elsewhere), E_b = 1/2 sum r^2. Two passes
 // for a deterministic sum spread over the SMs: kLossParts CTAs per signal write float64 partials (fixed
 // coefficient ranges), one warp per signal adds them in a fixed order.
@@ -995,10 +1076,18 @@ void launch_loss(const Plan& p, const DeviceTables& d, const float* S, int64_t S
 void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64_t r_sb, float* go,
                      int64_t go_sb, uint64_t own, int B, cudaStream_t st) {
   if (p.o_size == 0 || d.phT_ntiles == 0) return;
+  if (d.ph3_natiles > 0) {
+    k_phiT_adj3<<<dim3((unsigned)d.ph3_natiles, (unsigned)B), 256, 0, st>>>(
+        r, r_sb, go, go_sb, d.ph3_groups, d.ph3_rows, d.ph3_atiles, d.units, d.binfo, d.phiT_half, d.phiT_off,
+        d.phiT_H, d.ucoef, d.o2_start, (int)p.frames, own & d.ph3_mask);
+    count_launch();
+  }
+  const uint64_t rest = own & ~d.ph3_mask & ((d.n_blocks >= 64 ? ~0ull : (1ull << d.n_blocks) - 1));
+  if (rest == 0) return;
   dim3 g((unsigned)d.phT_ntiles, (unsigned)B);
   k_phiT_adj2<<<g, 256, 0, st>>>(r, r_sb, go, go_sb, d.units, d.binfo, d.phiT_half, d.phiT_off, d.phiT_H, d.ucoef,
                                  d.phT_tiles, d.o2_start, (int)p.frames,
-                                 p.pad_left / p.T, own);
+                                 p.pad_left / p.T, rest);
   count_launch();
 }
 

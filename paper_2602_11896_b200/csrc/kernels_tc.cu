@@ -514,6 +514,7 @@ struct TcBwArgs {
   int ng;                           // filter groups (see TcArgs); ng > 1: D2 partials to gp, reduced after
   float2* gp; int64_t gp_sb;
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
+  int bmode;                        // tc_bwd_mode preference (tc_bwd_mode_pref)
 };
 
 
@@ -539,7 +540,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
   const bool ksm = TB.ks != 0;                         // split-K block: W from the forward, no GEMM1
   int nab, ta;                                         // A2 buffers; Y2 tile in TMEM (GEMM1 TS form)
   if (ksm) { nab = N2 <= 256 ? 2 : 1; ta = 0; }
-  else tc_bwd_mode(K, K2, &nab, &ta);
+  else tc_bwd_mode(K, K2, &nab, &ta, a.bmode);
   float* a_hi = reinterpret_cast<float*>(sm);          // [128][K2] (SMEM mode only)
   float* a_lo = a_hi + 128 * K2;
   float* bst1 = (ta || ksm) ? a_hi : a_lo + 128 * K2;   // ring 1 (GEMM1 B images): NS1 x STG1 floats
@@ -940,7 +941,7 @@ void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2
     return;
   }
   int nab, ta;
-  tc_bwd_mode(K, K2, &nab, &ta);
+  tc_bwd_mode(K, K2, &nab, &ta, tc_bwd_mode_pref());
   const long avail = 224L * 1024 - 1024 - (ta ? 0L : (long)2 * 128 * K2 * 4);
   // ring 2 holds up to three tiles of B2 chunks (GEMM2 runs a tile behind GEMM1 and a B2 tile takes
   // ~2 us to land from L2), ring 1 the rest
@@ -948,6 +949,14 @@ void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2
   while (n2 > 2 && avail - (long)n2 * *STG2 * 4 < 2L * *STG1 * 4) --n2;
   *NS2 = n2;
   *NS1 = (int)std::min<long>(kTcMaxStages, (avail - (long)n2 * *STG2 * 4) / (*STG1 * 4));
+}
+
+int tc_bwd_mode_pref() {
+  static const int m = [] {
+    const char* e = std::getenv("JTFS_BWD_MODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
 }
 
 static const int g_tc_expt = [] {
@@ -960,7 +969,7 @@ static void launch_tc_bwd(const TcBwArgs& a, const TcClass& C, int B, cudaStream
   int NS1, NS2, STG1, STG2;
   tc_bwd_rings(C.Kmax, C.ks ? 0 : C.K2max, C.kcw, C.kb2, &NS1, &STG1, &NS2, &STG2);
   int nab, ta;
-  tc_bwd_mode(C.Kmax, C.K2max, &nab, &ta);
+  tc_bwd_mode(C.Kmax, C.K2max, &nab, &ta, tc_bwd_mode_pref());
   if (C.ks) ta = 1;   // no A tile in SMEM
   const size_t sm = (size_t)((ta ? 0 : 2 * 128 * C.K2max) + NS1 * STG1 + NS2 * STG2) * 4 + 1024;
   cudaFuncSetAttribute(k_joint_bwd_tc<KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -996,7 +1005,7 @@ void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
     if (C.n_blocks == 0 || !owns_block(own, C.bi)) continue;   // path shards: own blocks only
     TcBwArgs a{Y2, y_sb, go, go_sb, gY, gy_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img,
                d.tc_img2, d.tc_img1b, d.tc_wts, d.tc_units, (int)p.L_fr.size(), own, thr, g_tc_expt, wbuf, wb_sb,
-               tc_groups(C, B), gp, gp_sb, nullptr};
+               tc_groups(C, B), gp, gp_sb, nullptr, tc_bwd_mode_pref()};
 #ifdef JTFS_TC_TRACE
     static long long* trace = nullptr;
     if (!trace) cudaMalloc(&trace, 16 * 512 * 8);

@@ -84,12 +84,16 @@ inline
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-void tc_bwd_mode(int K, int K2, int* nab, int* ta) {
+void tc_bwd_mode(int K, int K2, int* nab, int* ta, int pref = 0) {
   const int N2 = ((2 * K + 15) / 16) * 16;
+  // pref 1 (JTFS_BWD_MODE=1, tuning): double-buffered A2 with the Y2 tile in SMEM (GEMM1 SS form) wherever
+  // the TS form would leave a single A2 buffer
+  if (pref == 1 && N2 <= 128 && 384 + N2 + 2 * K2 > 512 && 384 + N2 <= 512) { *nab = 2; *ta = 0; return; }
   if (N2 <= 128 && 384 + N2 + 2 * K2 <= 512) { *nab = 2; *ta = 1; }
   else if (256 + N2 + 2 * K2 <= 512) { *nab = 1; *ta = 1; }
   else { *nab = N2 <= 128 ? 2 : 1; *ta = 0; }
 }
+int tc_bwd_mode_pref();   // host: JTFS_BWD_MODE (default 0)
 // backward B ring sizing shared by the planner (chooses kb2) and the launcher (kernels_tc.cu)
 void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2, int* STG2);
 int tc_fwd_stages(int CT, int KAP, int K2, int kcw);
@@ -153,6 +157,9 @@ struct Plan {
   std::vector<char> blk_tc;                     // [n_blocks] 1 = forward on the tensor-core path
   std::vector<char> blk_tcb;                    // [n_blocks] 1 = backward on the tensor-core path
   std::vector<double> block_cost;               // [n_blocks] path-shard LPT cost (planner.cpp)
+  // phi_T banded-GEMM adjoint (kernels_fr.cu k_phiT_adj3) over the halo-pruned blocks
+  std::vector<int32_t> ph3_groups, ph3_rows, ph3_atiles;
+  uint64_t ph3_mask = 0;
   double order1_cost = 0.0;
   std::vector<char> blk_ks;                     // [n_blocks] 1 = split-K tensor-core block
   std::vector<TcBlock> tcb_blocks;              // backward-eligible blocks (cls = KAP class)

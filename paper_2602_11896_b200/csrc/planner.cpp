@@ -440,7 +440,12 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
   p->Ft = p->N_pad / T;
   for (int i = 0; i + 1 < N1; ++i)
     if (p->psi1[i].j > p->psi1[i + 1].j) { *err = "internal: j1 not nondecreasing"; return 1; }
-  if (ceil_div(N1, F) > 32) { *err = "ceil(N1/F) must be <= 32 (GPU kernel limit)"; return 1; }
+  // kept rows per path: up to 32 on the tensor-core / CUDA-core joint kernels; up to 64 on the FFT route of
+  // the joint stage (kernels_frfft.cu, P <= 1024), which route_of picks for blocks beyond 32 rows
+  if (ceil_div(N1, F) > 64 || (ceil_div(N1, F) > 32 && p->P > 1024)) {
+    *err = "ceil(N1/F) must be <= 32, or <= 64 with P <= 1024 (GPU kernel limit)";
+    return 1;
+  }
   for (int n2 = 0; n2 < (int)p->psi2.size(); ++n2) {
     int j2 = p->psi2[n2].j, n1_max = 0;
     for (auto& f : p->psi1) n1_max += (j2 > f.j);
@@ -640,6 +645,35 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     }
   }
   p->o_size = ooff;
+  // phi_T adjoint as banded GEMMs over the halo-pruned (unwrapped) blocks: 32-row groups of (unit, rho)
+  // rows, 256-column tiles (kernels_fr.cu k_phiT_adj3)
+  {
+    const int nfr_all = (int)p->L_fr.size();
+    for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
+      const BlockInfo& bf = p->binfo[bi];
+      if (bf.n_cols >= bf.T2) continue;               // whole circle: per-row kernels (k_phiT_fwd2/adj2)
+      p->ph3_mask |= 1ull << bi;
+      std::vector<int32_t> rows;
+      for (int f = 0; f < nfr_all; ++f) {
+        const int u = (int)bi * nfr_all + f;
+        for (int rho = 0; rho < p->units[u].rows_out; ++rho) { rows.push_back(u); rows.push_back(rho); }
+      }
+      const int nrows = (int)(rows.size() / 2);
+      for (int r0 = 0; r0 < nrows; r0 += 32) {
+        const int gi = (int)(p->ph3_groups.size() / 8);
+        const int first = (int)(p->ph3_rows.size() / 2);
+        for (int r = r0; r < std::min(nrows, r0 + 32); ++r) {
+          p->ph3_rows.push_back(rows[2 * r]);
+          p->ph3_rows.push_back(rows[2 * r + 1]);
+        }
+        p->ph3_groups.insert(p->ph3_groups.end(), {first, std::min(32, nrows - r0), (int32_t)bi, 0, 0, 0, 0, 0});
+        for (int64_t t = 0; t < (bf.n_cols + 255) / 256; ++t) {
+          p->ph3_atiles.push_back(gi);
+          p->ph3_atiles.push_back((int32_t)t);
+        }
+      }
+    }
+  }
   // path-shard cost model (LPT, jtfs_api.cu block_owner): per block, the joint stage's contraction flops
   // (8 K forward + 16 K backward per modulus cell) plus its time-axis FFTs (5 L log2 L forward and
   // backward per Y2 row); order 1 (shard 0) as its row sums over the needed frames

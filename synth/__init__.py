@@ -36,6 +36,7 @@ VARIANTS = {
     "q2": dict(N=1024, J=5, Q=2, J_fr=3, Q_fr=1, T=8, F=2, Q2=2),
     "q2b": dict(N=4096, J=6, Q=8, J_fr=3, Q_fr=1, T=64, F=8, Q2=4),
     "j2gtT": dict(N=2048, J=6, Q=4, J_fr=2, Q_fr=1, T=8, F=2),
+    "wide": dict(N=4096, J=6, Q=8, J_fr=3, Q_fr=1, T=64, F=1),     # ceil(N1/F) = 38 > 32 rows per path
 }
 
 _CINDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}

@@ -56,7 +56,7 @@ def test_stage_U1_S1t_Y2(plans, name):
         assert rel(g3, Y2) <= 1e-5
 
 
-@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1", "q2", "q2b", "j2gtT"])
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1", "q2", "q2b", "j2gtT", "wide"])
 def test_forward_parity(plans, name):
     p = plans(name)
     o = Oracle(plan_args(ALL[name]))
@@ -70,7 +70,7 @@ def test_forward_parity(plans, name):
         assert rel(S[:, sl], So[:, sl]) <= 1e-3, q
 
 
-@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1", "q2", "q2b", "j2gtT"])
+@pytest.mark.parametrize("name", ["t1", "t2", "spec", "c1", "q2", "q2b", "j2gtT", "wide"])
 def test_loss_grad_parity(plans, name):
     p = plans(name)
     o = Oracle(plan_args(ALL[name]))
