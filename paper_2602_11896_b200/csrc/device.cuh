@@ -108,9 +108,22 @@ void launch_gather(const float2* in, int64_t in_sb, float2* out, int64_t out_sb,
 void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t out_sb, const GatherJob* jobs,
                       const int64_t* tiles, int njobs, int64_t ntiles, const double* vals, int B, cudaStream_t st);
 void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
-                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st);
-void launch_modulus(const float2* z, int64_t zsb, double2* u, int64_t usb, int64_t n_per_b, int B,
-                    cudaStream_t st);
+                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st,
+                      uint64_t own = kOwnAll);
+// level groups of the layer-1 rows for the pair-packed U1 FFT (<= kMaxPackGroups distinct lengths)
+constexpr int kMaxPackGroups = 24;
+struct PackGroups {
+  int64_t off[kMaxPackGroups];          // first row element of the group (natural layout)
+  int64_t pstart[kMaxPackGroups + 1];   // packed (compact) offset of each group = Plan::l1_pgroups[g].off
+  int count[kMaxPackGroups];            // rows of the group
+  int lgL[kMaxPackGroups];              // log2 row length
+  int n;
+};
+PackGroups pack_groups(const Plan& p);
+void launch_modulus_pack(const float2* z, int64_t zsb, double2* u, int64_t usb, const PackGroups& G, int B,
+                         cudaStream_t st);
+void launch_unpack_u1(const double2* u, int64_t usb, float* out, int64_t out_sb, const PackGroups& G, int64_t n,
+                      int B, cudaStream_t st);
 void launch_real_rows_d(const double2* in, int64_t in_sb, float* out, int64_t out_sb, int64_t n, int B,
                         cudaStream_t st);
 void launch_real_rows(const float2* in, int64_t in_sb, int64_t in_off, float* out, int64_t out_sb,

@@ -63,7 +63,7 @@ struct StRows {  // last pass writes global rows, scaled
 };
 
 template <class TI, class TO, class C>
-__global__ void __launch_bounds__(256) k_fft_small(const TI* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 2 : 1) k_fft_small(const TI* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
                                                    int lgL, int lgM, int inv, double scale,
                                                    const C* __restrict__ tw) {
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -92,7 +92,7 @@ struct FftJobs {
   int n;
 };
 template <class TI, class TO, class C>
-__global__ void __launch_bounds__(256) k_fft_small_multi(const TI* __restrict__ in, TO* __restrict__ out,
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 2 : 1) k_fft_small_multi(const TI* __restrict__ in, TO* __restrict__ out,
                                                          int64_t in_sb, int64_t out_sb, FftJobs J, int inv,
                                                          const C* __restrict__ tw) {
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -345,6 +345,11 @@ cudaError_t fft_groups(const float2* in, float2* out, int64_t in_sb, int64_t out
 cudaError_t fft_groups_df(const double2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
                           int B, bool inverse, const FftTables& T, cudaStream_t st) {
   return fft_groups_t<double2, float2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
+}
+
+cudaError_t fft_groups_dd(const double2* in, double2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                          int B, bool inverse, const FftTables& T, cudaStream_t st) {
+  return fft_groups_t<double2, double2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
 }
 
 cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,

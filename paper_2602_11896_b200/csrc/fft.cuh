@@ -34,6 +34,8 @@ cudaError_t fft_launch_df(const double2* in, float2* out, Rows ri, Rows ro, int 
 struct FftGroup;
 cudaError_t fft_groups(const float2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
                        int B, bool inverse, const FftTables& T, cudaStream_t st);
+cudaError_t fft_groups_dd(const double2* in, double2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
+                          int B, bool inverse, const FftTables& T, cudaStream_t st);
 cudaError_t fft_groups_df(const double2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
                           int B, bool inverse, const FftTables& T, cudaStream_t st);
 std::vector<float2> fft_twiddle_table();

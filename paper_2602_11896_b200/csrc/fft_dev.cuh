@@ -3,6 +3,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#ifndef JTFS_CF_INLINE
+#define JTFS_CF_INLINE __noinline__
+#endif
+
 namespace jtfs {
 
 constexpr int kTw = 4096;  // twiddle table length
@@ -193,7 +197,7 @@ using CfSmem = SeqCol<float2>;
 // 2^lgT >= L; lgT = -1: the per-pass table of length L (fft.cuh fft_pass_tables). All loads happen before the barrier and all stores after it (in place when ld and st address
 // the same buffer). CFAST: consecutive threads take consecutive sequences.
 template <class Cp, int R, int NT, int NPT, bool CFAST, class LD, class ST>
-__device__ __noinline__ void cf_pass(int lgC, int lgL, int lgNs, bool inv, const Cp* tws, int lgT, LD ld, ST st) {
+__device__ JTFS_CF_INLINE void cf_pass(int lgC, int lgL, int lgNs, bool inv, const Cp* tws, int lgT, LD ld, ST st) {
   using RT = typename Cx<Cp>::R;
   constexpr int lgR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
   constexpr int NB = NPT / R > 0 ? NPT / R : 1;                      // butterflies per thread

@@ -428,7 +428,10 @@ static Layout layout(const Plan& p, int with_grad) {
   // A holds the complex128 layer-1 spectra (sum L1) or complex64 (sum Y2, sum L1)
   L.xp = al(p.N_pad * 16); L.Xh = al(p.N_pad * 16);
   L.A = al(std::max(2 * p.sumL1, p.sumY2) * 8);
-  L.Z1 = al(p.sumL1 * 8); L.U1h = al(p.sumL1 * 8); L.Y2 = al(std::max<int64_t>(p.sumY2, 1) * 8);
+  // Z1 and U1_hat share a stride; U1_hat holds the pair-packed float64 spectra (u1p_size complex128) in the
+  // forward and g_hat_U1 (sum L1 complex64) in the backward
+  L.Z1 = al(std::max(p.sumL1 * 8, p.u1p_size * 16)); L.U1h = L.Z1;
+  L.Y2 = al(std::max<int64_t>(p.sumY2, 1) * 8);
   L.cs = al((1 + N1) * p.Ft * 8); L.ct = L.cs;
   L.S1t = al(N1 * p.Ft * 4);
   L.W1 = al(nfr1 * p.P * p.Ft * 8);
@@ -478,6 +481,24 @@ static cudaError_t fft_rows(const Plan& p, const float2* in, int64_t in_sb, floa
   return fft_launch(in, out, ri, ro, B, inv, p.dev->fftt, st);
 }
 
+PackGroups jtfs::pack_groups(const Plan& p) {
+  PackGroups G{};
+  G.n = (int)p.l1_groups.size();
+  int64_t acc = 0;
+  for (int g = 0; g < G.n; ++g) {
+    const FftGroup& q = p.l1_groups[g];
+    G.off[g] = q.off;
+    G.count[g] = (int)q.count;
+    int lg = 0;
+    while ((int64_t(1) << lg) < q.L) ++lg;
+    G.lgL[g] = lg;
+    G.pstart[g] = acc;
+    acc += ((q.count + 1) / 2) * q.L;
+  }
+  G.pstart[G.n] = acc;
+  return G;
+}
+
 // Y2 row groups (one per second-order block) of the blocks a path shard owns
 static std::vector<FftGroup> own_groups(const Plan& p, uint64_t own) {
   std::vector<FftGroup> g;
@@ -508,16 +529,20 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals_d, mb, st);
   if ((e = fft_groups_df(Ad, w.Z1, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt, st)))
     return e;
-  launch_modulus(w.Z1, w.s_L1, Ad, sAd, p.sumL1, mb, st);  // A rows (complex128) use the L1 layout
+  const PackGroups pg = pack_groups(p);
+  launch_modulus_pack(w.Z1, w.s_L1, Ad, sAd, pg, mb, st);   // A: pair-packed complex128 rows (L1 layout)
   RET();
   if (stop == 1) return cudaSuccess;
-  // U1_hat = FFT(U1) in float64, rounded to complex64 per bin (R22 precision)
-  if ((e = fft_groups_df(Ad, w.U1h, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, false, d.fftt,
+  // U1_hat = FFT(U1) in float64, two real rows per complex FFT (pair packing), kept in float64 (the gathers
+  // unpack the two spectra, so a row's bins must not carry its partner's rounding: DESIGN.md R22 precision)
+  double2* U1hd = reinterpret_cast<double2*>(w.U1h);
+  const int64_t sU1d = w.s_L1 / 2;
+  if ((e = fft_groups_dd(Ad, U1hd, sAd, sU1d, p.l1_pgroups.data(), (int)p.l1_pgroups.size(), mb, false, d.fftt,
                          st)))
     return e;
   // S0 and S1 time averages (Eq.3 time part)
   launch_gather_df(Xhd, sd, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
-  launch_gather(w.U1h, w.s_L1, w.cs + p.Ft, w.s_c, d.s1_jobs, d.s1_tiles, d.n_s1, d.s1_ntiles, d.spec_vals, mb, st);
+  launch_gather_df(U1hd, sU1d, w.cs + p.Ft, w.s_c, d.s1_jobs, d.s1_tiles, d.n_s1, d.s1_ntiles, d.spec_vals, mb, st);
   if ((e = fft_rows(p, w.cs, w.s_c, w.ct, w.s_c, 0, 1 + (int64_t)p.psi1.size(), p.Ft, mb, true, st))) return e;
   launch_s0_out(w.ct, w.s_c, S, S_sb, p, mb, st);
   launch_real_rows(w.ct, w.s_c, p.Ft, w.S1t, w.s_S1t, 0, (int64_t)p.psi1.size() * p.Ft, mb, st);
@@ -528,7 +553,7 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   // A4: layer 2, width-first
   if (!p.blocks.empty()) {
     // path shards compute only their own blocks' Y2 (layer 1 is the only replicated stage)
-    launch_gather(w.U1h, w.s_L1, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st, own);
+    launch_gather_df(U1hd, sU1d, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st, own);
     const std::vector<FftGroup> g2 = own_groups(p, own);
     if (!g2.empty() &&
         (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, true, d.fftt, st)))
@@ -1048,7 +1073,8 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
   if (stage == 1) {
     if (out_bytes < (size_t)B * p.sumL1 * 4) return fail(JTFS_ERR_SIZE, "out too small");
     CK(run_forward(p, x, p.N, n, w.S, w.s_S, w, kOwnAll, st, 1));
-    launch_real_rows_d(reinterpret_cast<const double2*>(w.A), w.s_A / 2, (float*)out, p.sumL1, p.sumL1, n, st);
+    launch_unpack_u1(reinterpret_cast<const double2*>(w.A), w.s_A / 2, (float*)out, p.sumL1, pack_groups(p), p.sumL1,
+                     n, st);
   } else if (stage == 2) {
     int64_t per = (int64_t)p.psi1.size() * p.Ft;
     if (out_bytes < (size_t)B * per * 4) return fail(JTFS_ERR_SIZE, "out too small");

@@ -66,11 +66,18 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
     // L_in, L_out: powers of two (grid lengths N_pad >> k)
     int64_t s = J.lo + ((m - J.lo) & (J.L_out - 1));          // smallest s >= lo with s = m mod L_out
     R ax = 0, ay = 0;
+    const int64_t msk = J.L_in - 1;
     for (; s < J.lo + J.len; s += J.L_out) {
       const R h = (R)__ldg(vals + J.val_off + (s - J.lo));
-      const TI v = src[s & (J.L_in - 1)];
-      ax += h * (R)v.x;
-      ay += h * (R)v.y;
+      const TI z = src[s & msk];
+      R vx = (R)z.x, vy = (R)z.y;
+      if (J.par >= 0) {   // pair-packed real rows (plan.h GatherJob::par)
+        const TI w = src[(-s) & msk];
+        if (J.par == 0) { vx = (R)0.5 * ((R)z.x + (R)w.x); vy = (R)0.5 * ((R)z.y - (R)w.y); }
+        else { vx = (R)0.5 * ((R)z.y + (R)w.y); vy = (R)0.5 * ((R)w.x - (R)z.x); }
+      }
+      ax += h * vx;
+      ay += h * vy;
     }
     st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
   }
@@ -95,25 +102,57 @@ void launch_gather_dd(const double2* in, int64_t in_sb, double2* out, int64_t ou
   gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
 }
 void launch_gather_df(const double2* in, int64_t in_sb, float2* out, int64_t out_sb, const GatherJob* jobs,
-                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st) {
-  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st);
+                      const int64_t* tiles, int njobs, int64_t ntiles, const float* vals, int B, cudaStream_t st,
+                      uint64_t own) {
+  gather_t(in, in_sb, out, out_sb, jobs, tiles, njobs, ntiles, vals, B, st, own);
 }
 
-// U1 = |Z1|, stored as a float64 complex row with zero imaginary part for the next FFT
-// (P:211), which runs in float64: the FFT's rounding is relative to the whole row (dominated by the
-// envelope's mean), and the second-layer bands it feeds are far below that (reading R22).
-__global__ void k_modulus(const float2* __restrict__ z, int64_t zsb, double2* __restrict__ u, int64_t usb,
-                          int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// U1 = |Z1| as float64 rows for the next FFT, which runs in float64: the FFT's rounding is
+// relative to the whole row (dominated by the envelope's mean), and the second-layer bands it feeds are far
+// below that (reading R22). The rows are real, so two of a level group share one complex FFT
+// (pair packing, the R2C trick): packed row p of group g = U1[2p] + i U1[2p + 1] (imaginary 0 for an odd
+// last row); the gathers unpack the two spectra (GatherJob::par).
+__global__ void k_modulus_pack(const float2* __restrict__ z, int64_t zsb, double2* __restrict__ u, int64_t usb,
+                               PackGroups G) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= G.pstart[G.n]) return;
+  int g = 0;
+  while (g + 1 < G.n && q >= G.pstart[g + 1]) ++g;
+  const int64_t loc = q - G.pstart[g];
+  const int lgL = G.lgL[g];
+  const int64_t p = loc >> lgL, e = loc & ((int64_t(1) << lgL) - 1);
+  const float2* zr = z + blockIdx.y * zsb + G.off[g] + ((2 * p) << lgL) + e;
+  const float2 va = zr[0];
+  const float2 vb = (2 * p + 1 < G.count[g]) ? zr[int64_t(1) << lgL] : make_float2(0.f, 0.f);
+  u[blockIdx.y * usb + q] =   // compact packed layout: element q
+      make_double2((double)sqrtf(va.x * va.x + va.y * va.y), (double)sqrtf(vb.x * vb.x + vb.y * vb.y));
+}
+
+void launch_modulus_pack(const float2* z, int64_t zsb, double2* u, int64_t usb, const PackGroups& G, int B,
+                         cudaStream_t st) {
+  const int64_t n = G.pstart[G.n];
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
+  k_modulus_pack<<<g, 256, 0, st>>>(z, zsb, u, usb, G);
+  count_launch();
+}
+
+// debug stage U1: unpack the pair-packed float64 rows -> fp32 [sum L1] in the natural row layout
+__global__ void k_unpack_u1(const double2* __restrict__ u, int64_t usb, float* __restrict__ out, int64_t out_sb,
+                            PackGroups G, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  float2 v = z[blockIdx.y * zsb + i];
-  u[blockIdx.y * usb + i] = make_double2((double)sqrtf(v.x * v.x + v.y * v.y), 0.0);
+  int g = 0;
+  while (g + 1 < G.n && i >= G.off[g + 1]) ++g;
+  const int lgL = G.lgL[g];
+  const int64_t r = (i - G.off[g]) >> lgL, e = (i - G.off[g]) & ((int64_t(1) << lgL) - 1);
+  const double2 v = u[blockIdx.y * usb + G.pstart[g] + ((r >> 1) << lgL) + e];
+  out[blockIdx.y * out_sb + i] = (float)((r & 1) ? v.y : v.x);
 }
 
-void launch_modulus(const float2* z, int64_t zsb, double2* u, int64_t usb, int64_t n_per_b, int B,
-                    cudaStream_t st) {
-  dim3 g((unsigned)((n_per_b + 255) / 256), (unsigned)B);
-  k_modulus<<<g, 256, 0, st>>>(z, zsb, u, usb, n_per_b);
+void launch_unpack_u1(const double2* u, int64_t usb, float* out, int64_t out_sb, const PackGroups& G, int64_t n,
+                      int B, cudaStream_t st) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
+  k_unpack_u1<<<g, 256, 0, st>>>(u, usb, out, out_sb, G, n);
   count_launch();
 }
 

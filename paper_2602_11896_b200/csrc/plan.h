@@ -32,6 +32,10 @@ struct GatherJob {
   int64_t in_off, L_in, lo, len, val_off, out_off, L_out;
   float scale;
   int32_t blk;   // second-order block of a layer-2 job (path shards skip unowned blocks), -1 otherwise
+  int32_t par;   // -1: plain complex row; 0 / 1: the row is the real / imaginary half of a pair-packed row
+                 // whose FFT carries two real rows (Z = U_a + i U_b): U_a^[s] = (Z[s] + conj Z[-s]) / 2,
+                 // U_b^[s] = (Z[s] - conj Z[-s]) / 2i
+  int32_t pad_;
 };
 
 // Batched FFT group: `count` rows of length L starting at `off` (per signal).
@@ -133,6 +137,9 @@ struct Plan {
   std::vector<BlockInfo> binfo;
   std::vector<JointUnit> units;        // order-2 (block, filter) units in path order
   std::vector<FftGroup> l1_groups, y2_groups;
+  std::vector<FftGroup> l1_pgroups;             // pair-packed U1 rows: ceil(count / 2) rows per level (R2C pairs),
+                                                // compact offsets (complex128 elements)
+  int64_t u1p_size = 0;                         // complex128 elements of the packed U1 / U1_hat rows
   std::vector<GatherJob> l1_jobs, s1_jobs, l2_jobs;
   GatherJob s0_job{};
   // order-1 unit rows (per f in xi >= 0 prefix)

@@ -482,6 +482,10 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     int n = n1;
     while (n < N1 && p->L1[n] == p->L1[n1]) ++n;
     p->l1_groups.push_back({p->L1_off[n1], n - n1, p->L1[n1]});
+    // pair-packed U1 rows, compact: group after group, ceil(count / 2) rows of L (complex128 elements)
+    p->l1_pgroups.push_back({p->u1p_size, (n - n1 + 1) / 2, p->L1[n1]});
+    p->u1p_size += (int64_t)((n - n1 + 1) / 2) * p->L1[n1];
+    if (p->l1_groups.size() > 24) { *err = "more than 24 first-layer levels"; return 1; }   // PackGroups
     n1 = n;
   }
 
@@ -525,17 +529,30 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     auto& sp = p->psi1_sup_d[n1];
     int k1 = std::min(p->psi1[n1].j, log2T);
     p->l1_jobs.push_back({0, p->N_pad, sp.lo, sp.len, sp.off, p->L1_off[n1], p->L1[n1],
-                          (float)std::ldexp(1.0, -k1), -1});
+                          (float)std::ldexp(1.0, -k1), -1, -1, 0});
   }
   {
     auto& sp = p->phiT_sup[0];
-    p->s0_job = {0, p->N_pad, sp.lo, sp.len, sp.off, 0, p->Ft, (float)std::ldexp(1.0, -log2T), -1};
+    p->s0_job = {0, p->N_pad, sp.lo, sp.len, sp.off, 0, p->Ft, (float)std::ldexp(1.0, -log2T), -1, -1, 0};
+  }
+  // U1_hat rows are pair-packed (l1_pgroups): row n1 of a level group lives in packed row (n1 - first) / 2
+  // of the group, parity (n1 - first) & 1
+  std::vector<int64_t> u1_in(N1);
+  std::vector<int32_t> u1_par(N1);
+  for (size_t gi = 0; gi < p->l1_groups.size(); ++gi) {
+    const FftGroup& g = p->l1_groups[gi];
+    for (int64_t r = 0; r < g.count; ++r) {
+      int n1 = -1;
+      for (int q = 0; q < N1; ++q) if (p->L1_off[q] == g.off + r * g.L) n1 = q;
+      u1_in[n1] = p->l1_pgroups[gi].off + (r / 2) * g.L;   // complex128 elements of the packed spectra
+      u1_par[n1] = (int32_t)(r & 1);
+    }
   }
   for (int n1 = 0; n1 < N1; ++n1) {
     int k1 = std::min(p->psi1[n1].j, log2T);
     auto& sp = p->phiT_sup[k1];
-    p->s1_jobs.push_back({p->L1_off[n1], p->L1[n1], sp.lo, sp.len, sp.off, (int64_t)n1 * p->Ft, p->Ft,
-                          (float)std::ldexp(1.0, -(log2T - k1)), -1});
+    p->s1_jobs.push_back({u1_in[n1], p->L1[n1], sp.lo, sp.len, sp.off, (int64_t)n1 * p->Ft, p->Ft,
+                          (float)std::ldexp(1.0, -(log2T - k1)), -1, u1_par[n1], 0});
   }
   int64_t yoff = 0;
   for (size_t bi = 0; bi < p->blocks.size(); ++bi) {
@@ -545,8 +562,8 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
     for (int n1 = 0; n1 < b.n1_max; ++n1) {
       int k1 = std::min(p->psi1[n1].j, log2T);
       auto& sp = p->psi2_sup[bi * (log2T + 1) + k1];
-      p->l2_jobs.push_back({p->L1_off[n1], p->L1[n1], sp.lo, sp.len, sp.off, yoff + n1 * bf.T2, bf.T2,
-                            (float)std::ldexp(1.0, -(b.s2 - k1)), (int32_t)bi});
+      p->l2_jobs.push_back({u1_in[n1], p->L1[n1], sp.lo, sp.len, sp.off, yoff + n1 * bf.T2, bf.T2,
+                            (float)std::ldexp(1.0, -(b.s2 - k1)), (int32_t)bi, u1_par[n1], 0});
     }
     p->y2_groups.push_back({yoff, b.n1_max, bf.T2});
     yoff += (int64_t)b.n1_max * bf.T2;
