@@ -4,10 +4,11 @@ An independent O(L^2) implementation of the multirate forward (SURVEY.md §8(c) 
 Fourier product replaced by the mathematically identical direct circular sum with the
 closed-form (Poisson-summed) kernel `plan.time_kernel_closed_form` (O1):
     (D_s C_h u)[n] = sum_m u[m] h[(n s - m) mod L]
-It recomputes every path depth-first (one (n1, n2, n_fr) at a time, no stacking), so agreement
-with oracle/jtfs.py pins: the FFT route, subsample_fourier as decimation, the level
+It recomputes every path depth-first (one (n1, n2, n_fr) at a time, no stacking), and its gradient
+(`loss_grad`) reverses it with explicit adjoints (no autodiff), so agreement with oracle/jtfs.py pins: the FFT route, subsample_fourier as decimation, the level
 (fold-sum) convention R9, the width-first stacking, zero-padding to P, the
-spin order R12 and the packing R15. Only usable on tiny configurations (N_pad <= 4096).
+spin order R12 and the packing R15. Direct sums over each closed-form kernel's taps (|h| > 1e-18 of its peak): usable up to c1
+(N_pad = 8192).
 """
 from __future__ import annotations
 
@@ -16,13 +17,24 @@ import numpy as np
 from .plan import Plan, time_kernel_closed_form
 
 
-def _circ(h: np.ndarray, u: np.ndarray, s: int) -> np.ndarray:
-    """(D_s C_h u)[n] = sum_m u[m] h[(n s - m) mod L] along the last axis of u (direct sum)."""
+def _support(h: np.ndarray) -> np.ndarray:
+    """Taps j (as offsets in (-L/2, L/2]) where the closed-form kernel exceeds 1e-18 of its peak: the
+    direct sums skip the rest (their total weight is below the float64 rounding of the sum)."""
     L = h.shape[0]
-    n = np.arange(L // s)[:, None] * s
-    m = np.arange(L)[None, :]
-    M = h[(n - m) % L]                     # [L/s, L]
-    return u @ M.T
+    a = np.abs(h)
+    j = np.nonzero(a > 1e-18 * a.max())[0] if a.max() > 0 else np.zeros(0, np.int64)
+    return np.where(j > L // 2, j - L, j)
+
+
+def _circ(h: np.ndarray, u: np.ndarray, s: int) -> np.ndarray:
+    """(D_s C_h u)[n] = sum_m u[m] h[(n s - m) mod L] along the last axis of u (direct sum):
+    = sum over the kernel's taps j of h[j] u[(n s - j) mod L], one shifted gather per tap."""
+    L = h.shape[0]
+    n = np.arange(L // s) * s
+    out = np.zeros(u.shape[:-1] + (L // s,), dtype=np.result_type(u, h))
+    for j in _support(h):
+        out += h[j % L] * u[..., (n - j) % L]
+    return out
 
 
 def _circ_rows(h: np.ndarray, X: np.ndarray, s: int) -> np.ndarray:
@@ -40,10 +52,11 @@ def _reflect(plan: Plan, x: np.ndarray) -> np.ndarray:
     return out
 
 
-def forward(plan: Plan, x: np.ndarray) -> np.ndarray:
-    """Packed coefficients of one signal (float64) by direct sums, depth-first."""
+def forward(plan: Plan, x: np.ndarray, blocks=None) -> np.ndarray:
+    """Packed coefficients of one signal (float64) by direct sums, depth-first (`blocks`: only those
+    second-order blocks, the others left 0, as Oracle.forward)."""
     p = plan
-    assert p.N_pad <= 4096, "brute force is for tiny configurations only"
+    assert p.N_pad <= 8192, "brute force is for tiny configurations and c1 only"
     xp = _reflect(p, np.asarray(x, dtype=np.float64))
     f0, nfr = p.pad_left // p.T, p.frames
     hT = lambda k: time_kernel_closed_form(p.phiT, p.N_pad, k)
@@ -73,8 +86,11 @@ def forward(plan: Plan, x: np.ndarray) -> np.ndarray:
             Y = _circ_rows(hF(kf), V, 2 ** (p.log2F - kf)).real
         out.append(Y[:rows1, f0:f0 + nfr].ravel())
 
-    for blk in p.blocks:
+    for bi, blk in enumerate(p.blocks):
         rows2 = -(-blk.n1_max // p.F)
+        if blocks is not None and bi not in blocks:
+            out += [np.zeros(rows2 * nfr)] * len(p.L_fr)
+            continue
         for f in range(len(p.L_fr)):
             kf = p.k_fr(f)
             # depth-first: build the column stack one n1 at a time (no width-first stacking op)
@@ -99,13 +115,15 @@ def forward(plan: Plan, x: np.ndarray) -> np.ndarray:
 # ----------------------------------------------------------------------------------------------
 
 def _circ_adj(h: np.ndarray, g: np.ndarray, s: int) -> np.ndarray:
-    """Adjoint of u -> _circ(h, u, s) along the last axis: the conjugate transpose of the same
-    [L/s, L] matrix, A^H g (no use of the Hermitian-kernel shortcut R21)."""
+    """Adjoint of u -> _circ(h, u, s) along the last axis: the conjugate transpose of the same matrix,
+    (A^H g)[m] = sum_n conj(h[(n s - m) mod L]) g[n] (no use of the Hermitian-kernel shortcut R21); per tap
+    j the targets m = (n s - j) mod L are distinct, so each tap is one scatter-add."""
     L = h.shape[0]
-    n = np.arange(L // s)[:, None] * s
-    m = np.arange(L)[None, :]
-    M = h[(n - m) % L]
-    return g @ M.conj()
+    n = np.arange(L // s) * s
+    out = np.zeros(g.shape[:-1] + (L,), dtype=np.result_type(g, h))
+    for j in _support(h):
+        out[..., (n - j) % L] += np.conj(h[j % L]) * g
+    return out
 
 
 def _circ_rows_adj(h: np.ndarray, G: np.ndarray, s: int) -> np.ndarray:
@@ -133,14 +151,19 @@ def _phase(z: np.ndarray, thr: float) -> np.ndarray:
     return np.where(keep, z.real / d + 1j * (z.imag / d), 0.0)
 
 
-def loss_grad(plan: Plan, y: np.ndarray, S_target: np.ndarray) -> tuple[float, np.ndarray]:
+def loss_grad(plan: Plan, y: np.ndarray, S_target: np.ndarray, blocks=None) -> tuple[float, np.ndarray]:
     """E = 1/2 sum_{orders 1,2} (S(y) - S_target)^2 (R19) and dE/dy for one signal, by reversing
-    `forward` stage by stage with the explicit adjoints above (modulus: g_z = (z/|z|) g_v)."""
+    `forward` stage by stage with the explicit adjoints above (modulus: g_z = (z/|z|) g_v).
+    `blocks` restricts the loss to order 1 and those second-order blocks (as Oracle.loss_grad_subset)."""
     p = plan
-    assert p.N_pad <= 4096, "brute force is for tiny configurations only"
-    S = forward(p, y)
+    assert p.N_pad <= 8192, "brute force is for tiny configurations and c1 only"
+    S = forward(p, y, blocks)
     r = S - np.asarray(S_target, dtype=np.float64)
     r[: p.frames] = 0.0                                                  # S0 not in the loss
+    if blocks is not None:
+        for q in p.paths:
+            if q.order == 2 and q.block not in blocks:
+                r[q.offset:q.offset + q.rows * q.frames] = 0.0
     E = 0.5 * float(r @ r)
     y = np.asarray(y, dtype=np.float64)
     thr = max(EPS_MOD * float(np.sqrt(np.mean(y * y))), np.finfo(np.float64).tiny)
@@ -184,8 +207,11 @@ def loss_grad(plan: Plan, y: np.ndarray, S_target: np.ndarray) -> tuple[float, n
         g_U1[n1] += _circ_adj(hT(k1), gS1t[n1], 2 ** (p.log2T - k1)).real
 
     # order 2, depth-first per (block, filter)
-    for blk in p.blocks:
+    for bi, blk in enumerate(p.blocks):
         rows2 = -(-blk.n1_max // p.F)
+        if blocks is not None and bi not in blocks:
+            off += len(p.L_fr) * rows2 * nfr
+            continue
         T2 = p.N_pad >> blk.s2
         h2 = [time_kernel_closed_form(p.psi2[blk.n2], p.N_pad, p.k1(n1)) for n1 in range(blk.n1_max)]
         X = np.zeros((p.P, T2), dtype=np.complex128)

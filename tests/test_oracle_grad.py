@@ -177,3 +177,22 @@ def test_metamer_quadratic_toy_converges():
         E = 0.5 * ((st["y"] - c) ** 2).sum(1)
         st = metamer.step(st, E, st["y"] - c)
     assert np.abs(st["y"] - c).max() < 1e-6
+
+
+def test_c1_direct_sums_equal_fft_autograd():
+    # BASELINE configs[0] (c1) by the independent route: direct sums over the closed-form kernels' taps
+    # and explicit adjoints (oracle/brute.py, no FFT, no autodiff) vs the FFT + autograd oracle, on the
+    # c1 music input; the loss restricted to order 1 + block 0 bounds the time (~30 s)
+    from synth import batch
+    p = make_plan(*plan_args(CONFIGS["c1"]))
+    o = Oracle(p)
+    x = batch("c1", 1).astype(np.float64)
+    y = batch("c1", 1, which="y").astype(np.float64)
+    St = o.forward(x)
+    Sb = brute.forward(p, x[0], blocks=[0])
+    So = o.forward(x, blocks=[0])[0].numpy()
+    assert np.linalg.norm(Sb - So) <= 1e-12 * np.linalg.norm(So)
+    Eb, gb = brute.loss_grad(p, y[0], St[0].numpy(), blocks=[0])
+    E, g = o.loss_grad_subset(y, St, [0])
+    assert abs(Eb - float(E[0])) <= 1e-12 * float(E[0])
+    assert np.linalg.norm(gb - g[0].numpy()) <= 1e-10 * np.linalg.norm(gb)
