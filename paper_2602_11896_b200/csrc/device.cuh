@@ -124,6 +124,8 @@ void launch_modulus_pack(const float2* z, int64_t zsb, double2* u, int64_t usb, 
                          cudaStream_t st);
 void launch_unpack_u1(const double2* u, int64_t usb, float* out, int64_t out_sb, const PackGroups& G, int64_t n,
                       int B, cudaStream_t st);
+void launch_untranspose_rows(const float2* z, int64_t zsb, float2* out, int64_t out_sb, const PackGroups& G,
+                             int64_t n, int B, cudaStream_t st);
 void launch_real_rows_d(const double2* in, int64_t in_sb, float* out, int64_t out_sb, int64_t n, int B,
                         cudaStream_t st);
 void launch_real_rows(const float2* in, int64_t in_sb, int64_t in_off, float* out, int64_t out_sb,

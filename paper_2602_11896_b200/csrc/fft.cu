@@ -186,6 +186,77 @@ __global__ void __launch_bounds__(NT) k_fft_rowB(const C* __restrict__ in, TO* _
   }
 }
 
+// ---------------------------------------------------------------- "T-layout" passes (no transposition)
+// A four-step transform whose rows are stored in place keeps every global access row-contiguous: the
+// natural -> T pair (k_fft_colA, then k_fft_rowT without twiddle) leaves X[k1 + L1 k2] at position
+// k1 L2 + k2, and the T -> natural pair (k_fft_rowT with the twiddle W_L^{k1 n2} on its store, then
+// k_fft_colT) takes a row-major T-layout input back to natural order. Chains whose consumers are
+// elementwise (Z1 -> |Z1| -> U1 FFT; g_U1 -> phase -> g_Z1 FFT) run in T-layout in between.
+template <class C, class TO, int NPT, int NT>
+__global__ void __launch_bounds__(NT) k_fft_rowT(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
+                                                  int lgL1, int lgM, int inv, double scale, const C* __restrict__ tw,
+                                                  const C* __restrict__ lo, const C* __restrict__ hi) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  constexpr int lgL2 = 12, L2 = 4096;
+  C* s = reinterpret_cast<C*>(smraw);                 // [M][L2] swizzled
+  C* tws = s + (L2 << lgM);                           // [L2]
+  const int64_t r = blockIdx.y;
+  const int b = blockIdx.z;
+  const int64_t L = (int64_t)L2 << lgL1;
+  const int M = 1 << lgM;
+  const int k10 = blockIdx.x * M;
+  const C* src = in + b * ri.stride_b + ri.off + r * L + (int64_t)k10 * L2;
+  TO* dst = out + b * ro.stride_b + ro.off + r * L + (int64_t)k10 * L2;
+  load_twiddles<C, NT>(tws, tw, lgL2);
+  __syncthreads();
+  const LdRows<C, C> ld{src, lgL2, M};
+  const SeqCol<C> buf{s, L2};
+  seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, -1, ld, buf, buf);
+  const typename Cx<C>::R sc = (typename Cx<C>::R)scale;
+  for (int i = threadIdx.x; i < (L2 << lgM); i += NT) {
+    const int m = i >> lgL2, n2 = i & (L2 - 1);           // row-contiguous stores
+    C v = buf(m, n2);
+    if (lo) {                                             // T -> natural: twiddle W_L^{k1 n2}
+      const int e = (k10 + m) * n2;
+      C w = cmul_f(lo[e & 4095], hi[e >> 12]);
+      if (inv) w.y = -w.y;
+      v = cmul_f(v, w);
+    }
+    dst[(int64_t)m * L2 + n2] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
+  }
+}
+
+template <class C, class TO>
+struct StCols {
+  TO* base;
+  int L2;
+  typename Cx<C>::R sc;
+  __device__ __forceinline__ void operator()(int c, int n1, C v) const {
+    base[(int64_t)n1 * L2 + c] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
+  }
+};
+
+// column pass of the T -> natural pair: L1-point transforms of columns, no twiddle, out of place
+template <class C, class TO>
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) k_fft_colT(const C* __restrict__ in, TO* __restrict__ out,
+                                                                         Rows ri, Rows ro, int lgL1, int L2, int lgCW,
+                                                                         int inv, double scale,
+                                                                         const C* __restrict__ tw) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  C* s = reinterpret_cast<C*>(smraw);                  // [L1][CW] interleaved
+  C* tws = s + (1 << (lgL1 + lgCW));                   // [L1]
+  const int64_t r = blockIdx.y;
+  const int b = blockIdx.z;
+  const int64_t L = (int64_t)L2 << lgL1;
+  const int c0 = blockIdx.x << lgCW;
+  load_twiddles<C, 256>(tws, tw, lgL1);
+  __syncthreads();
+  const LdCols<C> ld{in + b * ri.stride_b + ri.off + r * L + c0, L2};
+  const StCols<C, TO> st{out + b * ro.stride_b + ro.off + r * L + c0, L2, (typename Cx<C>::R)scale};
+  const SeqInter<C> buf{s, 1 << lgCW};
+  seq_fft<C, 256, 16>(lgCW, lgL1, inv != 0, tws, -1, ld, st, buf);
+}
+
 // ---------------------------------------------------------------- host side
 template <class T>
 static std::vector<T> twiddles() {
@@ -251,7 +322,7 @@ static int ilog2_exact(int64_t v) {
 
 template <class TI, class TO, class C>
 static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,
-                                cudaStream_t st) {
+                                cudaStream_t st, int layout = kLayoutNatural) {
   // rowB: 2 rows per CTA, 512 threads x 16 points (256 threads x 32 points measured slower)
   constexpr int kRowNT = 512;
   constexpr int kRowNPT = (2 * 4096) / kRowNT;
@@ -282,6 +353,36 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
   static_assert(sizeof(TI) == sizeof(C), "four-step input must already be in the compute type");
   const int L2 = 4096, lgL1 = lgL - 12, L1 = 1 << lgL1;
   const int lgCW = std::min(12, 12 - lgL1);                   // CW * L1 = 4096 points per CTA
+  if (layout != kLayoutNatural) {
+    static bool attrT = false;
+    if (!attrT) {
+      cudaFuncSetAttribute(k_fft_rowT<C, TO, kRowNPT, kRowNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(((4096 << kRowLgM) + 4096) * sizeof(C)));
+      cudaFuncSetAttribute(k_fft_rowT<C, C, kRowNPT, kRowNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(((4096 << kRowLgM) + 4096) * sizeof(C)));
+      cudaFuncSetAttribute(k_fft_colT<C, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * sizeof(C)));
+      attrT = true;
+    }
+    const int lgM = std::min(kRowLgM, lgL1);
+    C* io = reinterpret_cast<C*>(const_cast<TI*>(in));
+    if (layout == kLayoutToT) {   // natural -> T: columns (twiddled, in place), then rows stored in place
+      dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
+      k_fft_colA<C><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw,
+                                                                      FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+      dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
+      k_fft_rowT<C, TO, kRowNPT, kRowNT><<<gb, kRowNT, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
+          io, out, ri, ro, lgL1, lgM, inverse ? 1 : 0, scale, tw, nullptr, nullptr);
+    } else {                      // T -> natural: rows (twiddled on store, in place), then columns out of place
+      dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
+      k_fft_rowT<C, C, kRowNPT, kRowNT><<<gb, kRowNT, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
+          io, io, ri, ri, lgL1, lgM, inverse ? 1 : 0, 1.0, tw, FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+      dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
+      k_fft_colT<C, TO><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, out, ri, ro, lgL1, L2, lgCW,
+                                                                          inverse ? 1 : 0, scale, tw);
+    }
+    count_launch(2);
+    return cudaGetLastError();
+  }
   {
     dim3 grid((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
     k_fft_colA<C><<<grid, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(
@@ -302,7 +403,7 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
 // kMaxFftJobs per launch), longer ones through fft_launch_t (four-step).
 template <class TI, class TO, class C>
 static cudaError_t fft_groups_t(const TI* in, TO* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                                int B, bool inverse, const FftTables& T, cudaStream_t st) {
+                                int B, bool inverse, const FftTables& T, cudaStream_t st, int layout = kLayoutNatural) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_small_multi<TI, TO, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -327,7 +428,7 @@ static cudaError_t fft_groups_t(const TI* in, TO* out, int64_t in_sb, int64_t ou
     if (g[i].count <= 0 || B <= 0) continue;
     if (g[i].L > 4096) {
       Rows ri{in_sb, g[i].off, g[i].count, g[i].L}, ro{out_sb, g[i].off, g[i].count, g[i].L};
-      if ((e = fft_launch_t<TI, TO, C>(in, out, ri, ro, B, inverse, T, st))) return e;
+      if ((e = fft_launch_t<TI, TO, C>(in, out, ri, ro, B, inverse, T, st, layout))) return e;
       continue;
     }
     const int lgL = ilog2_exact(g[i].L), lgM = 12 - lgL;
@@ -339,17 +440,16 @@ static cudaError_t fft_groups_t(const TI* in, TO* out, int64_t in_sb, int64_t ou
   return flush();
 }
 cudaError_t fft_groups(const float2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                       int B, bool inverse, const FftTables& T, cudaStream_t st) {
-  return fft_groups_t<float2, float2, float2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
+                       int B, bool inverse, const FftTables& T, cudaStream_t st, int layout) {
+  return fft_groups_t<float2, float2, float2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st, layout);
 }
 cudaError_t fft_groups_df(const double2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                          int B, bool inverse, const FftTables& T, cudaStream_t st) {
-  return fft_groups_t<double2, float2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
+                          int B, bool inverse, const FftTables& T, cudaStream_t st, int layout) {
+  return fft_groups_t<double2, float2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st, layout);
 }
-
 cudaError_t fft_groups_dd(const double2* in, double2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                          int B, bool inverse, const FftTables& T, cudaStream_t st) {
-  return fft_groups_t<double2, double2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st);
+                          int B, bool inverse, const FftTables& T, cudaStream_t st, int layout) {
+  return fft_groups_t<double2, double2, double2>(in, out, in_sb, out_sb, g, ng, B, inverse, T, st, layout);
 }
 
 cudaError_t fft_launch(const float2* in, float2* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,

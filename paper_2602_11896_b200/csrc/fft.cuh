@@ -29,15 +29,19 @@ cudaError_t fft_launch_dd(const double2* in, double2* out, Rows ri, Rows ro, int
                           const FftTables& T, cudaStream_t st);
 cudaError_t fft_launch_df(const double2* in, float2* out, Rows ri, Rows ro, int B, bool inverse,
                           const FftTables& T, cudaStream_t st);
+// Storage order of rows longer than 4096 points (four-step transforms): natural, or the "T-layout" in
+// which element k1 + L1 k2 (L1 = L / 4096) sits at k1 4096 + k2 -- the order the row pass leaves when it
+// stores in place, used between elementwise stages (fft.cu). Rows of <= 4096 points are always natural.
+constexpr int kLayoutNatural = 0, kLayoutToT = 1, kLayoutFromT = 2;
 // Row groups {off, count, L} (offsets shared by in and out, per-signal strides in_sb / out_sb): groups of
 // length <= 4096 run in grouped launches, longer ones as four-step transforms.
 struct FftGroup;
 cudaError_t fft_groups(const float2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                       int B, bool inverse, const FftTables& T, cudaStream_t st);
+                       int B, bool inverse, const FftTables& T, cudaStream_t st, int layout = kLayoutNatural);
 cudaError_t fft_groups_dd(const double2* in, double2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                          int B, bool inverse, const FftTables& T, cudaStream_t st);
+                          int B, bool inverse, const FftTables& T, cudaStream_t st, int layout = kLayoutNatural);
 cudaError_t fft_groups_df(const double2* in, float2* out, int64_t in_sb, int64_t out_sb, const FftGroup* g, int ng,
-                          int B, bool inverse, const FftTables& T, cudaStream_t st);
+                          int B, bool inverse, const FftTables& T, cudaStream_t st, int layout = kLayoutNatural);
 std::vector<float2> fft_twiddle_table();
 // Per-pass twiddles for the in-SMEM transforms of length L = 2^lg <= 4096, table of L at [L, 2L): pass p of
 // seq_fft (radix R_p, sub-transform size Ns_p) holds W_{Ns_p R_p}^{r k} at (Ns_p - 1) + (r - 1) Ns_p + k,

@@ -527,7 +527,10 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   // A2: layer 1: cdgmm + subsample_fourier (float64), ifft (float64 -> complex64 Z1),
   // modulus (-> float64 rows), fft (float64 -> complex64 U1_hat)
   launch_gather_dd(Xhd, sd, Ad, sAd, d.l1_jobs, d.l1_tiles, d.n_l1, d.l1_ntiles, d.spec_vals_d, mb, st);
-  if ((e = fft_groups_df(Ad, w.Z1, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt, st)))
+  // Z1 rows longer than 4096 points stay in the four-step's T-layout (fft.cuh): every consumer of Z1 and
+  // U1 up to the U1 FFT (which takes T-layout input) is elementwise
+  if ((e = fft_groups_df(Ad, w.Z1, sAd, w.s_L1, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt, st,
+                         kLayoutToT)))
     return e;
   const PackGroups pg = pack_groups(p);
   launch_modulus_pack(w.Z1, w.s_L1, Ad, sAd, pg, mb, st);   // A: pair-packed complex128 rows (L1 layout)
@@ -538,7 +541,7 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
   double2* U1hd = reinterpret_cast<double2*>(w.U1h);
   const int64_t sU1d = w.s_L1 / 2;
   if ((e = fft_groups_dd(Ad, U1hd, sAd, sU1d, p.l1_pgroups.data(), (int)p.l1_pgroups.size(), mb, false, d.fftt,
-                         st)))
+                         st, kLayoutFromT)))
     return e;
   // S0 and S1 time averages (Eq.3 time part)
   launch_gather_df(Xhd, sd, w.cs, w.s_c, d.s0_job, d.s0_tiles, 1, d.s0_ntiles, d.spec_vals, mb, st);
@@ -612,12 +615,12 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
   // A8: g_hat_U1 -> U1h ; g_U1 = Re IFFT -> A
   launch_adj_gather_u1(p, d, w.ct, w.s_c, w.Y2, w.s_Y2, w.U1h, w.s_L1, mb, st, own);
   if ((e = fft_groups(w.U1h, w.A, w.s_L1, w.s_A, p.l1_groups.data(), (int)p.l1_groups.size(), mb, true, d.fftt,
-                      st)))
+                      st, kLayoutToT)))   // g_U1 in T-layout, like Z1 (elementwise phase below)
     return e;
   // A9: modulus adjoint, FFT, layer-1 adjoint gather, IFFT, reflect adjoint
   launch_phase_mul(w.Z1, w.A, w.s_A, w.U1h, p.sumL1, w.s_L1, w.thr, mb, st);  // Z1, U1h share the L1 stride
   if ((e = fft_groups(w.U1h, w.A, w.s_L1, w.s_A, p.l1_groups.data(), (int)p.l1_groups.size(), mb, false, d.fftt,
-                      st)))
+                      st, kLayoutFromT)))   // T-layout g_Z1 -> natural spectrum
     return e;
   launch_adj_gather_x(p, d, w.A, w.s_A, w.Xh, w.s_xp, mb, st);
   if ((e = fft_rows(p, w.Xh, w.s_xp, w.xp, w.s_xp, 0, 1, p.N_pad, mb, true, st))) return e;
@@ -1092,7 +1095,7 @@ jtfs_status jtfs_debug_stage(jtfs_plan_t plan, int stage, const float* x, int64_
       CK(cudaMemcpy2DAsync(out, p.N_pad * 16, w.Xh, w.s_xp * 8, p.N_pad * 16, B, cudaMemcpyDeviceToDevice, st));
     } else {            // Z1, complex64 [B][sum L1]
       if (out_bytes < (size_t)B * p.sumL1 * 8) return fail(JTFS_ERR_SIZE, "out too small");
-      CK(cudaMemcpy2DAsync(out, p.sumL1 * 8, w.Z1, w.s_L1 * 8, p.sumL1 * 8, B, cudaMemcpyDeviceToDevice, st));
+      launch_untranspose_rows(w.Z1, w.s_L1, (float2*)out, p.sumL1, pack_groups(p), p.sumL1, (int)B, st);
     }
   } else if (stage == 4) {
     if (out_bytes < (size_t)B * p.n_coef * 4) return fail(JTFS_ERR_SIZE, "out too small");

@@ -136,6 +136,14 @@ void launch_modulus_pack(const float2* z, int64_t zsb, double2* u, int64_t usb, 
   count_launch();
 }
 
+// position of natural element n of a row of 2^lgL points in the T-layout of the four-step (fft.cuh):
+// n = k1 + L1 k2 sits at k1 4096 + k2 (rows of <= 4096 points are natural)
+__device__ __forceinline__ int64_t t_pos(int64_t n, int lgL) {
+  if (lgL <= 12) return n;
+  const int lgL1 = lgL - 12;
+  return ((n & ((int64_t(1) << lgL1) - 1)) << 12) + (n >> lgL1);
+}
+
 // debug stage U1: unpack the pair-packed float64 rows -> fp32 [sum L1] in the natural row layout
 __global__ void k_unpack_u1(const double2* __restrict__ u, int64_t usb, float* __restrict__ out, int64_t out_sb,
                             PackGroups G, int64_t n) {
@@ -145,8 +153,27 @@ __global__ void k_unpack_u1(const double2* __restrict__ u, int64_t usb, float* _
   while (g + 1 < G.n && i >= G.off[g + 1]) ++g;
   const int lgL = G.lgL[g];
   const int64_t r = (i - G.off[g]) >> lgL, e = (i - G.off[g]) & ((int64_t(1) << lgL) - 1);
-  const double2 v = u[blockIdx.y * usb + G.pstart[g] + ((r >> 1) << lgL) + e];
+  const double2 v = u[blockIdx.y * usb + G.pstart[g] + ((r >> 1) << lgL) + t_pos(e, lgL)];
   out[blockIdx.y * out_sb + i] = (float)((r & 1) ? v.y : v.x);
+}
+
+// debug stage Z1: rows in T-layout -> natural order
+__global__ void k_untranspose_rows(const float2* __restrict__ z, int64_t zsb, float2* __restrict__ out,
+                                   int64_t out_sb, PackGroups G, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int g = 0;
+  while (g + 1 < G.n && i >= G.off[g + 1]) ++g;
+  const int lgL = G.lgL[g];
+  const int64_t r = (i - G.off[g]) >> lgL, e = (i - G.off[g]) & ((int64_t(1) << lgL) - 1);
+  out[blockIdx.y * out_sb + i] = z[blockIdx.y * zsb + G.off[g] + (r << lgL) + t_pos(e, lgL)];
+}
+
+void launch_untranspose_rows(const float2* z, int64_t zsb, float2* out, int64_t out_sb, const PackGroups& G,
+                             int64_t n, int B, cudaStream_t st) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
+  k_untranspose_rows<<<g, 256, 0, st>>>(z, zsb, out, out_sb, G, n);
+  count_launch();
 }
 
 void launch_unpack_u1(const double2* u, int64_t usb, float* out, int64_t out_sb, const PackGroups& G, int64_t n,
