@@ -323,10 +323,11 @@ static int ilog2_exact(int64_t v) {
 template <class TI, class TO, class C>
 static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, bool inverse, const FftTables& T,
                                 cudaStream_t st, int layout = kLayoutNatural) {
-  // rowB: 2 rows per CTA, 512 threads x 16 points (256 threads x 32 points measured slower)
-  constexpr int kRowNT = 512;
-  constexpr int kRowNPT = (2 * 4096) / kRowNT;
-  constexpr int kRowLgM = 1;
+  // row passes: float32 4 rows per CTA, 1024 threads x 16 points (transposed stores in full 32-byte
+  // sectors); float64 2 rows, 512 threads (SMEM); 256 threads x 32 points measured slower
+  constexpr int kRowLgM = sizeof(C) == 8 ? 2 : 1;
+  constexpr int kRowNT = sizeof(C) == 8 ? 1024 : 512;
+  constexpr int kRowNPT = (4096 << kRowLgM) / kRowNT;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_rowB<C, TO, kRowNPT, kRowNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
