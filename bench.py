@@ -49,9 +49,12 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi clock / throttle sampling during the timed region (B200_PROFILING.md recipe)."""
+    """nvidia-smi clock / throttle sampling (B200_PROFILING.md recipe). The sampler starts before the
+    warm-up steps (nvidia-smi needs ~0.1-0.3 s to emit its first line) and every line carries a timestamp;
+    stop(t0, t1) keeps the samples inside the timed region [t0, t1] (host wall clock), or, for a timed
+    region shorter than the 200 ms sampling period, the samples nearest to it (flagged)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -68,28 +71,37 @@ class Clocks:
         except Exception:
             self.proc = None
 
-    def stop(self) -> dict:
+    def stop(self, t0: float | None = None, t1: float | None = None) -> dict:
+        import datetime
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
         self.proc.terminate()
         self.proc.wait()
-        sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in open(self.path):
             f = [s.strip() for s in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                smax = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), [n for n, v in zip(names, f[6:10]) if v.lower() == "active"]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [r for r in rows if t0 is None or (t0 - 0.05 <= r[0] <= t1 + 0.05)]
+        nearest = False
+        if not inside and rows and t0 is not None:
+            mid = 0.5 * (t0 + t1)
+            inside = sorted(rows, key=lambda r: abs(r[0] - mid))[:2]
+            nearest = True
+        sm = [r[1] for r in inside]
+        reasons = sorted({n for r in inside for n in r[3]})
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": inside[-1][2] if inside else None,
+               "reasons": reasons, "samples": len(inside)}
+        if nearest:
+            out["note"] = "timed region shorter than the 200 ms sampling period: nearest samples"
+        return out
 
 
 def _oracle_sample(config: str, o, x, y):
@@ -275,13 +287,13 @@ def main() -> None:
         else:
             plan.loss_grad(y, St, loss=loss, grad=grad, ws=ws)
 
+    clocks = Clocks(lrank)
+    clocks.start()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = Clocks(lrank)
-    clocks.start()
     plan.prof_enable(True)
     n0 = plan.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -289,16 +301,18 @@ def main() -> None:
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    t_wall0 = time.time()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
+    t_wall1 = time.time()
     ms = e0.elapsed_time(e1)
     launches = plan.launch_count() - n0
     plan.prof_enable(False)
     prof = {"joint_fwd": plan.prof_read(0), "joint_bwd": plan.prof_read(2)}
-    clk = clocks.stop()
+    clk = clocks.stop(t_wall0, t_wall1)
     if world > 1:
         dist.barrier()
         t = torch.tensor([ms], device=dev)

@@ -107,13 +107,16 @@ def test_microbatch_and_shards_sum(plans):
     ws = torch.empty(p.workspace_size(1, True), dtype=torch.uint8, device="cuda")
     l1, g1 = p.loss_grad(yd, S, ws=ws)
     assert torch.equal(g1, g) and torch.equal(l1, loss)
-    # path shards sum to the whole (only the fp32 summation order of the accumulations differs)
+    # path shards (whole blocks, jtfs_plan_shards) sum to the whole. The loss partials are float64 sums of
+    # disjoint coefficient sets (1e-6); each shard's gradient runs the fp32 adjoint chain (FFTs, gathers)
+    # on its own partial spectra, so the sum of shards differs from the one-shot gradient by fp32 rounding
+    # of those transforms (measured ~1e-6; bar 1e-5)
     ls, gs = 0, 0
     for sh in range(3):
         l_, g_ = p.loss_grad(yd, S, shard=sh, n_shards=3)
         ls, gs = ls + l_, gs + g_
     assert rel(gs.cpu().numpy(), g.cpu().numpy()) <= 1e-5
-    assert rel(ls.cpu().numpy(), loss.cpu().numpy()) <= 1e-5
+    assert rel(ls.cpu().numpy(), loss.cpu().numpy()) <= 1e-6
 
 
 def test_metamer_step_parity(plans):
