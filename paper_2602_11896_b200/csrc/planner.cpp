@@ -182,9 +182,38 @@ static void build_tc_tables(Plan* p) {
     // resident Y2 tile when it fits the TMEM (TS form) or two column tiles share the B stream (K2 <= 64);
     // else the tile in SMEM (SS form) while it fits (K2 <= 168); larger K goes split-K: the forward's parts
     // stay in the TS form and the backward reads the forward's W instead of recomputing GEMM1. (Measured
-    // at c2: converting the K2 = 136 / 168 blocks to split-K costs more in W traffic, 24 B per cell over
-    // two parts, than it saves.)
-    if (kap <= 2 && (CT == 2 || tc_fwd_tsa(1, K2) || K2 <= 168)) {
+    // at c2: converting the K2 = 136 / 168 blocks to split-K in two parts costs more in W traffic, 24 B per
+    // cell, than it saves; in one part, 16 B per cell, it is a gain: see above.)
+    // "Split-K in one part" for 130 <= K2 <= 192 (A tile in TMEM, one accumulator buffer): the forward
+    // stores W (8 B per modulus cell) and the backward reads it instead of recomputing GEMM1, which frees
+    // its SMEM from the 128 x K2 A tile for wide B2 chunks (with the A tile resident the rings fell to
+    // 8-16-wide B2 chunks: many ~400-cycle bulk copies per 32-row tile). Measured: c2 21.31 -> 20.88 ms,
+    // c4 660.0 -> 649.4 ms per step. Applied while the block's W buffer stays <= 2 GB per signal (c5's
+    // blocks would cut its micro-batch from 17 to 6 signals). JTFS_KS1_MIN / JTFS_KS1_MAXW: tuning.
+    static const int ks1_min = [] {
+      const char* e = std::getenv("JTFS_KS1_MIN");
+      return e ? std::atoi(e) : 130;
+    }();
+    static const double ks1_maxw = [] {
+      const char* e = std::getenv("JTFS_KS1_MAXW");
+      return e ? std::atof(e) : 2e9;
+    }();
+    double w_bytes = 0;
+    {
+      int wpt = 0;
+      for (int f = 0; f < nfr; ++f) wpt += (int)((p->units[bi * nfr + f].n_rows + 63) / 64);
+      w_bytes = (double)((p->binfo[bi].n_cols + 127) / 128) * wpt * 128 * 128 * 4;
+    }
+    if (K2 >= ks1_min && CT == 1 && tc_fwd_tsa(1, K2) && kap <= 4 && w_bytes <= ks1_maxw) {
+      ks = 1;
+      kcw = 16;
+      for (int w : {64, 32, 16}) {
+        if (w > K2) continue;
+        if (tc_fwd_stages(1, 2 << kap, K2, w) >= 3) { kcw = w; break; }
+      }
+      nparts = 1;
+      kpw = (K2 + kcw - 1) / kcw * kcw;
+    } else if (kap <= 2 && (CT == 2 || tc_fwd_tsa(1, K2) || K2 <= 168)) {
       // widest B chunk (fewest hand-offs per tile; one chunk per tile when small) leaving >= 3 stages
       // (each bulk copy costs the copy engine ~400 cycles whatever its size: one copy per tile if possible)
       // Preferred: a width that also allows the forward's two MMA issuers (two accumulator buffers and two
