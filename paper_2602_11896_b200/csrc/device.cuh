@@ -95,6 +95,7 @@ struct DeviceTables {
 
 constexpr int kGatherThreads = 256;                 // threads per CTA of the gather kernels
 constexpr int kGatherTile = 4 * kGatherThreads;     // outputs per CTA (4 per thread, 256 apart)
+constexpr int kGatherTileT = 4096;                  // outputs per CTA of a T-layout job (staged in SMEM)
 constexpr int kPhiTSmem = 12288;   // phi_T half kernel staged in SMEM up to this many taps
 constexpr int kJC = 64;            // joint stage: columns per CTA
 constexpr int kJR = 64;            // joint stage: rows per chunk

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -187,19 +188,38 @@ __global__ void __launch_bounds__(NT) k_fft_rowB(const C* __restrict__ in, TO* _
 }
 
 // ---------------------------------------------------------------- "T-layout" passes (no transposition)
+template <class C, class TO>
+struct StRowT {  // row m of the CTA at dst + m * 4096, element n2; T -> natural twiddle W_L^{(k10 + m) n2} if lo
+  TO* dst;
+  int k10, inv;
+  typename Cx<C>::R sc;
+  const C* lo;
+  const C* hi;
+  __device__ __forceinline__ void operator()(int m, int n2, C v) const {
+    if (lo) {
+      const int e = (k10 + m) * n2;
+      C w = cmul_f(lo[e & 4095], hi[e >> 12]);
+      if (inv) w.y = -w.y;
+      v = cmul_f(v, w);
+    }
+    dst[((int64_t)m << 12) + n2] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
+  }
+};
 // A four-step transform whose rows are stored in place keeps every global access row-contiguous: the
 // natural -> T pair (k_fft_colA, then k_fft_rowT without twiddle) leaves X[k1 + L1 k2] at position
 // k1 L2 + k2, and the T -> natural pair (k_fft_rowT with the twiddle W_L^{k1 n2} on its store, then
 // k_fft_colT) takes a row-major T-layout input back to natural order. Chains whose consumers are
 // elementwise (Z1 -> |Z1| -> U1 FFT; g_U1 -> phase -> g_Z1 FFT) run in T-layout in between.
-template <class C, class TO, int NPT, int NT>
-__global__ void __launch_bounds__(NT) k_fft_rowT(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
+// Occupancy (row passes are HBM bound; a CTA's load, compute and store phases only overlap with other
+// CTAs'): float32 2 rows x 512 threads (64 KB + 32 KB twiddles, 2 CTAs per SM); float64 1 row x 256 threads
+// with the twiddle table read through L1 (TWG; 64 KB, 2 CTAs per SM at 128 registers).
+template <class C, class TO, int NPT, int NT, bool TWG, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_fft_rowT(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
                                                   int lgL1, int lgM, int inv, double scale, const C* __restrict__ tw,
                                                   const C* __restrict__ lo, const C* __restrict__ hi) {
   extern __shared__ __align__(16) uint8_t smraw[];
   constexpr int lgL2 = 12, L2 = 4096;
   C* s = reinterpret_cast<C*>(smraw);                 // [M][L2] swizzled
-  C* tws = s + (L2 << lgM);                           // [L2]
   const int64_t r = blockIdx.y;
   const int b = blockIdx.z;
   const int64_t L = (int64_t)L2 << lgL1;
@@ -207,23 +227,20 @@ __global__ void __launch_bounds__(NT) k_fft_rowT(const C* __restrict__ in, TO* _
   const int k10 = blockIdx.x * M;
   const C* src = in + b * ri.stride_b + ri.off + r * L + (int64_t)k10 * L2;
   TO* dst = out + b * ro.stride_b + ro.off + r * L + (int64_t)k10 * L2;
-  load_twiddles<C, NT>(tws, tw, lgL2);
-  __syncthreads();
+  const C* tws = tw + L2;                             // per-pass table of length 4096 (global, via L1)
+  if constexpr (!TWG) {
+    C* t = s + (L2 << lgM);                           // [L2]
+    load_twiddles<C, NT>(t, tw, lgL2);
+    __syncthreads();
+    tws = t;
+  }
   const LdRows<C, C> ld{src, lgL2, M};
   const SeqCol<C> buf{s, L2};
-  seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, -1, ld, buf, buf);
-  const typename Cx<C>::R sc = (typename Cx<C>::R)scale;
-  for (int i = threadIdx.x; i < (L2 << lgM); i += NT) {
-    const int m = i >> lgL2, n2 = i & (L2 - 1);           // row-contiguous stores
-    C v = buf(m, n2);
-    if (lo) {                                             // T -> natural: twiddle W_L^{k1 n2}
-      const int e = (k10 + m) * n2;
-      C w = cmul_f(lo[e & 4095], hi[e >> 12]);
-      if (inv) w.y = -w.y;
-      v = cmul_f(v, w);
-    }
-    dst[(int64_t)m * L2 + n2] = t_cvt<TO>(Cx<C>::mk(v.x * sc, v.y * sc));
-  }
+  // the last radix-16 pass stores straight to global memory (consecutive threads hold consecutive n2 of a
+  // row: coalesced), with the T -> natural twiddle and the scale applied on the way; in place is safe (every
+  // load of the CTA's rows happens in the first pass)
+  const StRowT<C, TO> st{dst, k10, inv, (typename Cx<C>::R)scale, lo, hi};
+  seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, -1, ld, st, buf);
 }
 
 template <class C, class TO>
@@ -357,26 +374,58 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
   if (layout != kLayoutNatural) {
     static bool attrT = false;
     if (!attrT) {
-      cudaFuncSetAttribute(k_fft_rowT<C, TO, kRowNPT, kRowNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(((4096 << kRowLgM) + 4096) * sizeof(C)));
-      cudaFuncSetAttribute(k_fft_rowT<C, C, kRowNPT, kRowNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(((4096 << kRowLgM) + 4096) * sizeof(C)));
+      cudaFuncSetAttribute(k_fft_rowT<C, TO, 16, (sizeof(C) == 8 ? 512 : 256), sizeof(C) == 16, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12288 * sizeof(C)));
+      cudaFuncSetAttribute(k_fft_rowT<C, C, 16, (sizeof(C) == 8 ? 512 : 256), sizeof(C) == 16, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12288 * sizeof(C)));
       cudaFuncSetAttribute(k_fft_colT<C, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * sizeof(C)));
       attrT = true;
     }
-    const int lgM = std::min(kRowLgM, lgL1);
+    constexpr int kTLgM = sizeof(C) == 8 ? 1 : 0, kTNT = sizeof(C) == 8 ? 512 : 256;
+    constexpr bool kTwg = sizeof(C) == 16;
+    static const bool alt_rows = std::getenv("JTFS_ROWT_ALT") != nullptr;   // A/B timing only
+    const int lgM = std::min(kTLgM, lgL1);
+    const size_t smT = (size_t)((4096 << lgM) + (kTwg ? 0 : 4096)) * sizeof(C);
     C* io = reinterpret_cast<C*>(const_cast<TI*>(in));
+    if (alt_rows && sizeof(C) == 8) {   // A/B: float32 1 row x 256 threads, twiddles via L1, 4 CTAs per SM
+      static bool attrA = false;
+      if (!attrA) {
+        cudaFuncSetAttribute(k_fft_rowT<C, TO, 16, 256, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(4096 * sizeof(C)));
+        cudaFuncSetAttribute(k_fft_rowT<C, C, 16, 256, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(4096 * sizeof(C)));
+        attrA = true;
+      }
+      const size_t smA = (size_t)4096 * sizeof(C);
+      if (layout == kLayoutToT) {
+        dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
+        k_fft_colA<C><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw,
+                                                                        FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+        dim3 gb((unsigned)L1, (unsigned)ri.count, (unsigned)B);
+        k_fft_rowT<C, TO, 16, 256, true, 4><<<gb, 256, smA, st>>>(io, out, ri, ro, lgL1, 0, inverse ? 1 : 0, scale, tw,
+                                                                   nullptr, nullptr);
+      } else {
+        dim3 gb((unsigned)L1, (unsigned)ri.count, (unsigned)B);
+        k_fft_rowT<C, C, 16, 256, true, 4><<<gb, 256, smA, st>>>(io, io, ri, ri, lgL1, 0, inverse ? 1 : 0, 1.0, tw,
+                                                                  FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+        dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
+        k_fft_colT<C, TO><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, out, ri, ro, lgL1, L2, lgCW,
+                                                                            inverse ? 1 : 0, scale, tw);
+      }
+      count_launch(2);
+      return cudaGetLastError();
+    }
     if (layout == kLayoutToT) {   // natural -> T: columns (twiddled, in place), then rows stored in place
       dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
       k_fft_colA<C><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw,
                                                                       FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
       dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
-      k_fft_rowT<C, TO, kRowNPT, kRowNT><<<gb, kRowNT, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
-          io, out, ri, ro, lgL1, lgM, inverse ? 1 : 0, scale, tw, nullptr, nullptr);
+      k_fft_rowT<C, TO, 16, kTNT, kTwg, 2><<<gb, kTNT, smT, st>>>(io, out, ri, ro, lgL1, lgM, inverse ? 1 : 0, scale,
+                                                                 tw, nullptr, nullptr);
     } else {                      // T -> natural: rows (twiddled on store, in place), then columns out of place
       dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
-      k_fft_rowT<C, C, kRowNPT, kRowNT><<<gb, kRowNT, (size_t)((4096 << lgM) + 4096) * sizeof(C), st>>>(
-          io, io, ri, ri, lgL1, lgM, inverse ? 1 : 0, 1.0, tw, FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+      k_fft_rowT<C, C, 16, kTNT, kTwg, 2><<<gb, kTNT, smT, st>>>(io, io, ri, ri, lgL1, lgM, inverse ? 1 : 0, 1.0, tw,
+                                                               FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
       dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
       k_fft_colT<C, TO><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, out, ri, ro, lgL1, L2, lgCW,
                                                                           inverse ? 1 : 0, scale, tw);

@@ -190,7 +190,10 @@ static cudaError_t upload(Plan& p) {
   UP(p.cn_den, cn_den);
   auto job_tiles = [](const std::vector<GatherJob>& jobs) {
     std::vector<int64_t> c;
-    for (auto& j : jobs) c.push_back((j.L_out + kGatherTile - 1) / kGatherTile);
+    for (auto& j : jobs) {
+      const int64_t tile = j.tl ? kGatherTileT : kGatherTile;
+      c.push_back((j.L_out + tile - 1) / tile);
+    }
     return prefix(c);
   };
   std::vector<int64_t> t;
@@ -559,7 +562,8 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     launch_gather_df(U1hd, sU1d, w.A, w.s_A, d.l2_jobs, d.l2_tiles, d.n_l2, d.l2_ntiles, d.spec_vals, mb, st, own);
     const std::vector<FftGroup> g2 = own_groups(p, own);
     if (!g2.empty() &&
-        (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, true, d.fftt, st)))
+        (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, true, d.fftt, st,
+                        kLayoutFromT)))   // the gather left rows > 4096 points in T-layout
       return e;
     RET();
     if (stop == 3) return cudaSuccess;
@@ -600,7 +604,8 @@ static cudaError_t run_backward(const Plan& p, const Bufs& w, float* grad, int64
     // FFT of g_Y2 rows -> G_Y (into Y2), own blocks only
     const std::vector<FftGroup> g2 = own_groups(p, own);
     if (!g2.empty() &&
-        (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, false, d.fftt, st)))
+        (e = fft_groups(w.A, w.Y2, w.s_A, w.s_Y2, g2.data(), (int)g2.size(), mb, false, d.fftt, st,
+                        kLayoutToT)))   // spectra of rows > 4096 points left in T-layout (k_adj_gather_u1)
       return e;
   }
   // order-1 adjoint -> g_S1t ; G_S = FFT(g_S1t)

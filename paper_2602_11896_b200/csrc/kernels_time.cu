@@ -61,8 +61,15 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
   const GatherJob J = jobs[j];
   if (J.blk >= 0 && !owns_block(own, J.blk)) return;   // layer-2 block of another path shard
   const TI* src = in + b * in_sb + J.in_off;
-  const int64_t m0 = (tile - tiles[j]) * kGatherTile;
-  for (int64_t m = m0 + threadIdx.x; m < J.L_out && m < m0 + kGatherTile; m += kGatherThreads) {
+  const int tsz = J.tl ? kGatherTileT : kGatherTile;
+  const int64_t m0 = (tile - tiles[j]) * tsz;
+  // T-layout jobs (layer-2 rows > 4096 points, whose inverse FFT then runs row-contiguous): the tile's
+  // 4096 outputs are staged in SMEM [kk][k1] (m = m0 + k1 + L1 kk; k1 XOR-swizzled by kk, conflict-free
+  // both ways) and written as runs of 4096 / L1 consecutive k2 per k1 row of the T-layout
+  constexpr bool kCanT = sizeof(TO) == 8;
+  __shared__ TO stg[kCanT ? kGatherTileT : 1];
+  const int64_t L1t = J.L_out >> 12;
+  for (int64_t m = m0 + threadIdx.x; m < J.L_out && m < m0 + tsz; m += kGatherThreads) {
     // L_in, L_out: powers of two (grid lengths N_pad >> k)
     int64_t s = J.lo + ((m - J.lo) & (J.L_out - 1));          // smallest s >= lo with s = m mod L_out
     R ax = 0, ay = 0;
@@ -79,7 +86,21 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
       ax += h * vx;
       ay += h * vy;
     }
-    st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
+    if (kCanT && J.tl) {
+      const int64_t ml = m - m0, kk = ml / L1t, k1 = ml & (L1t - 1);
+      st_c(stg + kk * L1t + (k1 ^ (kk & (L1t - 1))), (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
+    } else {
+      st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
+    }
+  }
+  if (kCanT && J.tl) {
+    __syncthreads();
+    const int64_t W = kGatherTileT / L1t;
+    TO* dst = out + b * out_sb + J.out_off + m0 / L1t;
+    for (int i = threadIdx.x; i < kGatherTileT; i += kGatherThreads) {
+      const int64_t k1 = i / W, kk = i & (W - 1);
+      dst[(k1 << 12) + kk] = stg[kk * L1t + (k1 ^ (kk & (L1t - 1)))];
+    }
   }
 }
 
@@ -263,28 +284,71 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
   __syncthreads();
   const Support spT = phiT_sup[k1];
   const int nb = s_nb;
-  // kU1AdjTile elements per CTA, 256 apart per thread (coalesced), one setup per CTA
-  for (int64_t m = (tile - tiles[n1]) * kU1AdjTile + threadIdx.x; m < L1 && m < (tile - tiles[n1] + 1) * kU1AdjTile;
-       m += 256) {
-    float2 acc = make_float2(0.f, 0.f);
-    {
-      const int64_t t = (m - spT.lo) & (L1 - 1);                 // L1, Ft, T2: powers of two
-      if (t < spT.len) {
-        float h = __ldg(vals + spT.off + t);
-        float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m & (Ft - 1))];
-        acc = make_float2(h * v.x, h * v.y);
+  // kU1AdjTile elements per CTA, 256 apart per thread (coalesced), one setup per CTA. Blocks whose rows
+  // are longer than 4096 points hold their spectra in the four-step's T-layout (bin k1 + L1b k2 at
+  // k1 4096 + k2, fft.cuh): the CTA's 1024 consecutive bins are staged in SMEM by runs of 1024 / L1b
+  // consecutive k2 per k1 row ([kk][k1], k1 XOR-swizzled by kk), double-buffered (one barrier per block).
+  // Summation order per element: phi_T term, then blocks ascending (as in the natural-layout loop).
+  constexpr int kR = kU1AdjTile / 256;
+  __shared__ float2 stg[2][kU1AdjTile];
+  const int64_t mt0 = (tile - tiles[n1]) * kU1AdjTile;
+  float2 acc[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t m = mt0 + threadIdx.x + 256 * r;
+    acc[r] = make_float2(0.f, 0.f);
+    const int64_t t = (m - spT.lo) & (L1 - 1);                 // L1, Ft, T2: powers of two
+    if (m < L1 && t < spT.len) {
+      float h = __ldg(vals + spT.off + t);
+      float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m & (Ft - 1))];
+      acc[r] = make_float2(h * v.x, h * v.y);
+    }
+  }
+  int sb = 0;
+  for (int i = 0; i < nb; ++i) {
+    const int64_t T2 = s_T2[i];
+    const int64_t d0 = (mt0 - s_lo[i]) & (L1 - 1);
+    if (s_len[i] <= 0 || (d0 >= s_len[i] && d0 + kU1AdjTile <= L1)) continue;   // CTA-uniform: no overlap
+    const float2* gy = GY + b * GY_sb + s_y[i];
+    if (T2 > 4096) {
+      const int64_t L1b = T2 >> 12, Wb = kU1AdjTile / L1b, mm0 = mt0 & (T2 - 1);
+      const float2* src = gy + mm0 / L1b;
+      for (int e = threadIdx.x; e < kU1AdjTile; e += 256) {
+        const int64_t kq = e / Wb, kk = e & (Wb - 1);
+        stg[sb][kk * L1b + (kq ^ (kk & (L1b - 1)))] = src[(kq << 12) + kk];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int64_t m = mt0 + threadIdx.x + 256 * r;
+        const int64_t t = (m - s_lo[i]) & (L1 - 1);
+        if (m < L1 && t < s_len[i]) {
+          const int64_t ml = threadIdx.x + 256 * r, kk = ml / L1b, kq = ml & (L1b - 1);
+          const float h = __ldg(vals + s_off[i] + t);
+          const float2 v = stg[sb][kk * L1b + (kq ^ (kk & (L1b - 1)))];
+          acc[r].x = fmaf(h, v.x, acc[r].x);
+          acc[r].y = fmaf(h, v.y, acc[r].y);
+        }
+      }
+      sb ^= 1;
+    } else {
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int64_t m = mt0 + threadIdx.x + 256 * r;
+        const int64_t t = (m - s_lo[i]) & (L1 - 1);
+        if (m < L1 && t < s_len[i]) {
+          const float h = __ldg(vals + s_off[i] + t);
+          const float2 v = gy[m & (T2 - 1)];
+          acc[r].x = fmaf(h, v.x, acc[r].x);
+          acc[r].y = fmaf(h, v.y, acc[r].y);
+        }
       }
     }
-    for (int i = 0; i < nb; ++i) {
-      const int64_t t = (m - s_lo[i]) & (L1 - 1);
-      if (t < s_len[i]) {
-        float h = __ldg(vals + s_off[i] + t);
-        float2 v = GY[b * GY_sb + s_y[i] + (m & (s_T2[i] - 1))];
-        acc.x = fmaf(h, v.x, acc.x);
-        acc.y = fmaf(h, v.y, acc.y);
-      }
-    }
-    out[b * out_sb + l1_off[n1] + m] = acc;
+  }
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t m = mt0 + threadIdx.x + 256 * r;
+    if (m < L1) out[b * out_sb + l1_off[n1] + m] = acc[r];
   }
 }
 

@@ -35,7 +35,8 @@ struct GatherJob {
   int32_t par;   // -1: plain complex row; 0 / 1: the row is the real / imaginary half of a pair-packed row
                  // whose FFT carries two real rows (Z = U_a + i U_b): U_a^[s] = (Z[s] + conj Z[-s]) / 2,
                  // U_b^[s] = (Z[s] - conj Z[-s]) / 2i
-  int32_t pad_;
+  int32_t tl;    // 1: the output row (L_out > 4096 points) is written in the four-step's T-layout (fft.cuh):
+                 // element m = k1 + L1 k2 at k1 4096 + k2, so that its inverse FFT runs row-contiguous
 };
 
 // Batched FFT group: `count` rows of length L starting at `off` (per signal).

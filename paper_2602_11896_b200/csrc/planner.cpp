@@ -592,7 +592,8 @@ int make_plan(int64_t N, int J, int Q, int J_fr, int Q_fr, int64_t T, int64_t F,
       int k1 = std::min(p->psi1[n1].j, log2T);
       auto& sp = p->psi2_sup[bi * (log2T + 1) + k1];
       p->l2_jobs.push_back({u1_in[n1], p->L1[n1], sp.lo, sp.len, sp.off, yoff + n1 * bf.T2, bf.T2,
-                            (float)std::ldexp(1.0, -(b.s2 - k1)), (int32_t)bi, u1_par[n1], 0});
+                            (float)std::ldexp(1.0, -(b.s2 - k1)), (int32_t)bi, u1_par[n1],
+                            bf.T2 > 4096 ? 1 : 0});
     }
     p->y2_groups.push_back({yoff, b.n1_max, bf.T2});
     yoff += (int64_t)b.n1_max * bf.T2;
