@@ -211,8 +211,9 @@ struct StRowT {  // row m of the CTA at dst + m * 4096, element n2; T -> natural
 // k_fft_colT) takes a row-major T-layout input back to natural order. Chains whose consumers are
 // elementwise (Z1 -> |Z1| -> U1 FFT; g_U1 -> phase -> g_Z1 FFT) run in T-layout in between.
 // Occupancy (row passes are HBM bound; a CTA's load, compute and store phases only overlap with other
-// CTAs'): float32 2 rows x 512 threads (64 KB + 32 KB twiddles, 2 CTAs per SM); float64 1 row x 256 threads
-// with the twiddle table read through L1 (TWG; 64 KB, 2 CTAs per SM at 128 registers).
+// CTAs'): one row x 256 threads per CTA with the twiddle table read through L1 (TWG): float32 32 KB,
+// 4 CTAs per SM at 64 registers; float64 64 KB, 2 CTAs per SM at 128 registers (measured on the B200 against
+// 4 rows x 1024 threads and 2 rows x 512 threads with SMEM twiddles: c4 652.7 -> 638 ms/step).
 template <class C, class TO, int NPT, int NT, bool TWG, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_fft_rowT(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
                                                   int lgL1, int lgM, int inv, double scale, const C* __restrict__ tw,
@@ -374,57 +375,28 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
   if (layout != kLayoutNatural) {
     static bool attrT = false;
     if (!attrT) {
-      cudaFuncSetAttribute(k_fft_rowT<C, TO, 16, (sizeof(C) == 8 ? 512 : 256), sizeof(C) == 16, 2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12288 * sizeof(C)));
-      cudaFuncSetAttribute(k_fft_rowT<C, C, 16, (sizeof(C) == 8 ? 512 : 256), sizeof(C) == 16, 2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12288 * sizeof(C)));
+      cudaFuncSetAttribute(k_fft_rowT<C, TO, 16, 256, true, (sizeof(C) == 8 ? 4 : 2)>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4096 * sizeof(C)));
+      cudaFuncSetAttribute(k_fft_rowT<C, C, 16, 256, true, (sizeof(C) == 8 ? 4 : 2)>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4096 * sizeof(C)));
       cudaFuncSetAttribute(k_fft_colT<C, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * sizeof(C)));
       attrT = true;
     }
-    constexpr int kTLgM = sizeof(C) == 8 ? 1 : 0, kTNT = sizeof(C) == 8 ? 512 : 256;
-    constexpr bool kTwg = sizeof(C) == 16;
-    static const bool alt_rows = std::getenv("JTFS_ROWT_ALT") != nullptr;   // A/B timing only
+    constexpr int kTLgM = 0, kTNT = 256, kTMinB = sizeof(C) == 8 ? 4 : 2;
+    constexpr bool kTwg = true;
     const int lgM = std::min(kTLgM, lgL1);
     const size_t smT = (size_t)((4096 << lgM) + (kTwg ? 0 : 4096)) * sizeof(C);
     C* io = reinterpret_cast<C*>(const_cast<TI*>(in));
-    if (alt_rows && sizeof(C) == 8) {   // A/B: float32 1 row x 256 threads, twiddles via L1, 4 CTAs per SM
-      static bool attrA = false;
-      if (!attrA) {
-        cudaFuncSetAttribute(k_fft_rowT<C, TO, 16, 256, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(4096 * sizeof(C)));
-        cudaFuncSetAttribute(k_fft_rowT<C, C, 16, 256, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(4096 * sizeof(C)));
-        attrA = true;
-      }
-      const size_t smA = (size_t)4096 * sizeof(C);
-      if (layout == kLayoutToT) {
-        dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
-        k_fft_colA<C><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw,
-                                                                        FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
-        dim3 gb((unsigned)L1, (unsigned)ri.count, (unsigned)B);
-        k_fft_rowT<C, TO, 16, 256, true, 4><<<gb, 256, smA, st>>>(io, out, ri, ro, lgL1, 0, inverse ? 1 : 0, scale, tw,
-                                                                   nullptr, nullptr);
-      } else {
-        dim3 gb((unsigned)L1, (unsigned)ri.count, (unsigned)B);
-        k_fft_rowT<C, C, 16, 256, true, 4><<<gb, 256, smA, st>>>(io, io, ri, ri, lgL1, 0, inverse ? 1 : 0, 1.0, tw,
-                                                                  FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
-        dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
-        k_fft_colT<C, TO><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, out, ri, ro, lgL1, L2, lgCW,
-                                                                            inverse ? 1 : 0, scale, tw);
-      }
-      count_launch(2);
-      return cudaGetLastError();
-    }
     if (layout == kLayoutToT) {   // natural -> T: columns (twiddled, in place), then rows stored in place
       dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
       k_fft_colA<C><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw,
                                                                       FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
       dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
-      k_fft_rowT<C, TO, 16, kTNT, kTwg, 2><<<gb, kTNT, smT, st>>>(io, out, ri, ro, lgL1, lgM, inverse ? 1 : 0, scale,
+      k_fft_rowT<C, TO, 16, kTNT, kTwg, kTMinB><<<gb, kTNT, smT, st>>>(io, out, ri, ro, lgL1, lgM, inverse ? 1 : 0, scale,
                                                                  tw, nullptr, nullptr);
     } else {                      // T -> natural: rows (twiddled on store, in place), then columns out of place
       dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
-      k_fft_rowT<C, C, 16, kTNT, kTwg, 2><<<gb, kTNT, smT, st>>>(io, io, ri, ri, lgL1, lgM, inverse ? 1 : 0, 1.0, tw,
+      k_fft_rowT<C, C, 16, kTNT, kTwg, kTMinB><<<gb, kTNT, smT, st>>>(io, io, ri, ri, lgL1, lgM, inverse ? 1 : 0, 1.0, tw,
                                                                FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
       dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
       k_fft_colT<C, TO><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, out, ri, ro, lgL1, L2, lgCW,
