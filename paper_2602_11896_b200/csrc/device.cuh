@@ -19,6 +19,7 @@ struct TcClass {
   int K2max = 0, Kmax = 0, kcw = 32, kb2 = 8;
   int cls = 0;                     // kernel variant (TcBlock::cls)
   int ks = 0, nparts = 1;          // split-K block: K parts of the forward
+  int hyb = 0;                     // forward hybrid one-part mode (TcBlock::hyb)
   int ngmax = 1;                   // filter groups the launch may use (TcBlock::ngmax)
   int64_t n_cols = 0;              // columns of the block
   int bi = 0;                      // block index
@@ -181,8 +182,8 @@ void launch_phiT_adj(const Plan& p, const DeviceTables& d, const float* r, int64
 // the per-block launches go round-robin over the ns streams ss (forked from and joined to the caller's)
 // split-K blocks accumulate W in wbuf (per-signal stride wb_sb) and leave it there when keep_w (backward)
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, uint64_t own, int B,
-                         const cudaStream_t* ss, int ns);
+                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, const float* thr, uint64_t own,
+                         int B, const cudaStream_t* ss, int ns);
 void launch_joint_bwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, const float* go,
                          int64_t go_sb, float2* gY, int64_t gy_sb, const float* wbuf, int64_t wb_sb,
                          float2* gp, int64_t gp_sb, const float* thr, uint64_t own, int B,

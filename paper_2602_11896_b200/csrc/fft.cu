@@ -29,13 +29,11 @@ namespace jtfs {
 template <class C> struct FftTw;
 template <> struct FftTw<float2> {
   static const float2* base(const FftTables& t) { return t.twp; }
-  static const float2* lo(const FftTables& t, int lg) { return t.lo_f[lg]; }
-  static const float2* hi(const FftTables& t, int lg) { return t.hi_f[lg]; }
+  static const float2* tw2(const FftTables& t, int lg) { return t.tw2_f[lg]; }
 };
 template <> struct FftTw<double2> {
   static const double2* base(const FftTables& t) { return t.twpd; }
-  static const double2* lo(const FftTables& t, int lg) { return t.lo_d[lg]; }
-  static const double2* hi(const FftTables& t, int lg) { return t.hi_d[lg]; }
+  static const double2* tw2(const FftTables& t, int lg) { return t.tw2_d[lg]; }
 };
 
 // SMEM copy of the per-pass twiddle table of length L = 2^lgL (fft_pass_tables; cf_pass with lgT = -1)
@@ -117,7 +115,8 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 2 : 1) k_fft_small_multi
 
 // ---------------------------------------------------------------- four-step A: columns
 // x viewed as [L1][L2] (n = n1 L2 + n2). For the CTA's CW columns n2: y[k1][n2] = sum_n1 x[n1][n2]
-// W_L1^{n1 k1}, times W_L^{n2 k1}, written back in place. W_L^e (e = n2 k1 < L) = lo[e & 4095] hi[e >> 12].
+// W_L1^{n1 k1}, times W_L^{n2 k1}, written back in place. W_L^{n2 k1} = tw2[k1 4096 + n2] (fft_fourstep_table:
+// consecutive columns read consecutive words).
 template <class C>
 struct LdCols {
   const C* base;   // row n1 at base + n1 * L2
@@ -128,11 +127,9 @@ template <class C>
 struct StColsTw {
   C* base;
   int L2, c0, inv;
-  const C* lo;
-  const C* hi;
+  const C* tw2;
   __device__ __forceinline__ void operator()(int c, int k1, C v) const {
-    const int e = (c0 + c) * k1;
-    C w = cmul_f(lo[e & 4095], hi[e >> 12]);
+    C w = tw2[((int64_t)k1 << 12) + c0 + c];
     if (inv) w.y = -w.y;
     base[(int64_t)k1 * L2 + c] = cmul_f(v, w);
   }
@@ -140,8 +137,7 @@ struct StColsTw {
 
 template <class C>
 __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) k_fft_colA(C* __restrict__ data, Rows ri, int lgL1, int L2, int lgCW, int inv,
-                                                  const C* __restrict__ tw, const C* __restrict__ lo,
-                                                  const C* __restrict__ hi) {
+                                                  const C* __restrict__ tw, const C* __restrict__ tw2) {
   extern __shared__ __align__(16) uint8_t smraw[];
   C* s = reinterpret_cast<C*>(smraw);                  // [L1][CW] interleaved
   C* tws = s + (1 << (lgL1 + lgCW));                   // [L1]
@@ -153,7 +149,7 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) k_fft_colA(C* __r
   load_twiddles<C, 256>(tws, tw, lgL1);
   __syncthreads();
   const LdCols<C> ld{base, L2};
-  const StColsTw<C> st{base, L2, c0, inv, lo, hi};
+  const StColsTw<C> st{base, L2, c0, inv, tw2};
   const SeqInter<C> buf{s, 1 << lgCW};
   seq_fft<C, 256, 16>(lgCW, lgL1, inv != 0, tws, -1, ld, st, buf);
 }
@@ -189,16 +185,14 @@ __global__ void __launch_bounds__(NT) k_fft_rowB(const C* __restrict__ in, TO* _
 
 // ---------------------------------------------------------------- "T-layout" passes (no transposition)
 template <class C, class TO>
-struct StRowT {  // row m of the CTA at dst + m * 4096, element n2; T -> natural twiddle W_L^{(k10 + m) n2} if lo
+struct StRowT {  // row m of the CTA at dst + m * 4096, element n2; T -> natural twiddle W_L^{(k10 + m) n2} if tw2
   TO* dst;
   int k10, inv;
   typename Cx<C>::R sc;
-  const C* lo;
-  const C* hi;
+  const C* tw2;
   __device__ __forceinline__ void operator()(int m, int n2, C v) const {
-    if (lo) {
-      const int e = (k10 + m) * n2;
-      C w = cmul_f(lo[e & 4095], hi[e >> 12]);
+    if (tw2) {
+      C w = tw2[((int64_t)(k10 + m) << 12) + n2];
       if (inv) w.y = -w.y;
       v = cmul_f(v, w);
     }
@@ -217,7 +211,7 @@ struct StRowT {  // row m of the CTA at dst + m * 4096, element n2; T -> natural
 template <class C, class TO, int NPT, int NT, bool TWG, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_fft_rowT(const C* __restrict__ in, TO* __restrict__ out, Rows ri, Rows ro,
                                                   int lgL1, int lgM, int inv, double scale, const C* __restrict__ tw,
-                                                  const C* __restrict__ lo, const C* __restrict__ hi) {
+                                                  const C* __restrict__ tw2) {
   extern __shared__ __align__(16) uint8_t smraw[];
   constexpr int lgL2 = 12, L2 = 4096;
   C* s = reinterpret_cast<C*>(smraw);                 // [M][L2] swizzled
@@ -240,7 +234,7 @@ __global__ void __launch_bounds__(NT, MINB) k_fft_rowT(const C* __restrict__ in,
   // the last radix-16 pass stores straight to global memory (consecutive threads hold consecutive n2 of a
   // row: coalesced), with the T -> natural twiddle and the scale applied on the way; in place is safe (every
   // load of the CTA's rows happens in the first pass)
-  const StRowT<C, TO> st{dst, k10, inv, (typename Cx<C>::R)scale, lo, hi};
+  const StRowT<C, TO> st{dst, k10, inv, (typename Cx<C>::R)scale, tw2};
   seq_fft<C, NT, NPT>(lgM, lgL2, inv != 0, tws, -1, ld, st, buf);
 }
 
@@ -312,25 +306,21 @@ std::vector<float2> fft_pass_tables() { return pass_tables<float2>(); }
 std::vector<double2> fft_pass_tables_d() { return pass_tables<double2>(); }
 std::vector<double2> fft_twiddle_table_d() { return twiddles<double2>(); }
 
-// four-step twiddles W_L^e = lo[e & 4095] * hi[e >> 12] for L = 2^lgL > 4096 (float64 evaluation)
+// four-step twiddles for L = 2^lgL > 4096: tw2[k1 4096 + n2] = W_L^{k1 n2}, k1 < L / 4096, n2 < 4096 (float64
+// evaluation of the reduced exponent; one table of L entries per length)
 template <class T>
-static void fourstep_tables(int lgL, std::vector<T>* lo, std::vector<T>* hi) {
-  const double L = std::ldexp(1.0, lgL);
-  lo->resize(4096);
-  hi->resize((size_t)1 << (lgL - 12));
-  for (int e = 0; e < 4096; ++e) {
-    const double a = -2.0 * 3.14159265358979323846 * (double)e / L;
-    (*lo)[e].x = (decltype((*lo)[e].x))std::cos(a);
-    (*lo)[e].y = (decltype((*lo)[e].y))std::sin(a);
-  }
-  for (size_t e = 0; e < hi->size(); ++e) {
-    const double a = -2.0 * 3.14159265358979323846 * (double)(e * 4096) / L;
-    (*hi)[e].x = (decltype((*hi)[e].x))std::cos(a);
-    (*hi)[e].y = (decltype((*hi)[e].y))std::sin(a);
-  }
+static void fourstep_table(int lgL, std::vector<T>* t) {
+  const int64_t L = int64_t(1) << lgL, L1 = L >> 12;
+  t->resize((size_t)L);
+  for (int64_t k1 = 0; k1 < L1; ++k1)
+    for (int64_t n2 = 0; n2 < 4096; ++n2) {
+      const double a = -2.0 * 3.14159265358979323846 * (double)((k1 * n2) & (L - 1)) / (double)L;
+      (*t)[(size_t)((k1 << 12) + n2)].x = (decltype((*t)[0].x))std::cos(a);
+      (*t)[(size_t)((k1 << 12) + n2)].y = (decltype((*t)[0].x))std::sin(a);
+    }
 }
-void fft_fourstep_tables_f(int lgL, std::vector<float2>* lo, std::vector<float2>* hi) { fourstep_tables(lgL, lo, hi); }
-void fft_fourstep_tables_d(int lgL, std::vector<double2>* lo, std::vector<double2>* hi) { fourstep_tables(lgL, lo, hi); }
+void fft_fourstep_table_f(int lgL, std::vector<float2>* t) { fourstep_table(lgL, t); }
+void fft_fourstep_table_d(int lgL, std::vector<double2>* t) { fourstep_table(lgL, t); }
 
 static int ilog2_exact(int64_t v) {
   int l = 0;
@@ -390,14 +380,14 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
     if (layout == kLayoutToT) {   // natural -> T: columns (twiddled, in place), then rows stored in place
       dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
       k_fft_colA<C><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw,
-                                                                      FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+                                                                      FftTw<C>::tw2(T, lgL));
       dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
       k_fft_rowT<C, TO, 16, kTNT, kTwg, kTMinB><<<gb, kTNT, smT, st>>>(io, out, ri, ro, lgL1, lgM, inverse ? 1 : 0, scale,
-                                                                 tw, nullptr, nullptr);
+                                                                 tw, nullptr);
     } else {                      // T -> natural: rows (twiddled on store, in place), then columns out of place
       dim3 gb((unsigned)(L1 >> lgM), (unsigned)ri.count, (unsigned)B);
       k_fft_rowT<C, C, 16, kTNT, kTwg, kTMinB><<<gb, kTNT, smT, st>>>(io, io, ri, ri, lgL1, lgM, inverse ? 1 : 0, 1.0, tw,
-                                                               FftTw<C>::lo(T, lgL), FftTw<C>::hi(T, lgL));
+                                                               FftTw<C>::tw2(T, lgL));
       dim3 ga((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
       k_fft_colT<C, TO><<<ga, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(io, out, ri, ro, lgL1, L2, lgCW,
                                                                           inverse ? 1 : 0, scale, tw);
@@ -408,8 +398,7 @@ static cudaError_t fft_launch_t(const TI* in, TO* out, Rows ri, Rows ro, int B, 
   {
     dim3 grid((unsigned)(L2 >> lgCW), (unsigned)ri.count, (unsigned)B);
     k_fft_colA<C><<<grid, 256, (size_t)(4096 + L1) * sizeof(C), st>>>(
-        reinterpret_cast<C*>(const_cast<TI*>(in)), ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw, FftTw<C>::lo(T, lgL),
-        FftTw<C>::hi(T, lgL));
+        reinterpret_cast<C*>(const_cast<TI*>(in)), ri, lgL1, L2, lgCW, inverse ? 1 : 0, tw, FftTw<C>::tw2(T, lgL));
   }
   {
     const int lgM = std::min(kRowLgM, lgL1);

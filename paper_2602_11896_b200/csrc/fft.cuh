@@ -7,17 +7,16 @@
 #include "common.cuh"
 
 namespace jtfs {
-// Device twiddle tables: the 4096-entry W_4096^e tables (float, double) and, per length 2^lg > 4096, the
-// two-level four-step tables W_L^e = lo[e & 4095] * hi[e >> 12].
+// Device twiddle tables: the 4096-entry W_4096^e tables (float, double) and, per length L = 2^lg > 4096, the
+// four-step table tw2[k1 4096 + n2] = W_L^{k1 n2} (k1 < L / 4096): the column pass (consecutive columns n2)
+// and the T -> natural row pass (consecutive n2) read it coalesced.
 struct FftTables {
   const float2* tw = nullptr;
   const double2* twd = nullptr;
   const float2* twp = nullptr;     // per-pass tables (fft_pass_tables), lengths 2 .. 4096
   const double2* twpd = nullptr;
-  const float2* lo_f[23] = {};
-  const float2* hi_f[23] = {};
-  const double2* lo_d[23] = {};
-  const double2* hi_d[23] = {};
+  const float2* tw2_f[23] = {};
+  const double2* tw2_d[23] = {};
 };
 // Out-of-place batched C2C FFT of B x ri.count rows of length ri.L (power of two, 2..2^22).
 // For L > 4096 the input rows are clobbered (four-step scheme runs its first step in place).
@@ -50,6 +49,6 @@ std::vector<float2> fft_twiddle_table();
 std::vector<float2> fft_pass_tables();
 std::vector<double2> fft_pass_tables_d();
 std::vector<double2> fft_twiddle_table_d();
-void fft_fourstep_tables_f(int lgL, std::vector<float2>* lo, std::vector<float2>* hi);
-void fft_fourstep_tables_d(int lgL, std::vector<double2>* lo, std::vector<double2>* hi);
+void fft_fourstep_table_f(int lgL, std::vector<float2>* t);
+void fft_fourstep_table_d(int lgL, std::vector<double2>* t);
 }  // namespace jtfs

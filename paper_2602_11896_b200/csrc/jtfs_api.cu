@@ -254,6 +254,7 @@ static cudaError_t upload(Plan& p) {
       c.K2max = (fwd && tb.ks) ? tb.kpw : tb.K2;
       c.ks = tb.ks;
       c.nparts = tb.nparts;
+      c.hyb = fwd ? tb.hyb : 0;
       c.ngmax = tb.ngmax;
       c.n_cols = p.binfo[tb.bi].n_cols;
       c.bi = tb.bi;
@@ -360,19 +361,18 @@ static cudaError_t upload(Plan& p) {
     d->fftt.twpd = c;
   }
   for (int lg = 13; lg <= 22 && (int64_t(1) << lg) <= p.N_pad; ++lg) {
-    std::vector<float2> lf, hf;
-    std::vector<double2> ld, hd;
-    fft_fourstep_tables_f(lg, &lf, &hf);
-    fft_fourstep_tables_d(lg, &ld, &hd);
-    float2 *a = nullptr, *b2 = nullptr;
-    double2 *c = nullptr, *e2 = nullptr;
-    if ((e = up(lf, &a)) != cudaSuccess || (e = up(hf, &b2)) != cudaSuccess || (e = up(ld, &c)) != cudaSuccess ||
-        (e = up(hd, &e2)) != cudaSuccess) {
+    std::vector<float2> tf;
+    std::vector<double2> td;
+    fft_fourstep_table_f(lg, &tf);
+    fft_fourstep_table_d(lg, &td);
+    float2* a = nullptr;
+    double2* c = nullptr;
+    if ((e = up(tf, &a)) != cudaSuccess || (e = up(td, &c)) != cudaSuccess) {
       free_tables(d);
       return e;
     }
-    d->fs_bufs.insert(d->fs_bufs.end(), {(void*)a, (void*)b2, (void*)c, (void*)e2});
-    d->fftt.lo_f[lg] = a; d->fftt.hi_f[lg] = b2; d->fftt.lo_d[lg] = c; d->fftt.hi_d[lg] = e2;
+    d->fs_bufs.insert(d->fs_bufs.end(), {(void*)a, (void*)c});
+    d->fftt.tw2_f[lg] = a; d->fftt.tw2_d[lg] = c;
   }
   d->maxLf = (int)p.P;
   // FFT route tables and block lists
@@ -572,7 +572,7 @@ static cudaError_t run_forward(const Plan& p, const float* x, int64_t sx, int mb
     Fanout* fo = fanout_get(lane);
     fan_fork(fo, st);
     launch_joint_fft(p, d, false, w.Y2, w.s_Y2, w.o, w.s_o, nullptr, 0, nullptr, own, mb, fo->s[0]);
-    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.Wk, w.s_Wk, keep_w, own, mb, fo->s + 1,
+    launch_joint_fwd_tc(p, d, w.Y2, w.s_Y2, w.o, w.s_o, w.Wk, w.s_Wk, keep_w, w.thr, own, mb, fo->s + 1,
                         kFanStreams - 1);
     launch_joint_fwd(p, d, w.Y2, w.s_Y2, w.o, w.s_o, own, mb, fo->s[0]);
     fan_join(fo, st);
@@ -905,10 +905,11 @@ static jtfs_status loss_grad_impl(jtfs_plan_t plan, const float* y, const float*
     Bufs w = carve(p, L, (char*)ws + (size_t)l * mbl * L.per_signal(), mbl);
     for (int64_t b0 = (int64_t)l * mbl; b0 < B; b0 += (int64_t)lanes * mbl) {
     int n = (int)std::min<int64_t>(mbl, B - b0);
+    // R22 dead zone first: the forward's phase store (split-K blocks) decides it on the final W
+    launch_mod_threshold(y + b0 * p.N, p.N, kEpsMod, w.thr, n, ls);
     CK(run_forward(p, y + b0 * p.N, p.N, n, w.S, w.s_S, w, own, ls, 0, true, l));
     float* lossp = mstate ? mstate->loss + b0 : loss + b0;
     launch_loss(p, *p.dev, w.S, w.s_S, St + b0 * p.n_coef, p.n_coef, w.r, w.s_S, lossp, (double*)w.loss, own, n, ls);
-    launch_mod_threshold(y + b0 * p.N, p.N, kEpsMod, w.thr, n, ls);
     float* gp = mstate ? w.g : grad + b0 * p.N;
     int64_t sg = mstate ? w.s_g : p.N;
     CK(run_backward(p, w, gp, sg, n, own, ls, l));

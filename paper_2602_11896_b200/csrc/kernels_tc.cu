@@ -67,7 +67,7 @@ __device__ __forceinline__ void build_a(float* a_hi, float* a_lo, const float2* 
     tc::split_tf32(v.x, h0, l0);
     tc::split_tf32(v.y, h1, l1);
     const uint32_t o = tc::core_off((uint32_t)c, (uint32_t)(2 * n), (uint32_t)K2) / 4;
-    *reinterpret_cast<float2*>(a_hi + o) = make_float2(h0, h1);
+    if (a_hi) *reinterpret_cast<float2*>(a_hi + o) = make_float2(h0, h1);
     *reinterpret_cast<float2*>(a_lo + o) = make_float2(l0, l1);
   }
 }
@@ -87,8 +87,12 @@ struct TcArgs {
   int ng;                           // filter groups: CTA x handles column tile x % ntiles, filters f = x / ntiles mod ng
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
   int fexpt;                        // timing experiments only (JTFS_TC_FEXPT: 1 no W loads, 2 no W stores)
+  const float* thr;                 // per-signal modulus dead zone (R22), for the kept phase store
 };
-constexpr int kPmLoad = 1, kPmStore = 2, kPmFinish = 4;
+// K-part modes: load / store the fp32 W partials, finish (modulus, phi_F), and keep the phase of the final W
+// for the backward (kPmPhase, "phase store": the backward needs only W/|W| and the dead-zone decision)
+constexpr int kPmLoad = 1, kPmStore = 2, kPmFinish = 4, kPmPhase = 8;
+constexpr float kPhaseScale = 32767.f;   // phase store: 2 x int16 fixed point per cell (|error| <= 1.6e-5)
 static const int g_tc_fexpt = [] {
   const char* e = std::getenv("JTFS_TC_FEXPT");
   return e ? std::atoi(e) : 0;
@@ -126,10 +130,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   const int kp_lo = TB.ks ? a.part * TB.kpw : 0;            // k' range of this launch (split-K blocks)
   const int K2 = TB.ks ? min(TB.kpw, TB.K2 - kp_lo) : TB.K2;
   const int pmode = TB.ks ? a.pmode : kPmFinish;
-  const bool tsa = tc_fwd_tsa(CT, K2);                     // A in TMEM (TS-form MMAs)
-  const int nbuf = tc_fwd_nbuf(CT, K2);                    // TMEM accumulator buffers
+  // A (the Y2 tile, tf32 hi/lo) placement: both halves in TMEM (tsa, TS-form MMAs), both in SMEM (SS form),
+  // or hybrid (hyb, CT = 1): A_hi in TMEM and A_lo in SMEM -- a whole K up to 384 in one part, so split-K
+  // blocks need no fp32 W partials round trip through HBM
+  const bool hyb = TB.hyb != 0;
+  const bool tsa = !hyb && tc_fwd_tsa(CT, K2);            // A in TMEM (TS-form MMAs)
+  const int nbuf = hyb ? (256 + K2 <= 512 ? 2 : 1) : tc_fwd_nbuf(CT, K2);   // TMEM accumulator buffers
   float* a_hi = reinterpret_cast<float*>(sm);              // [CT][128][K2] canonical (SS form)
-  float* a_lo = a_hi + CT * 128 * K2;
+  float* a_lo = hyb ? a_hi : a_hi + CT * 128 * K2;         // hybrid: only A_lo in SMEM
   float* bst = tsa ? a_hi : a_lo + CT * 128 * K2;           // NS stages x STG floats
   float* red = bst + NS * STG;                              // [CT][KAP][128]
 
@@ -138,12 +146,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
     tc::fence_mbar_init();
   }
-  const int tcols = (CT == 1 && !tsa) ? 256 : 512;
+  const int tcols = (CT == 1 && !tsa && !hyb) ? 256 : 512;
   if (warp == 1) tc::tmem_alloc(&tmem_base, tcols);
   const float2* ysrc = a.Y2 + b * a.y_sb + bf.y_off;
-  if (!tsa)
+  if (!tsa && !hyb)
     for (int m = 0; m < CT; ++m)
       build_a(a_hi + m * 128 * K2, a_lo + m * 128 * K2, ysrc, bf, col0 + m * 128, K, K2, tid, kTcThreads, kp_lo / 2);
+  if (hyb) build_a(nullptr, a_lo, ysrc, bf, col0, K, K2, tid, kTcThreads, kp_lo / 2);
   tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   const uint32_t tbase = tmem_base;
   // TS form: A hi at TMEM columns [256, 256 + K2), lo at [256 + K2, 256 + 2 K2)
   const uint32_t taa_hi = tbase + 128 * (uint32_t)nbuf, taa_lo = taa_hi + (uint32_t)K2;
-  if (tsa) {
+  if (tsa || hyb) {
     if (warp >= 4 && warp < 8) {
       const uint32_t lq = (uint32_t)((warp & 3) * 32) << 16;
       const int64_t col = col0 + (warp & 3) * 32 + lane;
@@ -169,10 +178,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
         }
         if (K2 - k0 >= 16) {
           tc::tmem_st16(taa_hi + lq + (uint32_t)k0, hi);
-          tc::tmem_st16(taa_lo + lq + (uint32_t)k0, lo);
+          if (!hyb) tc::tmem_st16(taa_lo + lq + (uint32_t)k0, lo);
         } else {
           tc::tmem_st8(taa_hi + lq + (uint32_t)k0, hi);
-          tc::tmem_st8(taa_lo + lq + (uint32_t)k0, lo);
+          if (!hyb) tc::tmem_st8(taa_lo + lq + (uint32_t)k0, lo);
         }
       }
       tc::tmem_wait_st();
@@ -268,6 +277,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
                 tc::mma_tf32_ts(dbase, taa_hi + 8u * kg, dB_hi + 16u * ks, idesc, (ch > 0 || ks > 0) ? 1u : 0u);
                 tc::mma_tf32_ts(dbase, taa_hi + 8u * kg, dB_lo + 16u * ks, idesc, 1u);
                 tc::mma_tf32_ts(dbase, taa_lo + 8u * kg, dB_hi + 16u * ks, idesc, 1u);
+              } else if (hyb) {   // A_hi from TMEM (TS form), A_lo from SMEM (SS form)
+                tc::mma_tf32_ts(dbase, taa_hi + 8u * kg, dB_hi + 16u * ks, idesc, (ch > 0 || ks > 0) ? 1u : 0u);
+                tc::mma_tf32_ts(dbase, taa_hi + 8u * kg, dB_lo + 16u * ks, idesc, 1u);
+                tc::mma_tf32(dbase, dA_lo + 16u * kg, dB_hi + 16u * ks, idesc, 1u);
               } else {
 #pragma unroll
                 for (int m = 0; m < CT; ++m) {
@@ -359,10 +372,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
                 v[4 * i] += w.x; v[4 * i + 1] += w.y; v[4 * i + 2] += w.z; v[4 * i + 3] += w.w;
               }
             }
-            if ((pmode & kPmStore) && !(a.fexpt & 2)) {
+            if ((pmode & kPmStore) && !(pmode & kPmPhase) && !(a.fexpt & 2)) {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
                 wp[i * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+            if ((pmode & kPmPhase) && !(a.fexpt & 2)) {
+              // phase store: per cell (c, s) = round(32767 W/|W|) as two int16 (0 in the R22 dead zone, decided
+              // here on the final fp32 W exactly as the backward's recompute path decides it); per (column
+              // tile, 64-row tile) [16-byte group][column c], 4 rows per group, so a warp's 32 columns of one
+              // group are 512 contiguous bytes; half the bytes of the fp32 W
+              const float th2 = fmaxf(a.thr[b] * a.thr[b], 1.17549435e-38f);
+              // half h's groups start at h * wph / 256: with fp32 partials in the tile (wph = 4096) that is the
+              // start of the half's own partial region, which only this thread (column c) has read -- the
+              // store never overwrites a partial another thread still has to load
+              uint4* pq = reinterpret_cast<uint4*>(a.wbuf + b * a.wb_sb + TB.wp_off) +
+                          ((int64_t)ct * TB.wp_tiles + tu.wp_tile0 + t) * TB.wph + (h * (TB.wph >> 8)) * 128 + c;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                uint32_t wd[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                  const float re = v[8 * i + 2 * q4], im = v[8 * i + 2 * q4 + 1];
+                  const float m2 = fmaf(re, re, im * im);
+                  int cs = 0, sn = 0;
+                  if (m2 > th2) {
+                    const float sc = kPhaseScale * rsqrtf(m2);
+                    cs = __float2int_rn(fminf(fmaxf(re * sc, -kPhaseScale), kPhaseScale));
+                    sn = __float2int_rn(fminf(fmaxf(im * sc, -kPhaseScale), kPhaseScale));
+                  }
+                  wd[q4] = (uint32_t)(uint16_t)(int16_t)cs | ((uint32_t)(uint16_t)(int16_t)sn << 16);
+                }
+                pq[i * 128] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+              }
             }
             if (!(pmode & kPmFinish)) continue;
           }
@@ -411,15 +453,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   if (warp == 1) tc::tmem_dealloc(tbase, tcols);
 }
 
-static size_t tc_fwd_smem(int CT, int KAP, int NS, int K2, int STG) {
-  return (size_t)((tc_fwd_tsa(CT, K2) ? 0 : 2 * CT * 128 * K2) + NS * STG + CT * KAP * 128) * 4 + 1024;
+static size_t tc_fwd_smem(int CT, int KAP, int NS, int K2, int STG, bool hyb = false) {
+  const size_t a = hyb ? (size_t)128 * K2 : (tc_fwd_tsa(CT, K2) ? 0 : (size_t)2 * CT * 128 * K2);
+  return (a + NS * STG + CT * KAP * 128) * 4 + 1024;
 }
 
-// forward B ring stages that fit (the planner rejects chunk widths that leave fewer than 3)
-int tc_fwd_stages(int CT, int KAP, int K2, int kcw) {
+// forward B ring stages that fit (the planner rejects chunk widths that leave fewer than 3; 2 in hybrid mode)
+int tc_fwd_stages(int CT, int KAP, int K2, int kcw, bool hyb) {
   const int STG = 2 * kTcN * kcw;
   int NS = kTcMaxStages;
-  while (NS > 0 && tc_fwd_smem(CT, KAP, NS, K2, STG) > 224 * 1024) --NS;
+  while (NS > 0 && tc_fwd_smem(CT, KAP, NS, K2, STG, hyb) > 224 * 1024) --NS;
   return NS;
 }
 
@@ -440,8 +483,8 @@ static int tc_groups(const TcClass& C, int B) {
 template <int CT, int KAP>
 static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st) {
   const int STG = 2 * kTcN * C.kcw;
-  const int NS = tc_fwd_stages(CT, KAP, C.K2max, C.kcw);
-  const size_t sm = tc_fwd_smem(CT, KAP, NS, C.K2max, STG);
+  const int NS = tc_fwd_stages(CT, KAP, C.K2max, C.kcw, C.hyb != 0);
+  const size_t sm = tc_fwd_smem(CT, KAP, NS, C.K2max, STG, C.hyb != 0);
   cudaFuncSetAttribute(k_joint_fwd_tc<CT, KAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 g((unsigned)(C.ntiles * a.ng), (unsigned)B);
   k_joint_fwd_tc<CT, KAP><<<g, kTcThreads, sm, st>>>(a, NS, STG);
@@ -449,7 +492,7 @@ static void launch_tc(const TcArgs& a, const TcClass& C, int B, cudaStream_t st)
 }
 
 void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2, int64_t y_sb, float* o,
-                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, uint64_t own, int B,
+                         int64_t o_sb, float* wbuf, int64_t wb_sb, bool keep_w, const float* thr, uint64_t own, int B,
                          const cudaStream_t* ss, int ns) {
   int li = 0;
   for (const TcClass& C : d.tc) {
@@ -459,11 +502,11 @@ void launch_joint_fwd_tc(const Plan& p, const DeviceTables& d, const float2* Y2,
     for (int part = 0; part < nparts; ++part) {   // split-K parts run in order on one stream
       int pmode = kPmFinish;
       if (C.ks) {
-        pmode = (part > 0 ? kPmLoad : 0) | (part < nparts - 1 || keep_w ? kPmStore : 0) |
-                (part == nparts - 1 ? kPmFinish : 0);
+        pmode = (part > 0 ? kPmLoad : 0) | (part < nparts - 1 ? kPmStore : 0) |
+                (part == nparts - 1 ? kPmFinish | (keep_w ? kPmPhase : 0) : 0);
       }
       TcArgs a{Y2, y_sb, o, o_sb, d.units, d.binfo, C.blocks, C.tiles, C.n_blocks, d.tc_img, d.tc_wts, d.tc_units,
-               (int)p.L_fr.size(), own, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr, g_tc_fexpt};
+               (int)p.L_fr.size(), own, wbuf, wb_sb, part, pmode, tc_groups(C, B), nullptr, g_tc_fexpt, thr};
 #ifdef JTFS_TC_TRACE
       static long long* ftrace = nullptr;
       if (!ftrace) cudaMalloc(&ftrace, 16 * 512 * 8);
@@ -789,19 +832,20 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         gor[r] = (r < U.rows_out && colg < bf.n_cols) ? a.go[b * a.go_sb + U.o_off + (int64_t)r * bf.n_cols + colg]
                                                        : 0.f;
     };
-    // split-K mode: W of (tile, column, this warp's 8 rows) from the forward's buffer, one tile ahead
-    // forward's W layout per (column tile, 64-row tile): [float4 group g][column], g = (2 row + re/im) / 4
-    const float4* wcol = ksm ? reinterpret_cast<const float4*>(a.wbuf + b * a.wb_sb + TB.wp_off) +
-                                   (int64_t)ct * TB.wp_tiles * (128 * 32) + (h * 4) * 128 + c
-                             : nullptr;
-    auto load_wv = [&](int u, int t32, float4* wv) {
-      const float4* q4 = wcol + (int64_t)(a.tcu[u].wp_tile0 + (t32 >> 1)) * (128 * 32) + ((t32 & 1) * 16) * 128;
+    // split-K mode: the phase of W (tile, column, this warp's 8 rows) from the forward's phase store, one
+    // tile ahead; layout per (column tile, 64-row tile): [16-byte group][column], 2 x int16 per cell, row r in
+    // group (r / 32) * wph / 256 + (r % 32) / 4
+    const uint4* wcol = ksm ? reinterpret_cast<const uint4*>(a.wbuf + b * a.wb_sb + TB.wp_off) +
+                                  (int64_t)ct * TB.wp_tiles * TB.wph + (h * 2) * 128 + c
+                            : nullptr;
+    auto load_wv = [&](int u, int t32, uint4* wv) {
+      const uint4* q4 = wcol + (int64_t)(a.tcu[u].wp_tile0 + (t32 >> 1)) * TB.wph + ((t32 & 1) * (TB.wph >> 8)) * 128;
 #pragma unroll
-      for (int i = 0; i < kBwRpw / 2; ++i) wv[i] = q4[i * 128];
+      for (int i = 0; i < kBwRpw / 4; ++i) wv[i] = q4[i * 128];
     };
     int f = next_unit(0);
     float gor_n[KAP];
-    float4 wv_n[kBwRpw / 2];
+    uint4 wv_n[kBwRpw / 4];
     if (f < a.nfr) {
       pf_w(TB.bi * a.nfr + f, 0);
       load_go(TB.bi * a.nfr + f, gor_n);
@@ -836,10 +880,16 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           }
         }
         float v[2 * kBwRpw];
-        if (ksm) {
+        if (ksm) {   // decode the phase store: (re, im) = W/|W| (0 in the dead zone)
+          constexpr float kInv = 1.f / kPhaseScale;
 #pragma unroll
-          for (int i = 0; i < kBwRpw / 2; ++i) {
-            v[4 * i] = wv_n[i].x; v[4 * i + 1] = wv_n[i].y; v[4 * i + 2] = wv_n[i].z; v[4 * i + 3] = wv_n[i].w;
+          for (int i = 0; i < kBwRpw / 4; ++i) {
+            const uint32_t wd[4] = {wv_n[i].x, wv_n[i].y, wv_n[i].z, wv_n[i].w};
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              v[8 * i + 2 * q4] = (float)(int16_t)(wd[q4] & 0xffffu) * kInv;
+              v[8 * i + 2 * q4 + 1] = (float)(int16_t)(wd[q4] >> 16) * kInv;
+            }
           }
         }
         if (t + 1 < NT32) {
@@ -871,8 +921,13 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         for (int i = 0; i < kBwRpw; ++i) {
           // g_W = (W/|W|) Phi_F^T g_o (Eq.4 adjoint, modulus adjoint with the R22 dead zone)
           const float re = v[2 * i], im = v[2 * i + 1];
-          const float m2 = fmaf(re, re, im * im);
-          const float s = m2 > th2 ? gv[i] * tc::rsqrt_approx(m2) : 0.f;
+          float s;
+          if (ksm) {
+            s = gv[i];                                   // (re, im) is already the phase (or 0)
+          } else {
+            const float m2 = fmaf(re, re, im * im);
+            s = m2 > th2 ? gv[i] * tc::rsqrt_approx(m2) : 0.f;
+          }
           // (re, im) s and the lo halves as packed pairs (FMUL2 / FADD2); hi rounded on the integer pipe
           const float2 g2 = tc::mul2(make_float2(re, im), make_float2(s, s));
           const float2 h2 = make_float2(tc::tf32_rna(g2.x), tc::tf32_rna(g2.y));

@@ -74,8 +74,13 @@ struct TcBlock {
   int32_t ks, nparts;        // split-K block (A tile too large for SMEM): number of K parts
   int32_t kpw, wp_tiles;     // part width (k' elements, multiple of kcw); 64-row tiles per column tile
   int64_t wp_off;            // offset (floats, per signal) of the block's W buffer
-  int32_t ngmax, pad2;       // filter groups a launch may split into (few column tiles -> more CTAs)
+  int32_t ngmax;             // filter groups a launch may split into (few column tiles -> more CTAs)
+  int32_t wph;               // 16-byte words per 64-row tile of the kept phase store (2048; 4096 when the
+                             // tile also carries fp32 K-part partials): see kernels_tc.cu "phase store"
   int64_t gp_off;            // backward: offset (complex, per signal) of the block's g_Y2 partials
+  int32_t hyb;               // forward "hybrid" one-part split-K: A_hi in TMEM (TS form), A_lo in SMEM (SS form),
+                             // for K2 too large for both halves in TMEM (kernels_tc.cu)
+  int32_t pad3;
 };
 // forward class = 8 * ct_kind + kap_kind (ct_kind 0: 2 column tiles, 1: one; KAP = 2 << kap_kind,
 // rows_out <= 2, 4, 8, 16, 32); backward class = kap_kind
@@ -101,7 +106,7 @@ void tc_bwd_mode(int K, int K2, int* nab, int* ta, int pref = 0) {
 int tc_bwd_mode_pref();   // host: JTFS_BWD_MODE (default 0)
 // backward B ring sizing shared by the planner (chooses kb2) and the launcher (kernels_tc.cu)
 void tc_bwd_rings(int K, int K2, int kcw, int kb2, int* NS1, int* STG1, int* NS2, int* STG2);
-int tc_fwd_stages(int CT, int KAP, int K2, int kcw);
+int tc_fwd_stages(int CT, int KAP, int K2, int kcw, bool hyb = false);
 // forward TMEM plan: the Y2 tile (hi + lo, 2 K2 columns) goes to TMEM and the MMAs take the TS form when
 // it fits beside the double-buffered accumulators (CT = 1: 2 x 128 columns); the SS form reads A and B
 // from SMEM at 8 KB per N = 128 MMA, which saturates SMEM bandwidth together with the B stream

@@ -202,7 +202,7 @@ static void build_tc_tables(Plan* p) {
     {
       int wpt = 0;
       for (int f = 0; f < nfr; ++f) wpt += (int)((p->units[bi * nfr + f].n_rows + 63) / 64);
-      w_bytes = (double)((p->binfo[bi].n_cols + 127) / 128) * wpt * 128 * 128 * 4;
+      w_bytes = (double)((p->binfo[bi].n_cols + 127) / 128) * wpt * 128 * 64 * 4;   // phase store, 4 B per cell
     }
     if (K2 >= ks1_min && CT == 1 && tc_fwd_tsa(1, K2) && kap <= 4 && w_bytes <= ks1_maxw) {
       ks = 1;
@@ -251,6 +251,28 @@ static void build_tc_tables(Plan* p) {
       kcw = best_w;
       kpw = ((K2 + nparts - 1) / nparts + kcw - 1) / kcw * kcw;
     }
+    // Hybrid one-part forward instead of K parts (kernels_tc.cu): A_hi in TMEM beside one or two
+    // accumulators (128 + K2 <= 512), A_lo in SMEM, so the forward keeps only the phase store (4 B per cell)
+    // instead of fp32 W partials (24-40 B per cell over 2-3 parts). B chunks of >= 24 k' keep the copy
+    // engine (~400 cycles per bulk copy) below the MMA time (24 cycles per k' of a 64-row tile); widest chunk
+    // with >= 3 stages, else >= 2. JTFS_HYB=0: off (A/B timing).
+    static const bool hyb_on = [] {
+      const char* e = std::getenv("JTFS_HYB");
+      return !(e && std::atoi(e) == 0);
+    }();
+    int hyb = 0;
+    if (hyb_on && ks && nparts > 1 && CT == 1 && 128 + K2 <= 512 && w_bytes <= ks1_maxw) {
+      int wbest = 0;
+      for (int need = 3; need >= 2 && !wbest; --need)
+        for (int w = 64; w >= 24; w -= 8)
+          if (w <= K2 && tc_fwd_stages(1, 2 << kap, K2, w, true) >= need) { wbest = w; break; }
+      if (wbest) {
+        hyb = 1;
+        nparts = 1;
+        kcw = wbest;
+        kpw = K2;
+      }
+    }
     p->blk_tc[bi] = 1;
     p->blk_ks[bi] = (char)ks;
     // backward chunk widths: GEMM1 images (kcwb, own layout) and B2 images (kb2), chosen for the fewest bulk
@@ -274,7 +296,10 @@ static void build_tc_tables(Plan* p) {
     for (int f = 0; f < nfr; ++f) wp_tiles += (int)((p->units[bi * nfr + f].n_rows + 63) / 64);
     const int64_t n_ct = (p->binfo[bi].n_cols + 127) / 128;
     const int64_t wp_off = ks ? p->ks_w_floats : 0;
-    if (ks) p->ks_w_floats += n_ct * wp_tiles * 128 * 128;
+    // per 64-row tile: fp32 complex W partials (64 KB) for multi-part blocks; one-part blocks only ever hold
+    // the kept phase (2 x int16 per cell, 32 KB)
+    const int wph = nparts > 1 ? 4096 : 2048;
+    if (ks) p->ks_w_floats += n_ct * wp_tiles * 128 * (nparts > 1 ? 128 : 64);
     // launches with few column tiles split the filters over CTA groups: about two waves of 148 SMs for a
     // batch of kRefBatch signals. Fixed per plan (not per call), so every summation order and hence every
     // bit of a signal's result is independent of the batch / micro-batch it is computed in.
@@ -283,7 +308,7 @@ static void build_tc_tables(Plan* p) {
     const int ngmax =
         (int)std::min<int64_t>(nfr, std::max<int64_t>(1, (296 + n_tiles * kRefBatch - 1) / (n_tiles * kRefBatch)));
     p->tc_blocks.push_back({(int32_t)bi, K, K2, 8 * (CT == 2 ? 0 : 1) + kap, kcw, kb2, ks, nparts, kpw, wp_tiles,
-                            wp_off, ngmax, 0, 0});
+                            wp_off, ngmax, wph, 0, hyb, 0});
     int ns1, s1, ns2, s2;
     tc_bwd_rings(K, ks ? 0 : K2, kcwb, kb2, &ns1, &s1, &ns2, &s2);
     const bool bwd = best < (1 << 30) && (ks ? ns2 >= 2 : (N2 <= 256 && ns1 >= 2 && ns2 >= 2));
@@ -296,9 +321,9 @@ static void build_tc_tables(Plan* p) {
       }
       const int kw = ks ? kpw : K2;
       std::fprintf(stderr,
-                   "tc block %zu: K=%d K2=%d CT=%d KAP=%d ks=%d parts=%d kpw=%d kcw=%d fwdNS=%d nch=%d | bwd=%d kcwb=%d "
+                   "tc block %zu: K=%d K2=%d CT=%d KAP=%d ks=%d hyb=%d parts=%d kpw=%d kcw=%d fwdNS=%d nch=%d | bwd=%d kcwb=%d "
                    "kb2=%d ns1=%d ns2=%d | cols=%lld rows=%lld pad64=%lld pad32=%lld units=%d ng=%d\n",
-                   (size_t)bi, K, K2, CT, 2 << kap, ks, nparts, kpw, kcw, tc_fwd_stages(CT, 2 << kap, kw, kcw),
+                   (size_t)bi, K, K2, CT, 2 << kap, ks, hyb, nparts, kpw, kcw, tc_fwd_stages(CT, 2 << kap, kw, kcw, hyb != 0),
                    (kw + kcw - 1) / kcw, (int)bwd, kcwb, kb2, ns1, ns2, (long long)p->binfo[bi].n_cols,
                    (long long)rows, (long long)prow, (long long)prow32, nfr, ngmax);
     }
@@ -306,7 +331,7 @@ static void build_tc_tables(Plan* p) {
       p->blk_tcb[bi] = 1;
       const int ngb =
           (int)std::min<int64_t>(nfr, std::max<int64_t>(1, (296 + n_ct * kRefBatch - 1) / (n_ct * kRefBatch)));
-      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcwb, kb2, ks, nparts, kpw, wp_tiles, wp_off, ngb, 0,
+      p->tcb_blocks.push_back({(int32_t)bi, K, K2, kap, kcwb, kb2, ks, nparts, kpw, wp_tiles, wp_off, ngb, wph,
                                ngb > 1 ? p->gp_complex : 0});
       if (ngb > 1) p->gp_complex += (int64_t)ngb * K * p->binfo[bi].n_cols;
     }
