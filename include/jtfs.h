@@ -109,7 +109,9 @@ jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* S, 
  *   loss[b] = 1/2 sum_{orders 1,2} (S(y_b) - S_target_b)^2   (S0 excluded, R19)
  *   grad[b] = dE_b/dy_b, the TRUE gradient (the paper's "grad E" is its negative, R23).
  *   Modulus adjoint (R22): the phase z/|z| is 0 where |z| < 1e-12 * RMS(y_b), at
- *   every modulus site; elsewhere it is the exact phase (PyTorch autograd's).
+ *   every modulus site; elsewhere it is the exact phase (PyTorch autograd's). On the
+ *   split-K joint-stage blocks (large n1_max) the forward keeps that phase for the backward as
+ *   two int16 per cell (|error| <= 1.6e-5 on the unit vector).
  * y [B][N], S_target [B][n_coef], loss [B], grad [B][N]: device fp32.
  * shard/n_shards: second-order path shard (0,1 = whole; n_shards <= 64). With n_shards > 1 the call
  * computes the contribution of the second-order blocks jtfs_plan_shards assigns to `shard` (layer 2,
@@ -210,7 +212,7 @@ int64_t jtfs_launch_count(void);
  *  out[1] forward FP32 flops on the FFT-route blocks (per column: 5 P log2 P for FFT_P of y; per filter
  *         4 P fold + 5 L_f log2 L_f inverse FFT + 4 n_rows modulus + 2 rows_out n_rows phi_F)
  *  out[2] backward contraction flops on the tensor-core blocks (16 K per cell: recompute + adjoint;
- *         8 K on split-K blocks, whose backward reuses the W kept by the forward)
+ *         8 K on split-K blocks, whose backward reuses the phase of W kept by the forward)
  *  out[3] backward FP32 flops on the FFT-route blocks (recompute, phi_F adjoint, phase, DFT, spectrum
  *         accumulation, final inverse FFT_P)
  *  out[4] cells, out[5] HBM bytes of the joint stage (Y2 r fwd + r bwd, g_Y2 w, o w + g_o r). cap >= 8. */

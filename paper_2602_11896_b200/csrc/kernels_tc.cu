@@ -86,7 +86,8 @@ struct TcArgs {
   int part, pmode;                  // K part of this launch; kPm* bits
   int ng;                           // filter groups: CTA x handles column tile x % ntiles, filters f = x / ntiles mod ng
   long long* trace;                 // JTFS_TC_TRACE builds: per-tile event clocks of CTA (0, 0)
-  int fexpt;                        // timing experiments only (JTFS_TC_FEXPT: 1 no W loads, 2 no W stores)
+  int fexpt;                        // timing experiments only (JTFS_TC_FEXPT: 1 no W loads, 2 no W stores,
+                                    // 4 no B-image copies after the first two tiles, 8 no modulus / phi_F)
   const float* thr;                 // per-signal modulus dead zone (R22), for the kept phase store
 };
 // K-part modes: load / store the fp32 W partials, finish (modulus, phi_F), and keep the phase of the final W
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
   float* a_lo = hyb ? a_hi : a_hi + CT * 128 * K2;         // hybrid: only A_lo in SMEM
   float* bst = tsa ? a_hi : a_lo + CT * 128 * K2;           // NS stages x STG floats
   float* red = bst + NS * STG;                              // [CT][KAP][128]
+  float* swt = red + CT * KAP * 128;                        // KAP <= 8: [8 epilogue warps][32 rows][KAP] phi_F weights
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
@@ -217,7 +219,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
           const uint32_t bytes = (uint32_t)(2 * kTcN * kc * 4);
           const int sg = r * NSr + stage;
           tc::mbar_wait(&empty[sg], ph ^ 1);
-          if (tc::elect_one()) {
+          if ((a.fexpt & 4) && gt > 1) {   // timing experiment: B images of the first tiles only
+            if (tc::elect_one()) tc::mbar_arrive(&full[sg]);
+          } else if (tc::elect_one()) {
             tc::mbar_expect_tx(&full[sg], bytes);
             tc::bulk_g2s(bst + sg * STG, src, bytes, &full[sg]);
           }
@@ -326,10 +330,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
 #pragma unroll
         for (int r = 0; r < KAP; ++r) oacc[m][r] = 0.f;
       for (int t = 0; t < tu.NT; ++t) {
-        // lane l holds the phi_F weights of row (t*64 + h*32 + l); broadcast by shuffles below
-        float wl[KAP];
+        // lane l stages the phi_F weights of row (t*64 + h*32 + l) in the warp's SMEM slab [row][KAP]; the math
+        // below reads a row's weights as broadcast vector loads (one LDS per 2-4 outputs instead of one SHFL
+        // per output). The previous tile's reads are done: same warp, program order, then __syncwarp.
+        float wl[KAP];   // KAP >= 16: kept in registers and broadcast by shuffles (the slab would cost stages)
 #pragma unroll
         for (int r = 0; r < KAP; ++r) wl[r] = (r < ro) ? __ldg(wt + r * ldw + t * kTcRows + h * 32 + lane) : 0.f;
+        if constexpr (KAP <= 8) {
+          __syncwarp();
+          float* my = swt + (e * 32 + lane) * KAP;
+          if constexpr (KAP >= 4) {
+#pragma unroll
+            for (int r = 0; r < KAP; r += 4)
+              *reinterpret_cast<float4*>(my + r) = make_float4(wl[r], wl[r + 1], wl[r + 2], wl[r + 3]);
+          } else {
+            *reinterpret_cast<float2*>(my) = make_float2(wl[0], wl[1]);
+          }
+          __syncwarp();
+        }
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
         if (warp == 4 && lane == 0) TC_TRACE(5, ge);
@@ -408,12 +426,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
             }
             if (!(pmode & kPmFinish)) continue;
           }
+          if (a.fexpt & 8) {   // timing experiment: no modulus / phi_F math
+#pragma unroll
+            for (int r = 0; r < KAP; ++r) oacc[m][r] += v[r];
+            continue;
+          }
+          const float* sw = swt + e * 32 * KAP;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float mod = tc::sqrt_approx(fmaf(v[2 * i], v[2 * i], v[2 * i + 1] * v[2 * i + 1]));
 #pragma unroll
             for (int r = 0; r < KAP; r += 2) {   // outputs r, r + 1 as one packed FMA (FFMA2, bit-identical)
-              const float2 w2 = make_float2(__shfl_sync(0xffffffffu, wl[r], i), __shfl_sync(0xffffffffu, wl[r + 1], i));
+              float2 w2;
+              if constexpr (KAP > 8) {
+                w2 = make_float2(__shfl_sync(0xffffffffu, wl[r], i), __shfl_sync(0xffffffffu, wl[r + 1], i));
+              } else if constexpr (KAP >= 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(sw + i * KAP + (r & ~3));   // broadcast
+                w2 = (r & 2) ? make_float2(w4.z, w4.w) : make_float2(w4.x, w4.y);
+              } else {
+                w2 = *reinterpret_cast<const float2*>(sw + i * KAP);
+              }
               const float2 o2 = tc::fma2(w2, make_float2(mod, mod), make_float2(oacc[m][r], oacc[m][r + 1]));
               oacc[m][r] = o2.x;
               oacc[m][r + 1] = o2.y;
@@ -455,7 +487,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_joint_fwd_tc(TcArgs a, int NS
 
 static size_t tc_fwd_smem(int CT, int KAP, int NS, int K2, int STG, bool hyb = false) {
   const size_t a = hyb ? (size_t)128 * K2 : (tc_fwd_tsa(CT, K2) ? 0 : (size_t)2 * CT * 128 * K2);
-  return (a + NS * STG + CT * KAP * 128) * 4 + 1024;
+  return (a + NS * STG + CT * KAP * 128 + (KAP <= 8 ? 8 * 32 * KAP : 0)) * 4 + 1024;
 }
 
 // forward B ring stages that fit (the planner rejects chunk widths that leave fewer than 3; 2 in hybrid mode)

@@ -1,0 +1,7 @@
+# forward epilogue: phi_F weights as SMEM broadcast loads (KAP <= 8) instead of shuffles; parity + timing
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_large.py tests/test_gpu_tc.py -m gpu -q -rf -k "not c5 and not c4-b0" 2>&1 | tail -4 > gpurun_out/aa_tests.txt
+for c in c4 c2 c4 c2; do
+  timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-forward --no-e2e 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['ms_per_step'],2), d['clocks']['sm_mhz'], round(d['path_roofline']['rest_ms_measured'],2), d['config']['micro_batch'], {k:(round(v['ms_per_step'],1), round(v['frac'],3)) for k,v in d['roofline']['joint_kernels'].items()})"
+done > gpurun_out/aa_ab.txt 2>&1
