@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
   constexpr bool kCanT = sizeof(TO) == 8;
   __shared__ TO stg[kCanT ? kGatherTileT : 1];
   const int64_t L1t = J.L_out >> 12;
+  const int lgL1t = J.tl ? 63 - __clzll(L1t) : 0;   // L1t: power of two (shifts, not 64-bit divides)
   for (int64_t m = m0 + threadIdx.x; m < J.L_out && m < m0 + tsz; m += kGatherThreads) {
     // L_in, L_out: powers of two (grid lengths N_pad >> k)
     int64_t s = J.lo + ((m - J.lo) & (J.L_out - 1));          // smallest s >= lo with s = m mod L_out
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
       ay += h * vy;
     }
     if (kCanT && J.tl) {
-      const int64_t ml = m - m0, kk = ml / L1t, k1 = ml & (L1t - 1);
+      const int ml = (int)(m - m0), kk = ml >> lgL1t, k1 = ml & ((int)L1t - 1);
       st_c(stg + kk * L1t + (k1 ^ (kk & (L1t - 1))), (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
     } else {
       st_c(out + b * out_sb + J.out_off + m, (double)(ax * (R)J.scale), (double)(ay * (R)J.scale));
@@ -95,11 +96,11 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const TI* __restrict_
   }
   if (kCanT && J.tl) {
     __syncthreads();
-    const int64_t W = kGatherTileT / L1t;
-    TO* dst = out + b * out_sb + J.out_off + m0 / L1t;
+    const int lgW = 12 - lgL1t;                      // W = 4096 / L1t
+    TO* dst = out + b * out_sb + J.out_off + (m0 >> lgL1t);
     for (int i = threadIdx.x; i < kGatherTileT; i += kGatherThreads) {
-      const int64_t k1 = i / W, kk = i & (W - 1);
-      dst[(k1 << 12) + kk] = stg[kk * L1t + (k1 ^ (kk & (L1t - 1)))];
+      const int k1 = i >> lgW, kk = i & ((1 << lgW) - 1);
+      dst[((int64_t)k1 << 12) + kk] = stg[(kk << lgL1t) + (k1 ^ (kk & ((int)L1t - 1)))];
     }
   }
 }
@@ -291,41 +292,48 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
   // Summation order per element: phi_T term, then blocks ascending (as in the natural-layout loop).
   constexpr int kR = kU1AdjTile / 256;
   __shared__ float2 stg[2][kU1AdjTile];
-  const int64_t mt0 = (tile - tiles[n1]) * kU1AdjTile;
+  // within-row indices fit 32 bits (rows <= 2^22 points); powers of two divide by shifts
+  const int L1m = (int)L1 - 1;
+  const int mt0 = (int)((tile - tiles[n1]) * kU1AdjTile);
+  const float2* gsrow = GS + b * GS_sb + (int64_t)n1 * Ft;
+  const int Ftm = (int)Ft - 1;
   float2 acc[kR];
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
-    const int64_t m = mt0 + threadIdx.x + 256 * r;
+    const int m = mt0 + threadIdx.x + 256 * r;
     acc[r] = make_float2(0.f, 0.f);
-    const int64_t t = (m - spT.lo) & (L1 - 1);                 // L1, Ft, T2: powers of two
-    if (m < L1 && t < spT.len) {
+    const int t = (m - (int)spT.lo) & L1m;
+    if (m <= L1m && t < (int)spT.len) {
       float h = __ldg(vals + spT.off + t);
-      float2 v = GS[b * GS_sb + (int64_t)n1 * Ft + (m & (Ft - 1))];
+      float2 v = gsrow[m & Ftm];
       acc[r] = make_float2(h * v.x, h * v.y);
     }
   }
   int sb = 0;
   for (int i = 0; i < nb; ++i) {
-    const int64_t T2 = s_T2[i];
-    const int64_t d0 = (mt0 - s_lo[i]) & (L1 - 1);
-    if (s_len[i] <= 0 || (d0 >= s_len[i] && d0 + kU1AdjTile <= L1)) continue;   // CTA-uniform: no overlap
+    const int T2 = (int)s_T2[i], lo = (int)s_lo[i], len = (int)s_len[i];
+    const int d0 = (mt0 - lo) & L1m;
+    if (len <= 0 || (d0 >= len && d0 + kU1AdjTile <= L1m + 1)) continue;   // CTA-uniform: no overlap
     const float2* gy = GY + b * GY_sb + s_y[i];
+    const float* hv = vals + s_off[i];
     if (T2 > 4096) {
-      const int64_t L1b = T2 >> 12, Wb = kU1AdjTile / L1b, mm0 = mt0 & (T2 - 1);
-      const float2* src = gy + mm0 / L1b;
+      const int lgL1b = __ffs(T2) - 1 - 12, L1b = 1 << lgL1b;      // L1b = T2 / 4096
+      const int lgWb = 10 - lgL1b;                                  // Wb = 1024 / L1b
+      const int mm0 = mt0 & (T2 - 1);
+      const float2* src = gy + (mm0 >> lgL1b);
       for (int e = threadIdx.x; e < kU1AdjTile; e += 256) {
-        const int64_t kq = e / Wb, kk = e & (Wb - 1);
-        stg[sb][kk * L1b + (kq ^ (kk & (L1b - 1)))] = src[(kq << 12) + kk];
+        const int kq = e >> lgWb, kk = e & ((1 << lgWb) - 1);
+        stg[sb][(kk << lgL1b) + (kq ^ (kk & (L1b - 1)))] = src[((int64_t)kq << 12) + kk];
       }
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
-        const int64_t m = mt0 + threadIdx.x + 256 * r;
-        const int64_t t = (m - s_lo[i]) & (L1 - 1);
-        if (m < L1 && t < s_len[i]) {
-          const int64_t ml = threadIdx.x + 256 * r, kk = ml / L1b, kq = ml & (L1b - 1);
-          const float h = __ldg(vals + s_off[i] + t);
-          const float2 v = stg[sb][kk * L1b + (kq ^ (kk & (L1b - 1)))];
+        const int m = mt0 + threadIdx.x + 256 * r;
+        const int t = (m - lo) & L1m;
+        if (m <= L1m && t < len) {
+          const int ml = threadIdx.x + 256 * r, kk = ml >> lgL1b, kq = ml & (L1b - 1);
+          const float h = __ldg(hv + t);
+          const float2 v = stg[sb][(kk << lgL1b) + (kq ^ (kk & (L1b - 1)))];
           acc[r].x = fmaf(h, v.x, acc[r].x);
           acc[r].y = fmaf(h, v.y, acc[r].y);
         }
@@ -334,10 +342,10 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
     } else {
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
-        const int64_t m = mt0 + threadIdx.x + 256 * r;
-        const int64_t t = (m - s_lo[i]) & (L1 - 1);
-        if (m < L1 && t < s_len[i]) {
-          const float h = __ldg(vals + s_off[i] + t);
+        const int m = mt0 + threadIdx.x + 256 * r;
+        const int t = (m - lo) & L1m;
+        if (m <= L1m && t < len) {
+          const float h = __ldg(hv + t);
           const float2 v = gy[m & (T2 - 1)];
           acc[r].x = fmaf(h, v.x, acc[r].x);
           acc[r].y = fmaf(h, v.y, acc[r].y);
@@ -345,10 +353,11 @@ __global__ void __launch_bounds__(256) k_adj_gather_u1(
       }
     }
   }
+  float2* orow = out + b * out_sb + l1_off[n1];
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
-    const int64_t m = mt0 + threadIdx.x + 256 * r;
-    if (m < L1) out[b * out_sb + l1_off[n1] + m] = acc[r];
+    const int m = mt0 + threadIdx.x + 256 * r;
+    if (m <= L1m) orow[m] = acc[r];
   }
 }
 
