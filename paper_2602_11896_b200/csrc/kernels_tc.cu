@@ -597,7 +597,11 @@ template <int KAP>
 __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int NS1, int STG1, int NS2, int STG2) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t full1[kTcMaxStages], empty1[kTcMaxStages], full2[kTcMaxStages2], empty2[kTcMaxStages2];
-  __shared__ uint64_t tfull[2], tempty[2], a2full[2], a2empty[2], d2full;
+  // tile barriers in one struct: the epilogue addresses them from one base register (see eb below)
+  __shared__ struct { uint64_t tfull[2], tempty[2], a2full[2], a2empty[2], d2full; } tb_;
+  uint64_t* const tfull = tb_.tfull; uint64_t* const tempty = tb_.tempty;
+  uint64_t* const a2full = tb_.a2full; uint64_t* const a2empty = tb_.a2empty;
+  uint64_t& d2full = tb_.d2full;
   __shared__ uint32_t tmem_base;
   // logical warp roles: 0/2 producers, 1/3 MMA issuers, 4.. epilogue (epilogue on the low physical warps so
   // the producers and issuers get the higher, favoured warp ids; see the forward kernel)
@@ -838,6 +842,11 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     int buf = 0;
     uint32_t bph = 0;
     int g = 0;
+    // shared-window address of tb_ kept opaque in one register: tfull +0, tempty +16, a2full +32, a2empty +48
+    // (the compiler otherwise re-derives each barrier's address from SR_CgaCtaId at every use: ~5
+    // instructions and an S2R latency per barrier operation, four operations per tile and warp)
+    uint32_t eb = tc::smem_u32(&tb_);
+    asm volatile("" : "+r"(eb));
     // phi_F weights and g_o are prefetched one tile ahead (their L2 latency would otherwise sit on the
     // epilogue's critical path every tile)
     auto next_unit = [&](int f) {
@@ -933,7 +942,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           if (ksm) load_wv(TB.bi * a.nfr + fn, 0, wv_n);
         }
         if (!ksm) {
-          tc::mbar_wait(&tfull[buf], bph);
+          tc::mbar_wait_a(eb + 8u * buf, bph);
           tc::tc_fence_after();
           if (warp == 4 && lane == 0) TC_TRACE(5, g);
           const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 2 * kBwRpw);
@@ -941,7 +950,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           tc::tmem_wait_ld();
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+          if (lane == 0) tc::mbar_arrive_a(eb + 16u + 8u * buf);
           if (++buf == 2) { buf = 0; bph ^= 1; }
         }
         float ghi[2 * kBwRpw], glo[2 * kBwRpw];
@@ -949,17 +958,20 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
 #pragma unroll
           for (int i = 0; i < 2 * kBwRpw; ++i) ghi[i] = glo[i] = v[i] * 0.f;
         } else
+        {
+        // g_W = (W/|W|) Phi_F^T g_o (Eq.4 adjoint, modulus adjoint with the R22 dead zone); the split-K test sits
+        // outside the unrolled row loop (one uniform branch per tile instead of one per row)
+        if (!ksm) {                                      // split-K: (re, im) is already the phase (or 0)
+#pragma unroll
+          for (int i = 0; i < kBwRpw; ++i) {
+            const float m2 = fmaf(v[2 * i], v[2 * i], v[2 * i + 1] * v[2 * i + 1]);
+            gv[i] = m2 > th2 ? gv[i] * tc::rsqrt_approx(m2) : 0.f;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < kBwRpw; ++i) {
-          // g_W = (W/|W|) Phi_F^T g_o (Eq.4 adjoint, modulus adjoint with the R22 dead zone)
           const float re = v[2 * i], im = v[2 * i + 1];
-          float s;
-          if (ksm) {
-            s = gv[i];                                   // (re, im) is already the phase (or 0)
-          } else {
-            const float m2 = fmaf(re, re, im * im);
-            s = m2 > th2 ? gv[i] * tc::rsqrt_approx(m2) : 0.f;
-          }
+          const float s = gv[i];
           // (re, im) s and the lo halves as packed pairs (FMUL2 / FADD2); hi rounded on the integer pipe
           const float2 g2 = tc::mul2(make_float2(re, im), make_float2(s, s));
           const float2 h2 = make_float2(tc::tf32_rna(g2.x), tc::tf32_rna(g2.y));
@@ -967,11 +979,12 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           ghi[2 * i] = h2.x; ghi[2 * i + 1] = h2.y;
           glo[2 * i] = l2.x; glo[2 * i + 1] = l2.y;
         }
+        }
         // A2 buffer ab (TMEM) is free once the GEMM2 that last read it completed
         if (warp == 4 && lane == 0) TC_TRACE(6, g);
         const int ab = nab == 2 ? (g & 1) : 0;
         const uint32_t ta2_hi = ta2 + 128u * ab, ta2_lo = ta2_hi + 64u;
-        tc::mbar_wait(&a2empty[ab], (uint32_t)(((nab == 2 ? (g >> 1) : g) & 1) ^ 1));
+        tc::mbar_wait_a(eb + 48u + 8u * ab, (uint32_t)(((nab == 2 ? (g >> 1) : g) & 1) ^ 1));
         tc::tc_fence_after();
         if (warp == 4 && lane == 0) TC_TRACE(7, g);
         tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 2 * kBwRpw), ghi);
@@ -979,7 +992,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&a2full[ab]);
+        if (lane == 0) tc::mbar_arrive_a(eb + 32u + 8u * ab);
         if (warp == 4 && lane == 0) TC_TRACE(8, g);
       }
       f = fn;

@@ -51,6 +51,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// the same on a precomputed shared-window address (hot loops keep one base address in a register instead of
+// re-deriving every barrier's address from SR_CgaCtaId per use)
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // polling variant (mbarrier.test_wait never suspends the thread): for the MMA issuers, whose waits sit
 // on the tensor pipe's critical path
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
