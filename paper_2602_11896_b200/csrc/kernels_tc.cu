@@ -847,25 +847,17 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     // instructions and an S2R latency per barrier operation, four operations per tile and warp)
     uint32_t eb = tc::smem_u32(&tb_);
     asm volatile("" : "+r"(eb));
-    // phi_F weights and g_o are prefetched one tile ahead (their L2 latency would otherwise sit on the
-    // epilogue's critical path every tile)
+    // g_o (and, split-K, the W phase) of the next tile / unit are loaded one tile ahead
     auto next_unit = [&](int f) {
       while (f < a.nfr && (!owns_block(a.own, TB.bi) || f % a.ng != grp)) ++f;
       return f;
     };
     // phi_F weights of this warp's 8 rows of tile t (row block of output r at + r * ldw): read as two
     // warp-uniform float4 loads per r (broadcast) and folded into g_W's row factors before the tile's W is
-    // waited for; the next tile's lines are prefetched into L1 one tile ahead
+    // waited for. (A register-less "prefetch" load of the next tile's lines is dropped by ptxas as dead code,
+    // and staging them in SMEM by cp.async a tile ahead measured slower: the extra instructions cost more than
+    // the L2 latency they hide.)
     auto wrow = [&](int u, int t) { return a.wts + a.tcu[u].wt_off + t * kBwRows + h * kBwRpw; };
-    auto pf_w = [&](int u, int t) {
-      if (lane < min(KAP, a.units[u].rows_out))
-      {
-        // a load whose register is never read: brings the sector into L1 without stalling the warp
-        // (prefetch.global.L1 did not hide the L2 latency of the row-factor loads)
-        float dead;
-        asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(dead) : "l"(wrow(u, t) + (int64_t)lane * a.tcu[u].NT * kTcRows));
-      }
-    };
     auto load_go = [&](int u, float* gor) {
       const JointUnit U = a.units[u];
 #pragma unroll
@@ -888,7 +880,6 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     float gor_n[KAP];
     uint4 wv_n[kBwRpw / 4];
     if (f < a.nfr) {
-      pf_w(TB.bi * a.nfr + f, 0);
       load_go(TB.bi * a.nfr + f, gor_n);
       if (ksm) load_wv(TB.bi * a.nfr + f, 0, wv_n);
     }
@@ -934,10 +925,8 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           }
         }
         if (t + 1 < NT32) {
-          pf_w(u, t + 1);
           if (ksm) load_wv(u, t + 1, wv_n);
         } else if (fn < a.nfr) {
-          pf_w(TB.bi * a.nfr + fn, 0);
           load_go(TB.bi * a.nfr + fn, gor_n);
           if (ksm) load_wv(TB.bi * a.nfr + fn, 0, wv_n);
         }
