@@ -39,7 +39,10 @@ constexpr int kTcThreads = 384;     // 12 warps
 constexpr int kTcMaxStages = 8;
 constexpr int kTcMaxStages2 = 16;   // backward ring 2 (B2 chunks)
 constexpr int kBwRows = 32;         // rows per backward tile (GEMM1 N = 64, GEMM2 K = 64)
-constexpr int kBwEpiWarps = 16;     // backward epilogue warps: 4 TMEM lane quadrants x 4 row groups
+#ifndef JTFS_BW_EPIW
+#define JTFS_BW_EPIW 16
+#endif
+constexpr int kBwEpiWarps = JTFS_BW_EPIW;   // backward epilogue warps: 4 TMEM lane quadrants x 4 (or 2) row groups
 constexpr int kBwRpw = kBwRows / (kBwEpiWarps / 4);            // rows per epilogue warp (8)
 constexpr int kBwThreads = 128 + 32 * kBwEpiWarps;             // + producers / MMA issuers (warps 0-3)
 constexpr int kBwN1 = 2 * kBwRows;
@@ -869,7 +872,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     // tile ahead; layout per (column tile, 64-row tile): [16-byte group][column], 2 x int16 per cell, row r in
     // group (r / 32) * wph / 256 + (r % 32) / 4
     const uint4* wcol = ksm ? reinterpret_cast<const uint4*>(a.wbuf + b * a.wb_sb + TB.wp_off) +
-                                  (int64_t)ct * TB.wp_tiles * TB.wph + (h * 2) * 128 + c
+                                  (int64_t)ct * TB.wp_tiles * TB.wph + (h * (kBwRpw / 4)) * 128 + c
                             : nullptr;
     auto load_wv = [&](int u, int t32, uint4* wv) {
       const uint4* q4 = wcol + (int64_t)(a.tcu[u].wp_tile0 + (t32 >> 1)) * TB.wph + ((t32 & 1) * (TB.wph >> 8)) * 128;
@@ -902,12 +905,12 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
 #pragma unroll
           for (int r = 0; r < KAP; ++r) {
             if (r < U.rows_out) {
-              const float4 w0 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)r * ldw));
-              const float4 w1 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)r * ldw) + 1);
-              gv[0] = fmaf(w0.x, gor[r], gv[0]); gv[1] = fmaf(w0.y, gor[r], gv[1]);
-              gv[2] = fmaf(w0.z, gor[r], gv[2]); gv[3] = fmaf(w0.w, gor[r], gv[3]);
-              gv[4] = fmaf(w1.x, gor[r], gv[4]); gv[5] = fmaf(w1.y, gor[r], gv[5]);
-              gv[6] = fmaf(w1.z, gor[r], gv[6]); gv[7] = fmaf(w1.w, gor[r], gv[7]);
+#pragma unroll
+              for (int j = 0; j < kBwRpw / 4; ++j) {
+                const float4 w0 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)r * ldw) + j);
+                gv[4 * j] = fmaf(w0.x, gor[r], gv[4 * j]); gv[4 * j + 1] = fmaf(w0.y, gor[r], gv[4 * j + 1]);
+                gv[4 * j + 2] = fmaf(w0.z, gor[r], gv[4 * j + 2]); gv[4 * j + 3] = fmaf(w0.w, gor[r], gv[4 * j + 3]);
+              }
             }
           }
         }
@@ -935,7 +938,8 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           tc::tc_fence_after();
           if (warp == 4 && lane == 0) TC_TRACE(5, g);
           const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 2 * kBwRpw);
-          tc::tmem_ld16_nowait(ta, v);
+#pragma unroll
+          for (int j = 0; j < kBwRpw / 8; ++j) tc::tmem_ld16_nowait(ta + 16u * j, v + 16 * j);
           tc::tmem_wait_ld();
           tc::tc_fence_before();
           __syncwarp();
@@ -976,8 +980,11 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         tc::mbar_wait_a(eb + 48u + 8u * ab, (uint32_t)(((nab == 2 ? (g >> 1) : g) & 1) ^ 1));
         tc::tc_fence_after();
         if (warp == 4 && lane == 0) TC_TRACE(7, g);
-        tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 2 * kBwRpw), ghi);
-        tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 2 * kBwRpw), glo);
+#pragma unroll
+        for (int j = 0; j < kBwRpw / 8; ++j) {
+          tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 2 * kBwRpw + 16 * j), ghi + 16 * j);
+          tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 2 * kBwRpw + 16 * j), glo + 16 * j);
+        }
         tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
