@@ -842,6 +842,9 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
     const int64_t colg = col0 + c;
     const float th2 = fmaxf(a.thr[b] * a.thr[b], 1.17549435e-38f);   // R22 dead zone (and |w|^2 > FLT_MIN)
     const uint32_t lq = (uint32_t)(q * 32) << 16;
+    // this warp's TMEM lane quadrant + column offset of its rows, opaque (not re-derived from SR_TID per tile)
+    uint32_t lqh = lq + (uint32_t)(h * 2 * kBwRpw);
+    asm volatile("" : "+r"(lqh));
     int buf = 0;
     uint32_t bph = 0;
     int g = 0;
@@ -895,11 +898,12 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
       const int NT32 = (int)((U.n_rows + kBwRows - 1) / kBwRows);
       const int fn = next_unit(f + 1);
       const int ldw = a.tcu[u].NT * kTcRows;
+      const float* wbase = wrow(u, 0);   // per unit: no dependent offset load per tile
       for (int t = 0; t < NT32; ++t, ++g) {
         // gv[i] = (Phi_F^T g_o)[row i] for this column (Eq. 4 adjoint)
         float gv[kBwRpw];
         {
-          const float* wr = wrow(u, t);
+          const float* wr = wbase + t * kBwRows;
 #pragma unroll
           for (int i = 0; i < kBwRpw; ++i) gv[i] = 0.f;
 #pragma unroll
@@ -937,7 +941,7 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
           tc::mbar_wait_a(eb + 8u * buf, bph);
           tc::tc_fence_after();
           if (warp == 4 && lane == 0) TC_TRACE(5, g);
-          const uint32_t ta = tbase + lq + (uint32_t)(buf * kBwN1 + h * 2 * kBwRpw);
+          const uint32_t ta = tbase + lqh + (uint32_t)(buf * kBwN1);
 #pragma unroll
           for (int j = 0; j < kBwRpw / 8; ++j) tc::tmem_ld16_nowait(ta + 16u * j, v + 16 * j);
           tc::tmem_wait_ld();
@@ -982,8 +986,8 @@ __global__ void __launch_bounds__(kBwThreads, 1) k_joint_bwd_tc(TcBwArgs a, int 
         if (warp == 4 && lane == 0) TC_TRACE(7, g);
 #pragma unroll
         for (int j = 0; j < kBwRpw / 8; ++j) {
-          tc::tmem_st16(ta2_hi + lq + (uint32_t)(h * 2 * kBwRpw + 16 * j), ghi + 16 * j);
-          tc::tmem_st16(ta2_lo + lq + (uint32_t)(h * 2 * kBwRpw + 16 * j), glo + 16 * j);
+          tc::tmem_st16(ta2_hi + lqh + (uint32_t)(16 * j), ghi + 16 * j);
+          tc::tmem_st16(ta2_lo + lqh + (uint32_t)(16 * j), glo + 16 * j);
         }
         tc::tmem_wait_st();
         tc::tc_fence_before();
